@@ -1,0 +1,428 @@
+#!/usr/bin/env python
+"""DyLLM generation throughput on B200 — the BASELINE.json metric.
+
+One bench STEP = one complete generation (Alg. 1: T_total = L_R / n_u denoising steps, the
+4 FullSteps included, LM head + unmasking every step) of the per-GPU batch at the LLaDA-8B
+shape (32 layers, d=4096, 32 heads, FFN 12288, vocab 126464) with L_P=700 (GSM8K-5-shot
+length), L_R=256, block 32, n_u=1, batch 16 per GPU. Weights: random init on the device
+(IH4 generator, std 0.02). Inputs: synthetic uniform prompt ids (synth/gen.py).
+
+value  : tokens/s = (ranks x batch x L_R x K) / (max over ranks of the device time of K
+         generations), prompts already in HBM.
+e2e    : the same through the public Engine.generate API with the prompt H2D copy from pinned
+         memory and the D2H read of the generated tokens inside the timed region.
+Saliency threshold: per-layer tau calibrated on the first sparse steps to a target salient
+fraction (random-init models have degenerate similarity distributions); the
+achieved fraction over the run is reported.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tokens/sec at LLaDA-8B shape bs=16 (1/2/4/8 B200); salient-step % of roofline"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="llada8b")
+    ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (0 = config)")
+    ap.add_argument("--frac", type=float, default=0.10, help="target salient fraction for tau calibration")
+    ap.add_argument("--tau", type=float, default=None, help="fixed tau for all layers (skips calibration)")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--profile-steps", type=int, default=1, help="extra untimed generations with per-kernel events")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        load = [s for s in sm if mx and s > 0.3 * mx] or sm
+        return {"sm_mhz": float(np.median(load)) if load else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def layer_bytes_flops(cfg):
+    d, qw, kw, F = cfg.d_model, cfg.q_width, cfg.kv_width, cfg.d_ff
+    return {"qkv_w": 2 * d * (qw + 2 * kw), "o_w": 2 * d * qw, "gu_w": 2 * d * 2 * F, "down_w": 2 * d * F}
+
+
+# ----------------------------------------------------------------------------- CPU oracle leg
+def cpu_oracle_sample(cfg, run, seconds: float, frac: float, seed: int = 0):
+    """Time the oracle (as it stands) on one sequence of the bench workload: one response-only
+    sparse layer, one full-input sparse layer and one FullStep layer at the calibrated fraction,
+    extrapolated to the whole generation with the Alg. 1 step mix (labelled extrapolated)."""
+    import oracle as O
+    from synth import gen
+    t0 = time.time()
+    W = gen.layer_weights(cfg, seed, 0)
+    rng = np.random.default_rng(seed)
+    N, L_P = run.N, run.L_P
+    x_all = rng.standard_normal((N, cfg.d_model)) * 0.02
+    base = O.full_layer(x_all, W, cfg)                                  # cache state (untimed)
+    setup = time.time() - t0
+    timings = {}
+
+    def sparse(mode):
+        rows = np.arange(N) if mode == "fi" else np.arange(L_P, N)
+        idx = np.sort(rng.choice(rows, max(1, int(frac * len(rows))), replace=False))
+        x2 = x_all.copy()
+        x2[idx] += rng.standard_normal((len(idx), cfg.d_model)) * 0.02
+        lc = base.copy()
+        r = O.sparse_layer(x2, lc, W, cfg, idx, 2.0, rows, q_mode="cache")
+        tau = float(np.quantile(r.s, frac))
+        lc = base.copy()
+        t = time.time()
+        O.sparse_layer(x2, lc, W, cfg, idx, tau, rows, q_mode="cache")
+        return time.time() - t
+
+    timings["ro"] = sparse("ro")
+    timings["fi"] = sparse("fi")
+    t = time.time()
+    if timings["ro"] + timings["fi"] < seconds:
+        O.full_layer(x_all, W, cfg)
+        timings["full"] = time.time() - t
+    else:                                                               # bounded: scale by FLOPs
+        timings["full"] = timings["fi"] / max(frac, 1e-3)
+    T = run.T_total
+    n_full = min(run.T_full, T)
+    n_fi = sum(1 for t_ in range(n_full, T) if t_ % run.full_period == 0)
+    n_ro = T - n_full - n_fi
+    per_seq = cfg.n_layers * (n_full * timings["full"] + n_fi * timings["fi"] + n_ro * timings["ro"])
+    tok_s = run.L_R / per_seq
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count()
+    return {
+        "value": tok_s, "unit": UNIT, "cores": cores, "kind": "oracle",
+        "sample": (f"oracle fp64 NumPy on one sequence: one RO sparse layer ({timings['ro']:.2f}s), one FI "
+                   f"sparse layer ({timings['fi']:.2f}s), one FullStep layer ({timings['full']:.2f}s) at "
+                   f"salient fraction {frac}; extrapolated x{cfg.n_layers} layers x ({n_full} full, {n_fi} FI, "
+                   f"{n_ro} RO) steps, LM head excluded; setup {setup:.1f}s untimed"),
+        "extrapolated": True,
+    }
+
+
+def run_reference(args):
+    from synth import configs
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg, run = configs.preset(args.config)
+    vals = []
+    for _ in range(args.warmup + args.steps):
+        vals.append(cpu_oracle_sample(cfg, run, args.cpu_seconds / 4, args.frac))
+    v = float(np.mean([x["value"] for x in vals[args.warmup:]])) if args.steps else vals[-1]["value"]
+    base = vals[-1]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * run.L_R / v,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": f"{args.config} oracle sample", "batch": 1},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": base["cores"], "kind": "oracle",
+                         "sample": base["sample"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def calibrate_tau(eng, dy, cfg, run, frac, n_sparse=2):
+    """Per-layer tau_l = frac-quantile of s over the input rows, layer by layer in order, on the
+    first n_sparse sparse steps (the last one's values are kept). Uses only the public ABI:
+    snapshot layer caches, layer_step(tau=-2) to read s, restore, layer_step(tau_l)."""
+    import torch
+    N, b = run.N, run.batch
+    cache = eng.cache
+    dev = eng.tokens.device
+    taus = np.full(cfg.n_layers, 0.999, dtype=np.float32)
+    eng.tokens[:, run.L_P:].fill_(cfg.mask_id)
+    for t in range(run.T_full):
+        cache.denoise_step(t, taus, eng.tokens, eng.dec_pos, eng.dec_tok)
+    carried = None
+    idx_o = torch.zeros(b * N, dtype=torch.int32, device=dev)
+    off_o = torch.zeros(b + 1, dtype=torch.int32, device=dev)
+    sim = torch.zeros(b * N, dtype=torch.float32, device=dev)
+    fracs = []
+    for t in range(run.T_full, run.T_full + n_sparse):
+        row_lo = 0 if t % run.full_period == 0 else run.L_P
+        torch.cuda.synchronize()
+        dec = eng.dec_pos.cpu().numpy()
+        lists = []
+        for s in range(b):
+            base_set = set(range(run.L_P, N)) if carried is None else set(carried[s])
+            base_set |= set(int(r) - s * N for r in dec[s] if r >= 0)
+            lists.append(sorted(p for p in base_set if p >= row_lo))
+        rows = [s * N + p for s in range(b) for p in lists[s]]
+        off = np.cumsum([0] + [len(l) for l in lists])
+        idx_i = torch.zeros(b * N, dtype=torch.int32, device=dev)
+        idx_i[: len(rows)] = torch.tensor(rows, dtype=torch.int32, device=dev)
+        off_i = torch.tensor(off, dtype=torch.int32, device=dev)
+        layer_fr = []
+        for l in range(cfg.n_layers):
+            snap = [cache.tensor(l, w).clone() for w in (dy.K, dy.V, dy.Q, dy.CTX)] + [cache.tensor(l + 1, dy.H).clone()]
+            cache.layer_step(l, 0 if row_lo == 0 else 1, idx_i, off_i, -2.0, idx_o, off_o, sim)
+            torch.cuda.synchronize()
+            s_in = sim.view(b, N)[:, row_lo:].cpu().numpy().ravel()
+            taus[l] = np.float32(np.quantile(s_in, frac))
+            for tsr, w in zip(snap[:4], (dy.K, dy.V, dy.Q, dy.CTX)):
+                cache.tensor(l, w).copy_(tsr)
+            cache.tensor(l + 1, dy.H).copy_(snap[4])
+            cache.layer_step(l, 0 if row_lo == 0 else 1, idx_i, off_i, float(taus[l]), idx_o, off_o, sim)
+            torch.cuda.synchronize()
+            layer_fr.append(int(off_o[-1]) / (b * (N - row_lo)))
+            idx_i, off_i = idx_o.clone(), off_o.clone()
+        fracs.append(layer_fr)
+        o = off_i.cpu().numpy()
+        r = idx_i.cpu().numpy()
+        carried = [list(r[o[s]:o[s + 1]] - s * N) for s in range(b)]
+        cache.set_carried(idx_i, off_i)
+        cache.unmask(eng.tokens, eng.dec_pos, eng.dec_tok)
+    torch.cuda.synchronize()
+    return taus, fracs
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+    from dataclasses import replace
+
+    from synth import configs, gen
+    from paper_2603_08026_b200 import dyllm as dy
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    cfg, run = configs.preset(args.config)
+    if args.batch:
+        run = replace(run, batch=args.batch)
+    b, N = run.batch, run.N
+
+    ctx = dy.Context(local)
+    w = dy.Weights.random(ctx, cfg, seed=args.seed)
+    eng = dy.Engine(ctx, w, run)
+    # per-rank shard of the global batch: sequences [rank*b, (rank+1)*b) of the synthetic set
+    prompts_all = gen.prompt_tokens(args.seed + 1000 * rank, b, run.L_P, cfg.mask_id)
+    prompts_dev = torch.tensor(prompts_all, dtype=torch.int32, device=f"cuda:{local}")
+    prompts_host = torch.tensor(prompts_all, dtype=torch.int32).pin_memory()
+    out_host = torch.empty((b, N), dtype=torch.int32).pin_memory()
+
+    # ---- tau calibration (untimed)
+    eng.tokens[:, : run.L_P].copy_(prompts_dev)
+    if args.tau is None:
+        taus, cal_fracs = calibrate_tau(eng, dy, cfg, run, args.frac)
+    else:
+        taus, cal_fracs = np.full(cfg.n_layers, args.tau, np.float32), []
+
+    stream = ctx.stream
+
+    def one_generation():
+        eng.tokens[:, : run.L_P].copy_(prompts_dev, non_blocking=True)
+        eng.tokens[:, run.L_P:].fill_(cfg.mask_id)
+        eng.run_steps(taus)
+
+    for _ in range(args.warmup):
+        one_generation()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    l0 = dy.lib().dyllm_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        one_generation()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    launches = (dy.lib().dyllm_launch_count() - l0) // max(args.steps, 1)
+    ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    sal = eng.sal_counts.cpu().numpy()                   # [T][n_layers][b] of the last generation
+    if world > 1:
+        dist.barrier()
+    # ---- e2e through the public API (pinned H2D prompts, D2H tokens)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        eng.generate(prompts_host, taus, out_host=out_host)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = e0.elapsed_time(e1)
+    # ---- per-kernel events (separate untimed generation, same workload)
+    ctx.profile(True)
+    for _ in range(args.profile_steps):
+        one_generation()
+    torch.cuda.synchronize()
+    kc = {}
+    names = ["qkv_gemm", "qkv_post", "attn", "select", "o_gemm", "gu_gemm", "down_gemm", "gather", "scatter",
+             "lm_gemm", "other"]
+    for i, n in enumerate(names):
+        kc[n] = ctx.profile_read(i)
+        kc["full_" + n] = ctx.profile_read(16 + i)
+    ctx.profile(False)
+    sal_prof = eng.sal_counts.cpu().numpy()
+
+    # ---- max over ranks
+    t_dev = torch.tensor([ms, ms_e2e], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
+    ms, ms_e2e = t_dev.tolist()
+    tokens = world * b * run.L_R * args.steps
+    value = tokens / (ms / 1000.0)
+    e2e = tokens / (ms_e2e / 1000.0)
+
+    if rank == 0:
+        hbm, tf_burst, tf_sus, src = peaks()
+        T = run.T_total
+        sparse_t = [t for t in range(T) if t >= run.T_full]
+        in_rows = np.array([b * (N if t % run.full_period == 0 else run.L_R) for t in sparse_t], dtype=np.float64)
+        sel = sal_prof[sparse_t].sum(axis=2).astype(np.float64)        # [steps][layers] selected rows
+        f_layer = (sel / in_rows[:, None]).mean(axis=0)
+        # dominant kernel of the timed workload = the class with the largest total event time
+        totals = {k: float(v.sum()) for k, v in kc.items() if len(v)}
+        dom = max(totals, key=totals.get)
+        lb = layer_bytes_flops(cfg)
+        # algorithmic bytes / flops per launch for the sparse-step GEMMs (M = rows of the launch)
+        d, F, qw, kw = cfg.d_model, cfg.d_ff, cfg.q_width, cfg.kv_width
+        m_out = sel.ravel()                                           # launch order: step-major, layer-minor
+        m_in_layers = np.concatenate([[0], np.zeros(0)])
+        roof = None
+        if dom in ("gu_gemm", "down_gemm", "o_gemm"):
+            wbytes = {"gu_gemm": lb["gu_w"], "down_gemm": lb["down_w"], "o_gemm": lb["o_w"]}[dom]
+            act = {"gu_gemm": (2 * d + 2 * F), "down_gemm": (2 * F + 4 * d), "o_gemm": (2 * qw + 4 * d)}[dom]
+            flop = {"gu_gemm": 2 * d * 2 * F, "down_gemm": 2 * F * d, "o_gemm": 2 * qw * d}[dom]
+            times = kc[dom] / 1000.0
+            n = min(len(times), len(m_out))
+            byts = wbytes + act * m_out[:n]
+            flops = flop * m_out[:n]
+            t_hbm = byts / (hbm * 1e9)
+            t_tc = flops / (tf_sus * 1e12)
+            bound = "hbm" if t_hbm.sum() >= t_tc.sum() else "tensor"
+            if bound == "hbm":
+                ach = byts.sum() / times[:n].sum() / 1e9
+                roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm}
+            else:
+                ach = flops.sum() / times[:n].sum() / 1e12
+                roof = {"bound": "tensor", "achieved": ach, "peak": tf_sus, "unit": "TFLOP/s", "frac": ach / tf_sus}
+        elif dom.startswith("full_") and dom.endswith("gemm"):
+            k = dom[5:]
+            Mrows = b * N
+            flop = {"qkv_gemm": 2 * d * (qw + 2 * kw), "o_gemm": 2 * qw * d, "gu_gemm": 4 * d * F,
+                    "down_gemm": 2 * F * d, "lm_gemm": 2 * d * cfg.vocab}[k] * Mrows
+            ach = flop * len(kc[dom]) / (kc[dom].sum() / 1000.0) / 1e12
+            roof = {"bound": "tensor", "achieved": ach, "peak": tf_sus, "unit": "TFLOP/s", "frac": ach / tf_sus}
+        if roof is None:
+            roof = {"bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None}
+        roof.update({"kernel": dom, "traffic": None, "peak_source": src + (" sustained" if roof["unit"] == "TFLOP/s" else ""),
+                     "launches_timed": int(len(kc[dom])), "avg_launch_us": float(kc[dom].mean() * 1000.0)})
+        share = {k: round(v / sum(totals.values()), 4) for k, v in sorted(totals.items(), key=lambda x: -x[1])}
+        # per-mode step times from the profiled generation are in `share`; full-recompute extrapolation
+        full_ms = sum(float(v.sum()) for k, v in kc.items() if k.startswith("full_")) / max(run.T_full, 1)
+        full_tok_s = b * run.L_R / (T * full_ms / 1000.0) * world if full_ms > 0 else None
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            cpu = cpu_oracle_sample(cfg, run, args.cpu_seconds, args.frac)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{args.config}: L_P={run.L_P} L_R={run.L_R} block={run.block} "
+                                   f"n_u={run.n_u} T={T} (T_full={run.T_full}, period={run.full_period}) "
+                                   f"random-init bf16 weights, one step = one full generation",
+                       "global_batch": b * world, "per_gpu_batch": b, "seq_len": N,
+                       "parallelism": f"dp{world} (batch-parallel replicas)",
+                       "l2": "inputs larger than L2 (14 GB of weights streamed per denoising step)",
+                       "tau": "per-layer, calibrated to salient fraction %.2f" % args.frac if args.tau is None
+                       else args.tau},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(b * run.L_P * 4),
+                    "d2h_bytes_per_step": int(b * N * 4)},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "salient_fraction": {"per_layer_mean": [round(float(x), 4) for x in f_layer],
+                                 "run_mean": float(f_layer.mean()),
+                                 "calibration": [[round(x, 4) for x in fr] for fr in cal_fracs]},
+            "kernel_time_share": share,
+            "full_recompute": {"ms_per_full_step": full_ms, "tokens_per_s_extrapolated": full_tok_s,
+                               "speedup": (value / full_tok_s) if full_tok_s else None},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

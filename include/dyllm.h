@@ -1,0 +1,202 @@
+/*
+ * dyllm.h — C ABI of libdyllm.so, the B200 (sm_100a) implementation of DyLLM's
+ * salient-token denoising step (arxiv 2603.08026).
+ *
+ * Citations: P:n = PAPER.md line n (in /root/reference, not shipped), S:n = SPEC.md
+ * line n, Dn = a reading in DESIGN.md §2.
+ *
+ * Conventions (apply to every call)
+ *  - Status: 0 = DYLLM_OK, > 0 informational, < 0 error. Nothing throws across the ABI.
+ *    dyllm_last_error() returns a thread-local message for the last failing call.
+ *  - Handles (dyllm_ctx / dyllm_weights / dyllm_cache) are library-owned: create/destroy pairs.
+ *  - `d_` pointers are caller-owned DEVICE memory on the ctx's device; `h_` pointers are host
+ *    memory. Caller buffers must stay valid until the ctx stream has passed the call.
+ *  - Every compute call is asynchronous on the ctx stream (no host synchronisation inside,
+ *    row counts stay on the device), except the calls documented as synchronous.
+ *  - Arguments are validated before anything is enqueued; a CUDA error is sticky and is
+ *    reported (DYLLM_E_CUDA) by the next call on the ctx.
+ *  - Row ids: a token row is identified by r = seq * N + pos with N = L_P + L_R and pos the
+ *    0-based global position in the sequence. An index LIST is a packed array of
+ *    row ids, ascending, grouped by sequence, plus offsets off[batch+1] (off[0] = 0,
+ *    off[batch] = total count). Lists live on the device.
+ *  - Tensors: bf16 row-major. K/V caches [batch][N][n_kv_heads*head_dim]; Q and C caches
+ *    [batch][N][n_heads*head_dim]; hidden/FFN_OUT caches H_l [batch][N][d_model].
+ */
+#ifndef DYLLM_API_H_
+#define DYLLM_API_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  DYLLM_OK = 0,
+  DYLLM_DONE = 1,       /* no masked token left in any sequence */
+  DYLLM_E_ARG = -1,     /* null / out-of-range argument */
+  DYLLM_E_SHAPE = -2,   /* shape not supported by the kernels (see dyllm_model_cfg) */
+  DYLLM_E_INDEX = -3,   /* layer / step / which out of range */
+  DYLLM_E_STATE = -4,   /* cache not initialised, or wrong mode */
+  DYLLM_E_CUDA = -5,    /* CUDA runtime / driver error (sticky) */
+  DYLLM_E_NCCL = -6,    /* reserved: tensor-parallel collectives */
+  DYLLM_E_NOMEM = -7    /* device allocation failed */
+};
+
+typedef struct dyllm_ctx dyllm_ctx;
+typedef struct dyllm_weights dyllm_weights;
+typedef struct dyllm_cache dyllm_cache;
+
+/* Model shape (LLaDA / Dream style transformer, BASELINE.json configs).
+ * Constraints: d_model % 64 == 0, head_dim in {16, 32, 64, 128}, n_heads % n_kv_heads == 0,
+ * d_ff % 128 == 0, rope on all head_dim dims (rotate-half, D10). dtype must be 0 (bf16). */
+typedef struct {
+  int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ff, vocab, mask_id;
+  float rope_theta, rms_eps;
+  int32_t qkv_bias;      /* 1: Q/K/V projections carry a bias (Dream / Qwen2.5) */
+  int32_t residual_mode; /* 0: pre-norm residual block (D2 primary); 1: paper_literal Alg. 2/3 */
+  int32_t dtype;         /* 0: bf16 storage, fp32 accumulate (D12) */
+} dyllm_model_cfg;
+
+/* Generation shape and schedule (Alg. 1). */
+typedef struct {
+  int32_t batch, L_P, L_R;
+  int32_t block;         /* semi-AR block size B; must divide L_R */
+  int32_t n_u;           /* tokens unmasked per step per sequence */
+  int32_t T_full;        /* warm-up FullSteps */
+  int32_t full_period;   /* sparse step takes Concat(P,R) when t % full_period == 0 */
+  int32_t layer1_policy; /* 0: carried (Alg. 1 literal); 1: carried ∪ decoded (D5, default) */
+  int32_t cmp;           /* 0: s < tau (Alg. 3, D1); 1: s <= tau (§3.2) */
+} dyllm_run_cfg;
+
+/* input_mode of dyllm_layer_step / dyllm_select_salient */
+enum { DYLLM_INPUT_FULL = 0 /* Concat(P,R): rows [0,N) */, DYLLM_INPUT_RESPONSE = 1 /* R: rows [L_P,N) */ };
+
+/* `which` of dyllm_cache_copy */
+enum { DYLLM_K = 0, DYLLM_V = 1, DYLLM_Q = 2, DYLLM_C = 3, DYLLM_H = 4 };
+
+/* ------------------------------------------------------------------ context */
+const char *dyllm_last_error(void);
+int dyllm_version(void);                 /* returns an integer version, e.g. 100 */
+
+/* Create a context on `device`; `cuda_stream` is a cudaStream_t (NULL = a new stream owned by
+ * the ctx). Synchronous. */
+int dyllm_ctx_create(int device, void *cuda_stream, dyllm_ctx **out);
+int dyllm_ctx_sync(dyllm_ctx *ctx);      /* synchronous: waits for the ctx stream */
+void dyllm_ctx_destroy(dyllm_ctx *ctx);
+
+/* ------------------------------------------------------------------ weights (DS10) */
+/* Number of bf16 elements of the host blob expected by dyllm_weights_load for `cfg`. Blob order
+ * (all bf16, torch-Linear layout W[out][in]): emb[V][d], g_final[d], lm_head[V][d], then for each
+ * layer: g_attn[d], wq[H*hd][d], wk[KVH*hd][d], wv[KVH*hd][d], (bq, bk, bv if qkv_bias),
+ * wo[d][H*hd], g_ffn[d], w_gate[F][d], w_up[F][d], w_down[d][F]. */
+int64_t dyllm_weights_blob_elems(const dyllm_model_cfg *cfg);
+/* Upload a host blob (uint16 bf16 bit patterns, `n_elems` long). Synchronous. */
+int dyllm_weights_load(dyllm_ctx *ctx, const dyllm_model_cfg *cfg, const uint16_t *h_blob,
+                       int64_t n_elems, dyllm_weights **out);
+/* On-device counter-based init (IH4 generator) with the same values
+ * synth/gen.py produces for (seed, std): projections/embedding/lm-head ~ IH4(std), gains = 1,
+ * biases ~ IH4(std). Synchronous. */
+int dyllm_weights_init_random(dyllm_ctx *ctx, const dyllm_model_cfg *cfg, uint64_t seed, double std,
+                              dyllm_weights **out);
+void dyllm_weights_destroy(dyllm_weights *w);
+
+/* ------------------------------------------------------------------ caches (DS1-DS5) */
+/* Allocate the per-layer K/V/Q/C/H caches, H_0 and all scratch for `run`. Synchronous. */
+int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_cfg *run,
+                       dyllm_cache **out);
+void dyllm_cache_destroy(dyllm_cache *c);
+
+/* dyllm_cache_init = FullStep (Alg. 2) on d_tokens[batch][N] (int32): embeds all
+ * rows into H_0 and writes K, V, Q, C, H for every layer and row. Also resets the salient-set
+ * state (idx_sal = None, Alg. 1). Asynchronous. */
+int dyllm_cache_init(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, const int32_t *d_tokens);
+
+/* One layer of SparseStep (Alg. 3 lines 3-16) on layer `layer` (0-based):
+ *   input  : hidden H_{layer} (H_0 = embeddings) and caches of `layer` inside `c`;
+ *            salient list idx_in (d_idx_in, d_off_in[batch+1]) = previous layer's selection (D4),
+ *            every entry must be an input row of `input_mode`;
+ *            tau = cosine threshold (tau > 1: all salient, tau < -1: none).
+ *   output : H_{layer+1} updated in place for the selected rows (other rows keep FFN_OUT_cache,
+ *            P:896); K/V/Q rows of idx_in and C rows of all input rows updated;
+ *            selected list written to d_idx_out / d_off_out (capacity batch*N / batch+1);
+ *            d_sim_out (nullable) receives s per input row at index r (float[batch*N]).
+ * Asynchronous; counts stay on the device. */
+int dyllm_layer_step(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int layer, int input_mode,
+                     const int32_t *d_idx_in, const int32_t *d_off_in, float tau,
+                     int32_t *d_idx_out, int32_t *d_off_out, float *d_sim_out);
+
+/* One iteration of Alg. 1's loop body at step t:
+ *   t < T_full -> FullStep; else SparseStep over all layers with input Concat(P,R) when
+ *   t % full_period == 0, else R only; idx_sal initialised to the response rows on the first
+ *   sparse step; layer-1 idx_in per layer1_policy (D5).
+ *   Then logits for the masked rows of the active semi-AR block, confidence = max softmax
+ *   probability, argmax token; per sequence the n_u most confident positions (ties: lowest
+ *   position; argmax ties: lowest id; D13) are committed into d_tokens.
+ *   h_tau[n_layers] : host array of per-layer thresholds (D17; all equal = the paper's setting)
+ *   d_tokens        : [batch][N] int32, in/out
+ *   d_dec_pos/tok   : [batch][n_u] int32 out: decoded row ids (-1 if none) and token ids
+ *   d_sal_counts    : nullable [n_layers][batch] int32 out: |idx_sal| per layer and sequence
+ * Asynchronous. Returns DYLLM_DONE without work once t >= T_total. */
+int dyllm_denoise_step(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int t,
+                       const float *h_tau, int32_t *d_tokens, int32_t *d_dec_pos, int32_t *d_dec_tok,
+                       int32_t *d_sal_counts);
+
+/* Full-recompute comparison path: FullStep (all caches rewritten) + the same unmasking rule.
+ * Asynchronous. */
+int dyllm_full_step(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int32_t *d_tokens,
+                    int32_t *d_dec_pos, int32_t *d_dec_tok);
+
+/* process_logit + commit alone (Alg. 1 lines 20-21) on the current last-layer hidden
+ * states: the unmasking rule of dyllm_denoise_step without the layer stack. Asynchronous. */
+int dyllm_unmask(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int32_t *d_tokens, int32_t *d_dec_pos,
+                 int32_t *d_dec_tok);
+
+/* Device pointer to one cache tensor of one layer (layer in [0,n_layers); which = DYLLM_K..H;
+ * for DYLLM_H, layer in [0, n_layers] where H_0 = embeddings). Synchronous, no copy. */
+int dyllm_cache_tensor(const dyllm_cache *c, int layer, int which, void **d_ptr, int64_t *n_elems);
+/* Copy a cache tensor to (export=1) or from (export=0) `ptr`; `ptr_on_device` = 1 if ptr is
+ * device memory. Asynchronous on the ctx stream. Test / teacher-forcing hook. */
+int dyllm_cache_copy(dyllm_ctx *ctx, dyllm_cache *c, int layer, int which, void *ptr,
+                     int ptr_on_device, int export_);
+/* Set the carried salient list (idx_sal between steps) — test hook; NULL resets to None. */
+int dyllm_cache_set_carried(dyllm_ctx *ctx, dyllm_cache *c, const int32_t *d_idx, const int32_t *d_off);
+
+/* ------------------------------------------------------------------ kernel-level calls */
+/* K1: temporal cosine similarity of C_new vs C_cache for the input rows of every
+ * sequence, threshold (strict '<' unless cmp=1), stream compaction into a packed list,
+ * and commit C_cache <- C_new for those rows.
+ *   d_c_new, d_c_cache : [batch][N][width] bf16 (width % 8 == 0)
+ *   row_lo             : first input position (0 for full input, L_P for response-only)
+ * Outputs as in dyllm_layer_step. Asynchronous. */
+int dyllm_select_salient(dyllm_ctx *ctx, int batch, int N, int row_lo, int width, const void *d_c_new,
+                         void *d_c_cache, float tau, int cmp, int32_t *d_idx_out, int32_t *d_off_out,
+                         float *d_sim_out);
+
+/* Plain bf16 tcgen05 GEMM, D[M][N] = A[M][K] · W[N][K]^T (+ resid[M][N]) (+ bias[N]), fp32
+ * accumulate, bf16 out. M = *d_M if d_M != NULL (device-resident count, M <= M_cap) else M_cap.
+ * K % 64 == 0, N % 8 == 0. Asynchronous. */
+int dyllm_gemm_bf16(dyllm_ctx *ctx, const int32_t *d_M, int M_cap, int N, int K, const void *d_A,
+                    const void *d_W, void *d_D, const void *d_resid, const void *d_bias);
+
+/* ------------------------------------------------------------------ instrumentation */
+/* Kernel classes timed by the profiler (CUDA events on the ctx stream around each launch). */
+enum {
+  DYLLM_KC_QKV_GEMM = 0, DYLLM_KC_QKV_POST = 1, DYLLM_KC_ATTN = 2, DYLLM_KC_SELECT = 3, DYLLM_KC_O_GEMM = 4,
+  DYLLM_KC_GU_GEMM = 5, DYLLM_KC_DOWN_GEMM = 6, DYLLM_KC_GATHER = 7, DYLLM_KC_SCATTER = 8, DYLLM_KC_LM_GEMM = 9,
+  DYLLM_KC_OTHER = 10, DYLLM_KC_COUNT = 11,
+  DYLLM_KC_FULL = 16 /* added to the class of launches made by a FullStep */
+};
+/* enable = 1: record one event pair per launch from now on (clears previous records); 0: stop. */
+int dyllm_ctx_profile(dyllm_ctx *ctx, int enable);
+/* Synchronous: per-launch durations (ms, launch order) of class `kclass`; returns the number of
+ * records (writes at most max_n). */
+int dyllm_ctx_profile_read(dyllm_ctx *ctx, int kclass, float *h_ms, int max_n);
+/* Process-wide number of kernels libdyllm has launched so far. */
+uint64_t dyllm_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DYLLM_API_H_ */

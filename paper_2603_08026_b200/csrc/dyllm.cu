@@ -1,0 +1,808 @@
+// dyllm.cu — the C ABI (include/dyllm.h) and the step orchestration:
+// FullStep (Alg. 2), the per-layer SparseStep (Alg. 3 with Alg. 4 folded into the attention
+// kernel), the denoise step (Alg. 1 body) and the unmasking rule. No host synchronisation
+// inside a step: every kernel reads its row counts from device memory.
+#include <math.h>
+
+#include <atomic>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+#include "kernels.h"
+
+// ------------------------------------------------------------------ error state
+namespace dy {
+static thread_local std::string g_err;
+void set_error(const std::string &m) { g_err = m; }
+}  // namespace dy
+
+using namespace dy;
+
+#define CHECK_ARG(cond, msg)        \
+  do {                              \
+    if (!(cond)) {                  \
+      set_error(msg);               \
+      return DYLLM_E_ARG;           \
+    }                               \
+  } while (0)
+#define RET(expr)                   \
+  do {                              \
+    int _rc = (expr);               \
+    if (_rc != DYLLM_OK) return _rc; \
+  } while (0)
+
+struct ProfRec {
+  int cls;
+  cudaEvent_t a, b;
+};
+struct dyllm_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  unsigned *masks = nullptr;   // K1 ballot words (capacity kMaskCap)
+  unsigned *ticket = nullptr;  // K1 last-CTA ticket
+  // instrumentation
+  bool prof = false;
+  int cls_offset = 0;          // DYLLM_KC_FULL while a FullStep enqueues
+  std::vector<cudaEvent_t> pool;
+  size_t pool_next = 0;
+  std::vector<ProfRec> recs;
+};
+
+static std::atomic<uint64_t> g_launches{0};
+
+static cudaEvent_t prof_event(dyllm_ctx *c) {
+  if (c->pool_next == c->pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->pool.push_back(e);
+  }
+  return c->pool[c->pool_next++];
+}
+// RAII scope around one kernel launch: counts it and, when profiling, brackets it with events.
+struct KScope {
+  dyllm_ctx *c;
+  int cls;
+  cudaEvent_t a = nullptr;
+  KScope(dyllm_ctx *ctx, int k) : c(ctx), cls(k + ctx->cls_offset) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (c->prof) {
+      a = prof_event(c);
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~KScope() {
+    if (a) {
+      cudaEvent_t b = prof_event(c);
+      cudaEventRecord(b, c->stream);
+      c->recs.push_back({cls, a, b});
+    }
+  }
+};
+#define KL(cls, stmt)                  \
+  do {                                 \
+    KScope _ks(ctx, DYLLM_KC_##cls);   \
+    stmt;                              \
+  } while (0)
+static constexpr int64_t kMaskCap = 1 << 20;
+
+struct LayerW {
+  bf16 *g_attn, *wqkv, *bqkv, *wo, *g_ffn, *wgu, *wd;
+};
+struct dyllm_weights {
+  dyllm_model_cfg cfg;
+  bf16 *emb = nullptr, *g_final = nullptr, *lm_head = nullptr;
+  std::vector<LayerW> L;
+  std::vector<void *> allocs;
+};
+struct LayerC {
+  bf16 *K, *V, *Q, *C, *H;
+};
+struct dyllm_cache {
+  dyllm_model_cfg m;
+  dyllm_run_cfg r;
+  dyllm_ctx *ctx;
+  int N, rows;
+  std::vector<LayerC> L;
+  bf16 *H0;
+  bf16 *Xn, *qkv, *dV, *Cn, *Cg, *h, *hn, *act, *ffo, *Xf;
+  float4 *partials;
+  int *lst[2], *lst_off[2];
+  int *carried, *carried_off;
+  bool carried_valid = false;
+  int *ap_rows, *ap_off, *all_rows, *all_off, *zero_off, *lm_rows, *lm_off;
+  int *dec_prev;
+  bool have_dec_prev = false;
+  bool initialized = false;
+  std::vector<void *> allocs;
+};
+
+static int dalloc(std::vector<void *> &v, void **p, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    return DYLLM_E_NOMEM;
+  }
+  v.push_back(*p);
+  return DYLLM_OK;
+}
+template <typename T>
+static int dalloc_t(std::vector<void *> &v, T **p, size_t count) {
+  return dalloc(v, reinterpret_cast<void **>(p), count * sizeof(T));
+}
+
+static int sticky(dyllm_ctx *ctx) {
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("sticky CUDA error: ") + cudaGetErrorString(e));
+    return DYLLM_E_CUDA;
+  }
+  (void)ctx;
+  return DYLLM_OK;
+}
+
+static int validate_model(const dyllm_model_cfg *m) {
+  if (!m) {
+    set_error("null model cfg");
+    return DYLLM_E_ARG;
+  }
+  const int hd = m->head_dim;
+  if (m->n_layers < 1 || m->d_model < 64 || m->n_heads < 1 || m->n_kv_heads < 1 || m->vocab < 2 ||
+      m->mask_id < 0 || m->mask_id >= m->vocab || m->dtype != 0) {
+    set_error("model cfg out of range");
+    return DYLLM_E_ARG;
+  }
+  if (m->d_model % 64 || (hd != 16 && hd != 32 && hd != 64 && hd != 128) || m->n_heads % m->n_kv_heads ||
+      (m->n_heads * hd) % 64 || m->d_ff % 128 || m->vocab % 8 || m->residual_mode < 0 || m->residual_mode > 1) {
+    set_error("model cfg shape unsupported: d_model%64, head_dim in {16,32,64,128}, H%KVH, (H*hd)%64, d_ff%128, vocab%8");
+    return DYLLM_E_SHAPE;
+  }
+  return DYLLM_OK;
+}
+
+extern "C" {
+
+const char *dyllm_last_error(void) { return g_err.c_str(); }
+int dyllm_version(void) { return 100; }
+
+int dyllm_ctx_create(int device, void *cuda_stream, dyllm_ctx **out) {
+  CHECK_ARG(out, "null out");
+  DY_CUDA(cudaSetDevice(device));
+  dyllm_ctx *c = new dyllm_ctx();
+  c->device = device;
+  if (cuda_stream) {
+    c->stream = static_cast<cudaStream_t>(cuda_stream);
+  } else {
+    DY_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  DY_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+  int major = 0;
+  DY_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  if (major != 10) {
+    set_error("libdyllm requires an sm_100 (B200) device");
+    delete c;
+    return DYLLM_E_ARG;
+  }
+  DY_CUDA(cudaMalloc(&c->masks, kMaskCap * sizeof(unsigned)));
+  DY_CUDA(cudaMalloc(&c->ticket, sizeof(unsigned)));
+  DY_CUDA(cudaMemset(c->ticket, 0, sizeof(unsigned)));
+  *out = c;
+  return DYLLM_OK;
+}
+
+int dyllm_ctx_sync(dyllm_ctx *ctx) {
+  CHECK_ARG(ctx, "null ctx");
+  DY_CUDA(cudaStreamSynchronize(ctx->stream));
+  return DYLLM_OK;
+}
+
+void dyllm_ctx_destroy(dyllm_ctx *ctx) {
+  if (!ctx) return;
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(ctx->masks);
+  cudaFree(ctx->ticket);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+// ------------------------------------------------------------------ weights
+int64_t dyllm_weights_blob_elems(const dyllm_model_cfg *m) {
+  if (validate_model(m) != DYLLM_OK) return -1;
+  const int64_t d = m->d_model, qw = static_cast<int64_t>(m->n_heads) * m->head_dim,
+                kw = static_cast<int64_t>(m->n_kv_heads) * m->head_dim, F = m->d_ff, V = m->vocab;
+  int64_t per = d + qw * d + 2 * kw * d + (m->qkv_bias ? qw + 2 * kw : 0) + d * qw + d + 2 * F * d + d * F;
+  return V * d + d + V * d + per * m->n_layers;
+}
+
+static int alloc_weights(const dyllm_model_cfg *m, dyllm_weights *w) {
+  const int64_t d = m->d_model, qw = static_cast<int64_t>(m->n_heads) * m->head_dim,
+                kw = static_cast<int64_t>(m->n_kv_heads) * m->head_dim, F = m->d_ff, V = m->vocab;
+  w->cfg = *m;
+  RET(dalloc_t(w->allocs, &w->emb, V * d));
+  RET(dalloc_t(w->allocs, &w->g_final, d));
+  RET(dalloc_t(w->allocs, &w->lm_head, V * d));
+  w->L.resize(m->n_layers);
+  for (auto &L : w->L) {
+    RET(dalloc_t(w->allocs, &L.g_attn, d));
+    RET(dalloc_t(w->allocs, &L.wqkv, (qw + 2 * kw) * d));
+    L.bqkv = nullptr;
+    if (m->qkv_bias) RET(dalloc_t(w->allocs, &L.bqkv, qw + 2 * kw));
+    RET(dalloc_t(w->allocs, &L.wo, d * qw));
+    RET(dalloc_t(w->allocs, &L.g_ffn, d));
+    RET(dalloc_t(w->allocs, &L.wgu, 2 * F * d));
+    RET(dalloc_t(w->allocs, &L.wd, d * F));
+  }
+  return DYLLM_OK;
+}
+
+void dyllm_weights_destroy(dyllm_weights *w) {
+  if (!w) return;
+  for (void *p : w->allocs) cudaFree(p);
+  delete w;
+}
+
+int dyllm_weights_load(dyllm_ctx *ctx, const dyllm_model_cfg *m, const uint16_t *h_blob, int64_t n_elems,
+                       dyllm_weights **out) {
+  CHECK_ARG(ctx && h_blob && out, "null argument");
+  RET(validate_model(m));
+  const int64_t need = dyllm_weights_blob_elems(m);
+  if (n_elems != need) {
+    set_error("blob has " + std::to_string(n_elems) + " elements, expected " + std::to_string(need));
+    return DYLLM_E_SHAPE;
+  }
+  dyllm_weights *w = new dyllm_weights();
+  int rc = alloc_weights(m, w);
+  if (rc) {
+    dyllm_weights_destroy(w);
+    return rc;
+  }
+  const int64_t d = m->d_model, qw = static_cast<int64_t>(m->n_heads) * m->head_dim,
+                kw = static_cast<int64_t>(m->n_kv_heads) * m->head_dim, F = m->d_ff, V = m->vocab;
+  const uint16_t *p = h_blob;
+  auto put = [&](bf16 *dst, int64_t n) -> int {
+    DY_CUDA(cudaMemcpy(dst, p, n * 2, cudaMemcpyHostToDevice));
+    p += n;
+    return DYLLM_OK;
+  };
+#define PUT(dst, n)                 \
+  do {                              \
+    int _r = put(dst, n);           \
+    if (_r) {                       \
+      dyllm_weights_destroy(w);     \
+      return _r;                    \
+    }                               \
+  } while (0)
+  PUT(w->emb, V * d);
+  PUT(w->g_final, d);
+  PUT(w->lm_head, V * d);
+  for (auto &L : w->L) {
+    PUT(L.g_attn, d);
+    PUT(L.wqkv, (qw + 2 * kw) * d);   // wq, wk, wv are consecutive in the blob
+    if (m->qkv_bias) PUT(L.bqkv, qw + 2 * kw);
+    PUT(L.wo, d * qw);
+    PUT(L.g_ffn, d);
+    // gate / up interleaved in blocks of 128 rows: [gate blk][up blk] (SwiGLU GEMM epilogue)
+    const uint16_t *gate = p, *up = p + F * d;
+    for (int64_t b = 0; b < F / 128; ++b) {
+      cudaError_t e1 = cudaMemcpy(L.wgu + (2 * b) * 128 * d, gate + b * 128 * d, 128 * d * 2, cudaMemcpyHostToDevice);
+      cudaError_t e2 = cudaMemcpy(L.wgu + (2 * b + 1) * 128 * d, up + b * 128 * d, 128 * d * 2, cudaMemcpyHostToDevice);
+      if (e1 != cudaSuccess || e2 != cudaSuccess) {
+        set_error("cudaMemcpy gate/up failed");
+        dyllm_weights_destroy(w);
+        return DYLLM_E_CUDA;
+      }
+    }
+    p += 2 * F * d;
+    PUT(L.wd, d * F);
+  }
+#undef PUT
+  *out = w;
+  return DYLLM_OK;
+}
+
+static uint64_t mix64_host(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static uint64_t stream_key(uint64_t seed, uint64_t stream) { return mix64_host(seed ^ mix64_host(stream)); }
+enum { T_WQ = 1, T_WK = 2, T_WV = 3, T_BQ = 4, T_BK = 5, T_BV = 6, T_WO = 7, T_GATE = 8, T_UP = 9, T_DOWN = 10,
+       T_EMB = 20, T_LM = 22 };
+static constexpr uint64_t kGlobalLayer = 65535;
+
+int dyllm_weights_init_random(dyllm_ctx *ctx, const dyllm_model_cfg *m, uint64_t seed, double std,
+                              dyllm_weights **out) {
+  CHECK_ARG(ctx && out, "null argument");
+  RET(validate_model(m));
+  dyllm_weights *w = new dyllm_weights();
+  int rc = alloc_weights(m, w);
+  if (rc) {
+    dyllm_weights_destroy(w);
+    return rc;
+  }
+  const int64_t d = m->d_model, qw = static_cast<int64_t>(m->n_heads) * m->head_dim,
+                kw = static_cast<int64_t>(m->n_kv_heads) * m->head_dim, F = m->d_ff, V = m->vocab;
+  const float scale = static_cast<float>(std / sqrt((65536.0 * 65536.0 - 1.0) / 3.0));
+  cudaStream_t st = ctx->stream;
+  auto key = [&](uint64_t layer, int code) { return stream_key(seed, layer * 64 + code); };
+  launch_ih4_fill(w->emb, V, d, key(kGlobalLayer, T_EMB), 0, 0, scale, st);
+  launch_fill_const(w->g_final, d, 1.f, st);
+  launch_ih4_fill(w->lm_head, V, d, key(kGlobalLayer, T_LM), 0, 0, scale, st);
+  for (int l = 0; l < m->n_layers; ++l) {
+    LayerW &L = w->L[l];
+    launch_fill_const(L.g_attn, d, 1.f, st);
+    launch_fill_const(L.g_ffn, d, 1.f, st);
+    launch_ih4_fill(L.wqkv, qw, d, key(l, T_WQ), 0, 0, scale, st);
+    launch_ih4_fill(L.wqkv + qw * d, kw, d, key(l, T_WK), 0, 0, scale, st);
+    launch_ih4_fill(L.wqkv + (qw + kw) * d, kw, d, key(l, T_WV), 0, 0, scale, st);
+    if (m->qkv_bias) {
+      launch_ih4_fill(L.bqkv, 1, qw, key(l, T_BQ), 0, 0, scale, st);
+      launch_ih4_fill(L.bqkv + qw, 1, kw, key(l, T_BK), 0, 0, scale, st);
+      launch_ih4_fill(L.bqkv + qw + kw, 1, kw, key(l, T_BV), 0, 0, scale, st);
+    }
+    launch_ih4_fill(L.wo, d, qw, key(l, T_WO), 0, 0, scale, st);
+    launch_ih4_fill(L.wgu, 2 * F, d, key(l, T_GATE), key(l, T_UP), 128, scale, st);
+    launch_ih4_fill(L.wd, d, F, key(l, T_DOWN), 0, 0, scale, st);
+  }
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("init_random: ") + cudaGetErrorString(e));
+    dyllm_weights_destroy(w);
+    return DYLLM_E_CUDA;
+  }
+  *out = w;
+  return DYLLM_OK;
+}
+
+// ------------------------------------------------------------------ caches
+int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_cfg *r, dyllm_cache **out) {
+  CHECK_ARG(ctx && w && r && out, "null argument");
+  const dyllm_model_cfg &m = w->cfg;
+  if (r->batch < 1 || r->batch > 1024 || r->L_P < 1 || r->L_R < 1 || r->block < 1 || r->block > 256 ||
+      r->L_R % r->block || r->n_u < 1 || r->n_u > 64 || r->n_u > r->block || r->T_full < 0 || r->full_period < 1 ||
+      r->layer1_policy < 0 || r->layer1_policy > 1 || r->cmp < 0 || r->cmp > 1 || r->L_P + r->L_R > 32768) {
+    set_error("run cfg out of range (batch<=1024, block<=256 | L_R, n_u<=min(64,block), N<=32768)");
+    return DYLLM_E_ARG;
+  }
+  dyllm_cache *c = new dyllm_cache();
+  c->m = m;
+  c->r = *r;
+  c->ctx = ctx;
+  c->N = r->L_P + r->L_R;
+  c->rows = r->batch * c->N;
+  const int64_t rows = c->rows, d = m.d_model, qw = static_cast<int64_t>(m.n_heads) * m.head_dim,
+                kw = static_cast<int64_t>(m.n_kv_heads) * m.head_dim, F = m.d_ff;
+  const int64_t lm_cap = static_cast<int64_t>(r->batch) * r->block;
+  auto &A = c->allocs;
+  int rc = DYLLM_OK;
+#define AL(p, n)                        \
+  do {                                  \
+    rc = dalloc_t(A, &(p), (n));        \
+    if (rc) {                           \
+      dyllm_cache_destroy(c);           \
+      return rc;                        \
+    }                                   \
+  } while (0)
+  c->L.resize(m.n_layers);
+  for (auto &L : c->L) {
+    AL(L.K, rows * kw);
+    AL(L.V, rows * kw);
+    AL(L.Q, rows * qw);
+    AL(L.C, rows * qw);
+    AL(L.H, rows * d);
+  }
+  AL(c->H0, rows * d);
+  AL(c->Xn, rows * d);
+  AL(c->qkv, rows * (qw + 2 * kw));
+  AL(c->dV, rows * kw);
+  AL(c->Cn, rows * qw);
+  AL(c->Cg, rows * qw);
+  AL(c->h, rows * d);
+  AL(c->hn, rows * d);
+  AL(c->act, rows * F);
+  AL(c->ffo, rows * d);
+  AL(c->Xf, lm_cap * d);
+  AL(c->partials, lm_cap * gemm_lmhead_ntiles(m.vocab));
+  for (int i = 0; i < 2; ++i) {
+    AL(c->lst[i], rows);
+    AL(c->lst_off[i], r->batch + 1);
+  }
+  AL(c->carried, rows);
+  AL(c->carried_off, r->batch + 1);
+  AL(c->ap_rows, rows);
+  AL(c->ap_off, r->batch + 1);
+  AL(c->all_rows, rows);
+  AL(c->all_off, r->batch + 1);
+  AL(c->zero_off, r->batch + 1);
+  AL(c->lm_rows, lm_cap);
+  AL(c->lm_off, r->batch + 1);
+  AL(c->dec_prev, static_cast<int64_t>(r->batch) * r->n_u);
+#undef AL
+  cudaStream_t st = ctx->stream;
+  if (cudaMemsetAsync(c->zero_off, 0, (r->batch + 1) * sizeof(int), st) != cudaSuccess) {
+    set_error("memset failed");
+    dyllm_cache_destroy(c);
+    return DYLLM_E_CUDA;
+  }
+  launch_build_list(0, nullptr, nullptr, nullptr, 0, 0, r->batch, c->N, 0, 0, c->all_rows, c->all_off, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
+    set_error("cache_create: CUDA error");
+    dyllm_cache_destroy(c);
+    return DYLLM_E_CUDA;
+  }
+  *out = c;
+  return DYLLM_OK;
+}
+
+void dyllm_cache_destroy(dyllm_cache *c) {
+  if (!c) return;
+  for (void *p : c->allocs) cudaFree(p);
+  delete c;
+}
+
+// ------------------------------------------------------------------ step internals
+static int gemm(dyllm_ctx *ctx, const int *M_ptr, int M_cap, int N, int K, const bf16 *A, const bf16 *W, bf16 *D,
+                int ldd, int epi, const bf16 *resid = nullptr, int ldr = 0, const int *resid_rows = nullptr,
+                const bf16 *bias = nullptr, float4 *partials = nullptr) {
+  GemmCall g;
+  g.M_ptr = M_ptr;
+  g.M_cap = M_cap;
+  g.N = N;
+  g.K = K;
+  g.A = A;
+  g.W = W;
+  g.D = D;
+  g.ldd = ldd;
+  g.resid = resid;
+  g.ldr = ldr;
+  g.resid_rows = resid_rows;
+  g.bias = bias;
+  g.partials = partials;
+  g.epi = epi;
+  return gemm_launch(g, ctx->num_sms, ctx->stream);
+}
+
+// post-attention block on rows listed by (rows, M_ptr): h = x + C W_o ; out = h + FFN(RMSNorm(h))
+// (residual_mode 0) or h = RMSNorm(C W_o) ; out = FFN(h) (paper_literal).
+// A_c: contiguous C rows [M][qw]; x rows read through resid_rows from Hprev; result in `out`.
+static int post_attention(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int l, const int *M_ptr,
+                          const bf16 *A_c, const bf16 *Hprev, const int *resid_rows, bf16 *out) {
+  const dyllm_model_cfg &m = c->m;
+  const int d = m.d_model, qw = m.n_heads * m.head_dim, F = m.d_ff, rows = c->rows;
+  const LayerW &L = w->L[l];
+  cudaStream_t st = ctx->stream;
+  const bool res = m.residual_mode == 0;
+  KL(O_GEMM, RET(gemm(ctx, M_ptr, rows, d, qw, A_c, L.wo, c->h, d, res ? EPI_RESID : EPI_BF16, Hprev, d, resid_rows)));
+  KL(OTHER, launch_rmsnorm_rows(c->h, M_ptr, rows, L.g_ffn, m.rms_eps, c->hn, d, st));
+  KL(GU_GEMM, RET(gemm(ctx, M_ptr, rows, 2 * F, d, c->hn, L.wgu, c->act, F, EPI_SWIGLU)));
+  KL(DOWN_GEMM, RET(gemm(ctx, M_ptr, rows, d, F, c->act, L.wd, out, d, res ? EPI_RESID : EPI_BF16, c->h, d, nullptr)));
+  return DYLLM_OK;
+}
+
+// FullStep (Alg. 2): every row of every sequence, all caches rewritten.
+static int full_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, const int *d_tokens) {
+  const dyllm_model_cfg &m = c->m;
+  const int d = m.d_model, qw = m.n_heads * m.head_dim, kw = m.n_kv_heads * m.head_dim, rows = c->rows;
+  cudaStream_t st = ctx->stream;
+  ctx->cls_offset = DYLLM_KC_FULL;
+  KL(OTHER, launch_embed_rows(d_tokens, nullptr, nullptr, rows, w->emb, c->H0, d, st));
+  for (int l = 0; l < m.n_layers; ++l) {
+    const LayerW &L = w->L[l];
+    LayerC &C = c->L[l];
+    const bf16 *Hprev = l == 0 ? c->H0 : c->L[l - 1].H;
+    KL(GATHER, launch_gather_rmsnorm(Hprev, nullptr, nullptr, rows, L.g_attn, m.rms_eps, c->Xn, d, st));
+    KL(QKV_GEMM, RET(gemm(ctx, nullptr, rows, qw + 2 * kw, d, c->Xn, L.wqkv, c->qkv, qw + 2 * kw, EPI_BF16)));
+    KL(QKV_POST, launch_qkv_post(c->qkv, nullptr, nullptr, rows, L.bqkv, c->N, m.n_heads, m.n_kv_heads, m.head_dim,
+                                 m.rope_theta, C.Q, C.K, C.V, nullptr, st));
+    AttnArgs a{};
+    a.batch = c->r.batch;
+    a.N = c->N;
+    a.H = m.n_heads;
+    a.KVH = m.n_kv_heads;
+    a.hd = m.head_dim;
+    a.Q = C.Q;
+    a.K = C.K;
+    a.V = C.V;
+    a.dV = nullptr;
+    a.C_cache = C.C;
+    a.C_out = C.C;
+    a.ex_rows = c->all_rows;
+    a.ex_off = c->all_off;
+    a.ap_rows = c->ap_rows;
+    a.ap_off = c->zero_off;
+    a.sal_rows = c->all_rows;
+    a.sal_off = c->zero_off;
+    a.max_rows_per_seq = c->N;
+    a.scale = 1.f / sqrtf(static_cast<float>(m.head_dim));
+    KL(ATTN, RET(attention_launch(a, st)));
+    int prc = post_attention(ctx, w, c, l, nullptr, C.C, Hprev, nullptr, C.H);
+    if (prc) {
+      ctx->cls_offset = 0;
+      return prc;
+    }
+  }
+  ctx->cls_offset = 0;
+  c->carried_valid = false;
+  c->have_dec_prev = false;
+  c->initialized = true;
+  DY_CUDA(cudaGetLastError());
+  return DYLLM_OK;
+}
+
+// One layer of SparseStep (Alg. 3 lines 3-16) on internal lists.
+static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int l, int row_lo,
+                           const int *idx_in, const int *off_in, float tau, int *idx_out, int *off_out, float *sim,
+                           int *counts) {
+  const dyllm_model_cfg &m = c->m;
+  const int b = c->r.batch, N = c->N, rows = c->rows;
+  const int d = m.d_model, qw = m.n_heads * m.head_dim, kw = m.n_kv_heads * m.head_dim;
+  const LayerW &L = w->L[l];
+  LayerC &C = c->L[l];
+  const bf16 *Hprev = l == 0 ? c->H0 : c->L[l - 1].H;
+  cudaStream_t st = ctx->stream;
+  const int *M_in = off_in + b;
+  // exact rows = idx_in; approximate rows = input rows \ idx_in
+  KL(OTHER, launch_approx_rows(idx_in, off_in, b, N, row_lo, c->ap_rows, c->ap_off, st));
+  // a1 + a2: RMSNorm(x[idx_in]) -> QKV projection of the changed rows
+  KL(GATHER, launch_gather_rmsnorm(Hprev, idx_in, M_in, rows, L.g_attn, m.rms_eps, c->Xn, d, st));
+  KL(QKV_GEMM, RET(gemm(ctx, M_in, rows, qw + 2 * kw, d, c->Xn, L.wqkv, c->qkv, qw + 2 * kw, EPI_BF16)));
+  // a3: RoPE, dV (before overwrite), in-place K/V/Q cache rows
+  KL(QKV_POST, launch_qkv_post(c->qkv, idx_in, M_in, rows, L.bqkv, N, m.n_heads, m.n_kv_heads, m.head_dim,
+                               m.rope_theta, C.Q, C.K, C.V, c->dV, st));
+  // a4: exact rows + approximate rows (Alg. 4) -> Cn
+  AttnArgs a{};
+  a.batch = b;
+  a.N = N;
+  a.H = m.n_heads;
+  a.KVH = m.n_kv_heads;
+  a.hd = m.head_dim;
+  a.Q = C.Q;
+  a.K = C.K;
+  a.V = C.V;
+  a.dV = c->dV;
+  a.C_cache = C.C;
+  a.C_out = c->Cn;
+  a.ex_rows = idx_in;
+  a.ex_off = off_in;
+  a.ap_rows = c->ap_rows;
+  a.ap_off = c->ap_off;
+  a.sal_rows = idx_in;
+  a.sal_off = off_in;
+  a.max_rows_per_seq = N - row_lo;
+  a.scale = 1.f / sqrtf(static_cast<float>(m.head_dim));
+  KL(ATTN, RET(attention_launch(a, st)));
+  // a5: cosine similarity + threshold + compaction; C_cache <- Cn for the input rows
+  KL(SELECT, launch_select(c->Cn, C.C, b, N, row_lo, qw, tau, c->r.cmp, idx_out, off_out, sim, ctx->masks, ctx->ticket,
+                           counts, st));
+  const int *M_out = off_out + b;
+  // a6 + a7 on idx_out, a8 scatter-back into H_l (other rows keep FFN_OUT_cache)
+  KL(GATHER, launch_gather_rows(C.C, idx_out, M_out, rows, c->Cg, qw, st));
+  RET(post_attention(ctx, w, c, l, M_out, c->Cg, Hprev, idx_out, c->ffo));
+  KL(SCATTER, launch_scatter_rows(c->ffo, idx_out, M_out, rows, C.H, d, st));
+  DY_CUDA(cudaGetLastError());
+  return DYLLM_OK;
+}
+
+// logits of the masked rows of the active block -> unmask + commit (a9)
+static int unmask_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int *d_tokens, int *d_dec_pos,
+                       int *d_dec_tok) {
+  const dyllm_model_cfg &m = c->m;
+  const dyllm_run_cfg &r = c->r;
+  cudaStream_t st = ctx->stream;
+  const int lm_cap = r.batch * r.block;
+  const bf16 *HL = c->L[m.n_layers - 1].H;
+  KL(OTHER, launch_lm_candidates(d_tokens, r.batch, r.L_P, r.L_R, r.block, m.mask_id, c->lm_rows, c->lm_off, st));
+  KL(GATHER, launch_gather_rmsnorm(HL, c->lm_rows, c->lm_off + r.batch, lm_cap, w->g_final, m.rms_eps, c->Xf,
+                                   m.d_model, st));
+  KL(LM_GEMM, RET(gemm(ctx, c->lm_off + r.batch, lm_cap, m.vocab, m.d_model, c->Xf, w->lm_head, nullptr, 0, EPI_LMHEAD,
+                       nullptr, 0, nullptr, nullptr, c->partials)));
+  KL(OTHER, launch_lm_select_commit(c->partials, gemm_lmhead_ntiles(m.vocab), c->lm_rows, c->lm_off, r.batch, r.n_u,
+                                    d_tokens, c->dec_prev, d_dec_tok, w->emb, c->H0, m.d_model, st));
+  if (d_dec_pos)
+    DY_CUDA(cudaMemcpyAsync(d_dec_pos, c->dec_prev, sizeof(int) * r.batch * r.n_u, cudaMemcpyDeviceToDevice, st));
+  c->have_dec_prev = true;
+  DY_CUDA(cudaGetLastError());
+  return DYLLM_OK;
+}
+
+// ------------------------------------------------------------------ ABI: steps
+int dyllm_cache_init(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, const int32_t *d_tokens) {
+  CHECK_ARG(ctx && w && c && d_tokens, "null argument");
+  RET(sticky(ctx));
+  return full_step_impl(ctx, w, c, d_tokens);
+}
+
+int dyllm_layer_step(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int layer, int input_mode,
+                     const int32_t *d_idx_in, const int32_t *d_off_in, float tau, int32_t *d_idx_out,
+                     int32_t *d_off_out, float *d_sim_out) {
+  CHECK_ARG(ctx && w && c && d_idx_in && d_off_in && d_idx_out && d_off_out, "null argument");
+  if (layer < 0 || layer >= c->m.n_layers) {
+    set_error("layer out of range");
+    return DYLLM_E_INDEX;
+  }
+  CHECK_ARG(input_mode == DYLLM_INPUT_FULL || input_mode == DYLLM_INPUT_RESPONSE, "bad input_mode");
+  if (!c->initialized) {
+    set_error("cache not initialised (call dyllm_cache_init first)");
+    return DYLLM_E_STATE;
+  }
+  RET(sticky(ctx));
+  const int row_lo = input_mode == DYLLM_INPUT_FULL ? 0 : c->r.L_P;
+  return layer_step_impl(ctx, w, c, layer, row_lo, d_idx_in, d_off_in, tau, d_idx_out, d_off_out, d_sim_out, nullptr);
+}
+
+int dyllm_denoise_step(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int t, const float *h_tau,
+                       int32_t *d_tokens, int32_t *d_dec_pos, int32_t *d_dec_tok, int32_t *d_sal_counts) {
+  CHECK_ARG(ctx && w && c && d_tokens && d_dec_tok, "null argument");
+  const dyllm_run_cfg &r = c->r;
+  const int T_total = (r.L_R + r.n_u - 1) / r.n_u;
+  if (t < 0) {
+    set_error("t < 0");
+    return DYLLM_E_INDEX;
+  }
+  if (t >= T_total) return DYLLM_DONE;
+  RET(sticky(ctx));
+  cudaStream_t st = ctx->stream;
+  if (t < r.T_full) {
+    RET(full_step_impl(ctx, w, c, d_tokens));
+  } else {
+    CHECK_ARG(h_tau, "null tau");
+    if (!c->initialized) {
+      set_error("sparse step before any FullStep (T_full = 0 needs dyllm_cache_init)");
+      return DYLLM_E_STATE;
+    }
+    const int row_lo = (t % r.full_period == 0) ? 0 : r.L_P;
+    // layer-1 idx_in: carried (or response rows when None) [∪ decoded rows, D5], ∩ input rows
+    KL(OTHER, launch_build_list(1, c->carried_valid ? c->carried : nullptr, c->carried_off,
+                                c->have_dec_prev ? c->dec_prev : nullptr, r.n_u, r.layer1_policy, r.batch, c->N, row_lo,
+                                r.L_P, c->lst[0], c->lst_off[0], st));
+    int cur = 0;
+    for (int l = 0; l < c->m.n_layers; ++l) {
+      RET(layer_step_impl(ctx, w, c, l, row_lo, c->lst[cur], c->lst_off[cur], h_tau[l], c->lst[cur ^ 1],
+                          c->lst_off[cur ^ 1], nullptr, d_sal_counts ? d_sal_counts + l * r.batch : nullptr));
+      cur ^= 1;
+    }
+    DY_CUDA(cudaMemcpyAsync(c->carried, c->lst[cur], sizeof(int) * c->rows, cudaMemcpyDeviceToDevice, st));
+    DY_CUDA(cudaMemcpyAsync(c->carried_off, c->lst_off[cur], sizeof(int) * (r.batch + 1), cudaMemcpyDeviceToDevice, st));
+    c->carried_valid = true;
+  }
+  return unmask_impl(ctx, w, c, d_tokens, d_dec_pos, d_dec_tok);
+}
+
+int dyllm_full_step(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int32_t *d_tokens, int32_t *d_dec_pos,
+                    int32_t *d_dec_tok) {
+  CHECK_ARG(ctx && w && c && d_tokens && d_dec_tok, "null argument");
+  RET(sticky(ctx));
+  RET(full_step_impl(ctx, w, c, d_tokens));
+  return unmask_impl(ctx, w, c, d_tokens, d_dec_pos, d_dec_tok);
+}
+
+int dyllm_unmask(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int32_t *d_tokens, int32_t *d_dec_pos,
+                 int32_t *d_dec_tok) {
+  CHECK_ARG(ctx && w && c && d_tokens && d_dec_tok, "null argument");
+  if (!c->initialized) {
+    set_error("cache not initialised");
+    return DYLLM_E_STATE;
+  }
+  RET(sticky(ctx));
+  return unmask_impl(ctx, w, c, d_tokens, d_dec_pos, d_dec_tok);
+}
+
+// ------------------------------------------------------------------ ABI: instrumentation
+int dyllm_ctx_profile(dyllm_ctx *ctx, int enable) {
+  CHECK_ARG(ctx, "null ctx");
+  if (enable) {
+    DY_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->recs.clear();
+    ctx->pool_next = 0;
+  }
+  ctx->prof = enable != 0;
+  return DYLLM_OK;
+}
+
+int dyllm_ctx_profile_read(dyllm_ctx *ctx, int kclass, float *h_ms, int max_n) {
+  CHECK_ARG(ctx, "null ctx");
+  DY_CUDA(cudaStreamSynchronize(ctx->stream));
+  int n = 0;
+  for (const ProfRec &r : ctx->recs) {
+    if (r.cls != kclass) continue;
+    if (h_ms && n < max_n) {
+      float ms = 0.f;
+      DY_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+      h_ms[n] = ms;
+    }
+    ++n;
+  }
+  return n;
+}
+
+uint64_t dyllm_launch_count(void) { return g_launches.load(); }
+
+// ------------------------------------------------------------------ ABI: cache access
+int dyllm_cache_tensor(const dyllm_cache *c, int layer, int which, void **d_ptr, int64_t *n_elems) {
+  CHECK_ARG(c && d_ptr, "null argument");
+  const int64_t rows = c->rows, d = c->m.d_model, qw = static_cast<int64_t>(c->m.n_heads) * c->m.head_dim,
+                kw = static_cast<int64_t>(c->m.n_kv_heads) * c->m.head_dim;
+  if (which == DYLLM_H) {
+    if (layer < 0 || layer > c->m.n_layers) {
+      set_error("layer out of range");
+      return DYLLM_E_INDEX;
+    }
+    *d_ptr = layer == 0 ? c->H0 : c->L[layer - 1].H;
+    if (n_elems) *n_elems = rows * d;
+    return DYLLM_OK;
+  }
+  if (layer < 0 || layer >= c->m.n_layers || which < 0 || which > 4) {
+    set_error("layer/which out of range");
+    return DYLLM_E_INDEX;
+  }
+  const LayerC &L = c->L[layer];
+  switch (which) {
+    case DYLLM_K: *d_ptr = L.K; if (n_elems) *n_elems = rows * kw; break;
+    case DYLLM_V: *d_ptr = L.V; if (n_elems) *n_elems = rows * kw; break;
+    case DYLLM_Q: *d_ptr = L.Q; if (n_elems) *n_elems = rows * qw; break;
+    default: *d_ptr = L.C; if (n_elems) *n_elems = rows * qw; break;
+  }
+  return DYLLM_OK;
+}
+
+int dyllm_cache_copy(dyllm_ctx *ctx, dyllm_cache *c, int layer, int which, void *ptr, int ptr_on_device, int export_) {
+  CHECK_ARG(ctx && c && ptr, "null argument");
+  void *dp = nullptr;
+  int64_t n = 0;
+  RET(dyllm_cache_tensor(c, layer, which, &dp, &n));
+  const cudaMemcpyKind k = export_ ? (ptr_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost)
+                                   : (ptr_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
+  if (export_) DY_CUDA(cudaMemcpyAsync(ptr, dp, n * 2, k, ctx->stream));
+  else DY_CUDA(cudaMemcpyAsync(dp, ptr, n * 2, k, ctx->stream));
+  if (!export_) c->initialized = true;
+  return DYLLM_OK;
+}
+
+int dyllm_cache_set_carried(dyllm_ctx *ctx, dyllm_cache *c, const int32_t *d_idx, const int32_t *d_off) {
+  CHECK_ARG(ctx && c, "null argument");
+  if (!d_idx || !d_off) {
+    c->carried_valid = false;
+    return DYLLM_OK;
+  }
+  DY_CUDA(cudaMemcpyAsync(c->carried_off, d_off, sizeof(int) * (c->r.batch + 1), cudaMemcpyDeviceToDevice, ctx->stream));
+  DY_CUDA(cudaMemcpyAsync(c->carried, d_idx, sizeof(int) * c->rows, cudaMemcpyDeviceToDevice, ctx->stream));
+  c->carried_valid = true;
+  return DYLLM_OK;
+}
+
+// ------------------------------------------------------------------ ABI: kernel-level calls
+int dyllm_select_salient(dyllm_ctx *ctx, int batch, int N, int row_lo, int width, const void *d_c_new,
+                         void *d_c_cache, float tau, int cmp, int32_t *d_idx_out, int32_t *d_off_out,
+                         float *d_sim_out) {
+  CHECK_ARG(ctx && d_c_new && d_c_cache && d_idx_out && d_off_out, "null argument");
+  CHECK_ARG(batch >= 1 && batch <= 1024 && N >= 1 && row_lo >= 0 && row_lo < N && width >= 8 && width % 8 == 0 &&
+                (cmp == 0 || cmp == 1),
+            "select_salient: bad shape");
+  const int64_t words = static_cast<int64_t>(batch) * ((N - row_lo + 31) / 32);
+  CHECK_ARG(words <= kMaskCap, "select_salient: too many rows");
+  RET(sticky(ctx));
+  KL(SELECT, launch_select(static_cast<const bf16 *>(d_c_new), static_cast<bf16 *>(d_c_cache), batch, N, row_lo, width,
+                           tau, cmp, d_idx_out, d_off_out, d_sim_out, ctx->masks, ctx->ticket, nullptr, ctx->stream));
+  DY_CUDA(cudaGetLastError());
+  return DYLLM_OK;
+}
+
+int dyllm_gemm_bf16(dyllm_ctx *ctx, const int32_t *d_M, int M_cap, int N, int K, const void *d_A, const void *d_W,
+                    void *d_D, const void *d_resid, const void *d_bias) {
+  CHECK_ARG(ctx && d_A && d_W && d_D && M_cap > 0 && N > 0 && K > 0, "null argument");
+  RET(sticky(ctx));
+  KScope ks(ctx, DYLLM_KC_OTHER);
+  return gemm(ctx, d_M, M_cap, N, K, static_cast<const bf16 *>(d_A), static_cast<const bf16 *>(d_W),
+              static_cast<bf16 *>(d_D), N, d_resid ? EPI_RESID : EPI_BF16, static_cast<const bf16 *>(d_resid), N,
+              nullptr, static_cast<const bf16 *>(d_bias));
+}
+
+}  // extern "C"

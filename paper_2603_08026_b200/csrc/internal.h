@@ -1,0 +1,67 @@
+// internal.h — host-side internals shared by the libdyllm translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/dyllm.h"
+
+typedef __nv_bfloat16 bf16;
+
+namespace dy {
+
+void set_error(const std::string &msg);
+
+#define DY_CUDA(expr)                                                                              \
+  do {                                                                                             \
+    cudaError_t _e = (expr);                                                                       \
+    if (_e != cudaSuccess) {                                                                       \
+      ::dy::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e) + " @" + __FILE__ + ":" + \
+                      std::to_string(__LINE__));                                                   \
+      return DYLLM_E_CUDA;                                                                         \
+    }                                                                                              \
+  } while (0)
+
+// ------------------------------------------------------------------ GEMM (gemm.cu)
+enum Epi { EPI_BF16 = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_LMHEAD = 3 };
+
+struct GemmCall {
+  const int *M_ptr = nullptr;  // device row count (nullable -> M_cap)
+  int M_cap = 0;               // capacity rows of A (and of D)
+  int N = 0;                   // rows of W (for SWIGLU: 2*F interleaved rows)
+  int K = 0;
+  const bf16 *A = nullptr;     // [M_cap][K]
+  const bf16 *W = nullptr;     // [N][K]
+  bf16 *D = nullptr;           // output (EPI_BF16/RESID: [M][ldd]; SWIGLU: [M][ldd] with N/2 cols)
+  int ldd = 0;
+  const bf16 *resid = nullptr; // EPI_RESID: residual rows
+  int ldr = 0;
+  const int *resid_rows = nullptr;  // nullable: residual row index per output row
+  const bf16 *bias = nullptr;       // nullable [N]
+  float4 *partials = nullptr;       // EPI_LMHEAD: [M_cap][n_tiles] (max, sumexp, argmax, 0)
+  int epi = EPI_BF16;
+};
+int gemm_launch(const GemmCall &g, int num_sms, cudaStream_t st);
+int gemm_lmhead_ntiles(int N);
+
+// ------------------------------------------------------------------ kernels (kernels.cu)
+struct AttnArgs {
+  int batch, N, H, KVH, hd;
+  const bf16 *Q;          // [b][N][H*hd]
+  const bf16 *K, *V;      // [b][N][KVH*hd]
+  const bf16 *dV;         // [M_in][KVH*hd] compact, aligned with idx_in
+  const bf16 *C_cache;    // [b][N][H*hd] (approximate rows: base context)
+  bf16 *C_out;            // [b][N][H*hd]
+  const int *ex_rows, *ex_off;  // exact-row list (row ids) + offsets [b+1]
+  const int *ap_rows, *ap_off;  // approximate-row list + offsets
+  const int *sal_rows, *sal_off;  // idx_in (salient keys) + offsets
+  int max_rows_per_seq;         // upper bound of rows per list per sequence
+  float scale;
+};
+int attention_launch(const AttnArgs &a, cudaStream_t st);
+
+}  // namespace dy

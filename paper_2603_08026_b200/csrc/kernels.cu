@@ -1,0 +1,577 @@
+// kernels.cu — the HBM-bound kernels of the salient step
+// and the list / unmasking plumbing. All row counts are read from device memory.
+#include "common.cuh"
+#include "internal.h"
+#include "kernels.h"
+
+namespace dy {
+
+// ============================================================================ a0: embeddings
+// H0[r] = E[tokens[r]] for every row r of the list (or all rows when rows == nullptr).
+__global__ void embed_rows_kernel(const int *__restrict__ tokens, const int *__restrict__ rows,
+                                  const int *__restrict__ M_ptr, int M_cap, const bf16 *__restrict__ emb,
+                                  bf16 *__restrict__ H0, int d) {
+  const int M = M_ptr ? *M_ptr : M_cap;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+  for (int i = warp; i < M; i += gridDim.x * blockDim.x / 32) {
+    const int r = rows ? rows[i] : i;
+    const int tok = tokens[r];
+    const uint4 *src = reinterpret_cast<const uint4 *>(emb + static_cast<int64_t>(tok) * d);
+    uint4 *dst = reinterpret_cast<uint4 *>(H0 + static_cast<int64_t>(r) * d);
+    for (int c = lane; c < d / 8; c += 32) dst[c] = src[c];
+  }
+}
+
+// ============================================================================ a1: gather + RMSNorm
+// dst[i] = RMSNorm(src[idx[i]]) * g  (D3), one warp per row, fp32 statistics.
+__global__ void gather_rmsnorm_kernel(const bf16 *__restrict__ src, const int *__restrict__ idx,
+                                      const int *__restrict__ M_ptr, int M_cap, const bf16 *__restrict__ g,
+                                      float eps, bf16 *__restrict__ dst, int d) {
+  const int M = M_ptr ? *M_ptr : M_cap;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+  const int nv = d / 8;
+  for (int i = warp; i < M; i += gridDim.x * blockDim.x / 32) {
+    const int r = idx ? idx[i] : i;
+    const uint4 *s = reinterpret_cast<const uint4 *>(src + static_cast<int64_t>(r) * d);
+    float ss = 0.f;
+    for (int c = lane; c < nv; c += 32) {
+      float f[8];
+      unpack8(s[c], f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ss += f[j] * f[j];
+    }
+    ss = warp_sum(ss);
+    const float inv = rsqrtf(ss / d + eps);
+    uint4 *o = reinterpret_cast<uint4 *>(dst + static_cast<int64_t>(i) * d);
+    const uint4 *gv = reinterpret_cast<const uint4 *>(g);
+    for (int c = lane; c < nv; c += 32) {
+      float f[8], w[8];
+      unpack8(s[c], f);
+      unpack8(gv[c], w);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[j] = f[j] * inv * w[j];
+      o[c] = pack8(f);
+    }
+  }
+}
+
+// plain row gather dst[i] = src[idx[i]] (a6 A-operand: C[idx_out])
+__global__ void gather_rows_kernel(const bf16 *__restrict__ src, const int *__restrict__ idx,
+                                   const int *__restrict__ M_ptr, int M_cap, bf16 *__restrict__ dst, int width) {
+  const int M = M_ptr ? *M_ptr : M_cap;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+  const int nv = width / 8;
+  for (int i = warp; i < M; i += gridDim.x * blockDim.x / 32) {
+    const uint4 *s = reinterpret_cast<const uint4 *>(src + static_cast<int64_t>(idx[i]) * width);
+    uint4 *o = reinterpret_cast<uint4 *>(dst + static_cast<int64_t>(i) * width);
+    for (int c = lane; c < nv; c += 32) o[c] = ld_nc_v4(s + c);
+  }
+}
+
+// ============================================================================ a8: scatter-back
+// dst[idx[i]] = src[i]  (H_l[idx_out] <- FFN rows); other rows untouched (zero-copy reuse)
+__global__ void scatter_rows_kernel(const bf16 *__restrict__ src, const int *__restrict__ idx,
+                                    const int *__restrict__ M_ptr, int M_cap, bf16 *__restrict__ dst, int width) {
+  const int M = M_ptr ? *M_ptr : M_cap;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+  const int nv = width / 8;
+  for (int i = warp; i < M; i += gridDim.x * blockDim.x / 32) {
+    const uint4 *s = reinterpret_cast<const uint4 *>(src + static_cast<int64_t>(i) * width);
+    uint4 *o = reinterpret_cast<uint4 *>(dst + static_cast<int64_t>(idx[i]) * width);
+    for (int c = lane; c < nv; c += 32) o[c] = ld_nc_v4(s + c);
+  }
+}
+
+// ============================================================================ a3: RoPE, dV, cache rows
+// For packed row i (row id r = idx[i], pos = r % N): q,k,v = qkv[i] (+bias); RoPE(q,k) at pos
+// (rotate-half, D10); dV = v - V_cache[r] captured BEFORE the overwrite;
+// Q_cache[r], K_cache[r], V_cache[r] <- q, k, v (D6).
+__global__ void qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restrict__ idx,
+                                const int *__restrict__ M_ptr, int M_cap, const bf16 *__restrict__ bias, int N,
+                                int H, int KVH, int hd, float log2_theta, bf16 *__restrict__ Qc,
+                                bf16 *__restrict__ Kc, bf16 *__restrict__ Vc, bf16 *__restrict__ dV) {
+  const int M = M_ptr ? *M_ptr : M_cap;
+  const int qw = H * hd, kw = KVH * hd, W = qw + 2 * kw;
+  const int half = hd / 2;
+  for (int i = blockIdx.x; i < M; i += gridDim.x) {
+    const int r = idx ? idx[i] : i;
+    const float pos = static_cast<float>(r % N);
+    const bf16 *src = qkv + static_cast<int64_t>(i) * W;
+    // q and k: one thread per rotation pair
+    const int npairs = (H + KVH) * half;
+    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+      const int head = p / half, k = p - head * half;
+      const int col = head * hd + k;  // q cols [0,qw), k cols [qw, qw+kw) — heads are contiguous
+      float x1 = bf2f(src[col]), x2 = bf2f(src[col + half]);
+      if (bias) {
+        x1 += bf2f(bias[col]);
+        x2 += bf2f(bias[col + half]);
+      }
+      const float inv = exp2f(-(2.f * k / hd) * log2_theta);
+      float sn, cs;
+      sincosf(pos * inv, &sn, &cs);
+      const bf16 y1 = f2bf(x1 * cs - x2 * sn), y2 = f2bf(x2 * cs + x1 * sn);
+      if (col < qw) {
+        bf16 *q = Qc + static_cast<int64_t>(r) * qw;
+        q[col] = y1;
+        q[col + half] = y2;
+      } else {
+        bf16 *kk = Kc + static_cast<int64_t>(r) * kw;
+        kk[col - qw] = y1;
+        kk[col - qw + half] = y2;
+      }
+    }
+    // v: one thread per element
+    for (int c = threadIdx.x; c < kw; c += blockDim.x) {
+      float v = bf2f(src[qw + kw + c]);
+      if (bias) v += bf2f(bias[qw + kw + c]);
+      const bf16 vb = f2bf(v);
+      bf16 *vc = Vc + static_cast<int64_t>(r) * kw + c;
+      if (dV) dV[static_cast<int64_t>(i) * kw + c] = f2bf(bf2f(vb) - bf2f(*vc));
+      *vc = vb;
+    }
+  }
+}
+
+// ============================================================================ lists
+// Approximate-row list of each sequence: input rows [row_lo, N) that are NOT in idx_in
+// (exact rows = idx_in itself). One CTA per sequence. ap_off[s] = s*L - off_in[s].
+__global__ void approx_rows_kernel(const int *__restrict__ idx_in, const int *__restrict__ off_in, int N,
+                                   int row_lo, int *__restrict__ ap_rows, int *__restrict__ ap_off, int batch) {
+  extern __shared__ uint8_t flag[];
+  __shared__ int warp_cnt[32];
+  const int s = blockIdx.x;
+  const int L = N - row_lo;
+  for (int p = threadIdx.x; p < N; p += blockDim.x) flag[p] = 0;
+  __syncthreads();
+  const int b0 = off_in[s], b1 = off_in[s + 1];
+  for (int j = b0 + threadIdx.x; j < b1; j += blockDim.x) flag[idx_in[j] - s * N] = 1;
+  __syncthreads();
+  int base = s * L - b0;
+  if (threadIdx.x == 0) {
+    ap_off[s] = base;
+    if (s == batch - 1) ap_off[batch] = batch * L - off_in[batch];
+  }
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  for (int p0 = row_lo; p0 < N; p0 += blockDim.x) {
+    const int p = p0 + threadIdx.x;
+    const bool keep = p < N && !flag[p];
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) warp_cnt[warp] = __popc(m);
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int w = 0; w < nw; ++w) {
+      before += (w < warp) ? warp_cnt[w] : 0;
+      tot += warp_cnt[w];
+    }
+    if (keep) ap_rows[base + before + __popc(m & ((1u << lane) - 1))] = s * N + p;
+    base += tot;
+    __syncthreads();
+  }
+}
+
+// Single-CTA list builder used once per step: for each sequence, rows in [row_lo, N) that are
+//   mode 0: all rows (identity list)
+//   mode 1: in `carried` (its list), or (policy 1) in the decoded set dec_pos[b][n_u]  (D5)
+// Writes a packed row-id list + offsets [b+1].
+__global__ void build_list_kernel(int mode, const int *__restrict__ carried, const int *__restrict__ carried_off,
+                                  const int *__restrict__ dec_pos, int n_u, int policy, int batch, int N,
+                                  int row_lo, int resp_lo, int *__restrict__ out, int *__restrict__ out_off) {
+  extern __shared__ uint8_t flag[];
+  __shared__ int warp_cnt[32];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  int base = 0;
+  if (threadIdx.x == 0) out_off[0] = 0;
+  for (int s = 0; s < batch; ++s) {
+    for (int p = threadIdx.x; p < N; p += blockDim.x) flag[p] = (mode == 0) ? 1 : 0;
+    __syncthreads();
+    if (mode == 1) {
+      if (carried) {
+        for (int j = carried_off[s] + threadIdx.x; j < carried_off[s + 1]; j += blockDim.x)
+          flag[carried[j] - s * N] = 1;
+      } else {  // idx_sal = None -> the response rows [L_P, N)
+        for (int p = resp_lo + threadIdx.x; p < N; p += blockDim.x) flag[p] = 1;
+      }
+      if (policy == 1 && dec_pos) {
+        for (int j = threadIdx.x; j < n_u; j += blockDim.x) {
+          const int r = dec_pos[s * n_u + j];
+          if (r >= 0) flag[r - s * N] = 1;
+        }
+      }
+    }
+    __syncthreads();
+    for (int p0 = row_lo; p0 < N; p0 += blockDim.x) {
+      const int p = p0 + threadIdx.x;
+      const bool keep = p < N && flag[p];
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (lane == 0) warp_cnt[warp] = __popc(m);
+      __syncthreads();
+      int before = 0, tot = 0;
+      for (int w = 0; w < nw; ++w) {
+        before += (w < warp) ? warp_cnt[w] : 0;
+        tot += warp_cnt[w];
+      }
+      if (keep) out[base + before + __popc(m & ((1u << lane) - 1))] = s * N + p;
+      base += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out_off[s + 1] = base;
+  }
+}
+
+// ============================================================================ a5: K1
+// Temporal cosine similarity + threshold + stream compaction (+ commit C_cache <- C_new).
+// grid = (ceil(L/32), batch); 8 warps per CTA, 4 rows per warp; row reads are 16-byte,
+// coalesced, all loads of a row issued before the reductions. Each CTA produces one 32-bit
+// ballot mask of its 32 rows; the last CTA to finish (atomic ticket) scans the masks of all
+// sequences and writes the packed list + offsets (no second launch, no host sync).
+constexpr int kSelRowsPerCta = 32;
+
+__global__ void __launch_bounds__(256) select_salient_kernel(
+    const bf16 *__restrict__ c_new, bf16 *__restrict__ c_cache, int N, int row_lo, int width, float tau,
+    int cmp, int *__restrict__ idx_out, int *__restrict__ off_out, float *__restrict__ sim_out,
+    unsigned *__restrict__ masks, unsigned *__restrict__ ticket, int *__restrict__ counts_out) {
+  __shared__ unsigned row_flag[kSelRowsPerCta];
+  __shared__ bool is_last;
+  const int s = blockIdx.y;
+  const int L = N - row_lo;
+  const int chunk = blockIdx.x;
+  const int nchunks = gridDim.x;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nv = width / 8;
+  for (int rr = warp; rr < kSelRowsPerCta; rr += 8) {
+    const int p = row_lo + chunk * kSelRowsPerCta + rr;
+    unsigned f = 0;
+    if (p < N) {
+      const int64_t r = static_cast<int64_t>(s) * N + p;
+      const uint4 *a = reinterpret_cast<const uint4 *>(c_new + r * width);
+      uint4 *b = reinterpret_cast<uint4 *>(c_cache + r * width);
+      float dot = 0.f, na = 0.f, nb = 0.f;
+      for (int c = lane; c < nv; c += 32) {
+        const uint4 ua = ld_nc_v4(a + c);
+        const uint4 ub = b[c];
+        float fa[8], fb[8];
+        unpack8(ua, fa);
+        unpack8(ub, fb);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          dot = fmaf(fa[j], fb[j], dot);
+          na = fmaf(fa[j], fa[j], na);
+          nb = fmaf(fb[j], fb[j], nb);
+        }
+        b[c] = ua;  // commit C_cache <- C (Alg. 3 line 16)
+      }
+      dot = warp_sum(dot);
+      na = warp_sum(na);
+      nb = warp_sum(nb);
+      float sim;
+      const bool za = na < 1e-24f, zb = nb < 1e-24f;   // D9 zero-norm policy
+      if (za && zb) sim = 1.f;
+      else if (za || zb) sim = 0.f;
+      else sim = dot / sqrtf(na * nb);   // identical rows: sqrt(fl(x*x)) == x -> exactly 1
+      f = cmp ? (sim <= tau) : (sim < tau);
+      if (sim_out && lane == 0) sim_out[r] = sim;
+    }
+    if (lane == 0) row_flag[rr] = f;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const unsigned m = __ballot_sync(0xffffffffu, row_flag[threadIdx.x] != 0);
+    if (threadIdx.x == 0) {
+      masks[s * nchunks + chunk] = m;
+      __threadfence();
+      const unsigned t = atomicAdd(ticket, 1u);
+      is_last = (t == gridDim.x * gridDim.y - 1);
+    }
+  }
+  __syncthreads();
+  if (!is_last) return;
+  // ---- last CTA: scan all masks (b * nchunks words) and emit the packed list
+  __threadfence();
+  const int batch = gridDim.y;
+  const int nwords = batch * nchunks;
+  __shared__ int seq_base[1025];
+  // per-sequence counts (one warp per sequence, strided)
+  for (int sq = warp; sq < batch; sq += 8) {
+    int c = 0;
+    for (int w = lane; w < nchunks; w += 32) c += __popc(__ldcg(masks + sq * nchunks + w));
+    c = warp_sum_i(c);
+    if (lane == 0) seq_base[sq + 1] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    seq_base[0] = 0;
+    for (int sq = 0; sq < batch; ++sq) seq_base[sq + 1] += seq_base[sq];
+  }
+  __syncthreads();
+  for (int sq = threadIdx.x; sq <= batch; sq += blockDim.x) {
+    off_out[sq] = seq_base[sq];
+    if (counts_out && sq < batch) counts_out[sq] = seq_base[sq + 1] - seq_base[sq];
+  }
+  // each warp handles one sequence at a time: prefix over its words via ballots of popcounts
+  for (int sq = warp; sq < batch; sq += 8) {
+    int base = seq_base[sq];
+    for (int w0 = 0; w0 < nchunks; w0 += 32) {
+      const int w = w0 + lane;
+      const unsigned m = (w < nchunks) ? __ldcg(masks + sq * nchunks + w) : 0u;
+      int cnt = __popc(m);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      int pos = base + incl - cnt;
+      unsigned mm = m;
+      while (mm) {
+        const int bit = __ffs(mm) - 1;
+        mm &= mm - 1;
+        idx_out[pos++] = sq * N + row_lo + w * kSelRowsPerCta + bit;
+      }
+      base += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+  (void)nwords;
+  if (threadIdx.x == 0) *ticket = 0u;  // re-arm for the next launch (stream-ordered)
+}
+
+// ============================================================================ a9: unmasking
+// Candidate rows = masked positions of the active semi-AR block of each sequence (D13).
+__global__ void lm_candidates_kernel(const int *__restrict__ tokens, int batch, int L_P, int L_R, int block,
+                                     int mask_id, int *__restrict__ rows, int *__restrict__ off) {
+  // single CTA, one warp per sequence for the search; counts then prefix
+  __shared__ int cnt[1024];
+  __shared__ int blk_of[1024];
+  const int N = L_P + L_R;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  for (int s = warp; s < batch; s += nw) {
+    int found = -1;
+    for (int k = 0; k < L_R / block && found < 0; ++k) {
+      bool any = false;
+      for (int j = lane; j < block; j += 32) any |= tokens[s * N + L_P + k * block + j] == mask_id;
+      if (__any_sync(0xffffffffu, any)) found = k;
+    }
+    int c = 0;
+    if (found >= 0)
+      for (int j = lane; j < block; j += 32) c += tokens[s * N + L_P + found * block + j] == mask_id;
+    c = warp_sum_i(c);
+    if (lane == 0) {
+      cnt[s] = c;
+      blk_of[s] = found;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int s = 0; s < batch; ++s) {
+      off[s] = acc;
+      acc += cnt[s];
+    }
+    off[batch] = acc;
+  }
+  __syncthreads();
+  for (int s = warp; s < batch; s += nw) {
+    const int k = blk_of[s];
+    if (k < 0) continue;
+    int base = off[s];
+    for (int j0 = 0; j0 < block; j0 += 32) {
+      const int j = j0 + lane;
+      const int p = L_P + k * block + j;
+      const bool m = j < block && tokens[s * N + p] == mask_id;
+      const unsigned bal = __ballot_sync(0xffffffffu, m);
+      if (m) rows[base + __popc(bal & ((1u << lane) - 1))] = s * N + p;
+      base += __popc(bal);
+    }
+  }
+}
+
+// Reduce the LM-head partials of each candidate row to (max, sumexp, argmax), confidence =
+// max softmax probability = 1 / sum exp(z - max); choose the n_u most confident rows per
+// sequence (ties: lowest position), commit the argmax token (ties: lowest id), record the
+// decoded rows and refresh H_0 for them (Alg. 1).
+__global__ void lm_select_commit_kernel(const float4 *__restrict__ partials, int n_tiles,
+                                        const int *__restrict__ rows, const int *__restrict__ off, int n_u,
+                                        int *__restrict__ tokens, int *__restrict__ dec_pos,
+                                        int *__restrict__ dec_tok, const bf16 *__restrict__ emb,
+                                        bf16 *__restrict__ H0, int d) {
+  __shared__ float conf[256];
+  __shared__ int tok[256];
+  __shared__ int chosen[64];
+  const int s = blockIdx.x;
+  const int b0 = off[s], n = off[s + 1] - b0;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  for (int i = warp; i < n && i < 256; i += nw) {
+    const float4 *pr = partials + static_cast<int64_t>(b0 + i) * n_tiles;
+    float m = -INFINITY, sm = 0.f;
+    int a = 0x7fffffff;
+    for (int t = lane; t < n_tiles; t += 32) {
+      const float4 v = pr[t];
+      const int av = __float_as_int(v.z);
+      if (v.x > m) {
+        sm = sm * __expf(m - v.x) + v.y;
+        m = v.x;
+        a = av;
+      } else {
+        sm += v.y * __expf(v.x - m);
+        if (v.x == m && av < a) a = av;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+      const float s2 = __shfl_xor_sync(0xffffffffu, sm, o);
+      const int a2 = __shfl_xor_sync(0xffffffffu, a, o);
+      const float mn = fmaxf(m, m2);
+      const float snew = (m == -INFINITY ? 0.f : sm * __expf(m - mn)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mn));
+      int an;
+      if (m2 > m) an = a2;
+      else if (m > m2) an = a;
+      else an = min(a, a2);
+      m = mn;
+      sm = snew;
+      a = an;
+    }
+    if (lane == 0) {
+      conf[i] = 1.f / sm;
+      tok[i] = a;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int take = min(n_u, n);
+    for (int j = 0; j < n_u; ++j) {
+      dec_pos[s * n_u + j] = -1;
+      dec_tok[s * n_u + j] = -1;
+    }
+    for (int j = 0; j < take; ++j) {
+      int best = -1;
+      for (int i = 0; i < n; ++i) {
+        bool used = false;
+        for (int q = 0; q < j; ++q) used |= chosen[q] == i;
+        if (used) continue;
+        if (best < 0 || conf[i] > conf[best] || (conf[i] == conf[best] && rows[b0 + i] < rows[b0 + best])) best = i;
+      }
+      chosen[j] = best;
+      const int r = rows[b0 + best];
+      dec_pos[s * n_u + j] = r;
+      dec_tok[s * n_u + j] = tok[best];
+      tokens[r] = tok[best];
+    }
+  }
+  __syncthreads();
+  const int take = min(n_u, n);
+  for (int j = warp; j < take; j += nw) {
+    const int r = dec_pos[s * n_u + j];
+    const int t = dec_tok[s * n_u + j];
+    const uint4 *src = reinterpret_cast<const uint4 *>(emb + static_cast<int64_t>(t) * d);
+    uint4 *dst = reinterpret_cast<uint4 *>(H0 + static_cast<int64_t>(r) * d);
+    for (int c = lane; c < d / 8; c += 32) dst[c] = src[c];
+  }
+}
+
+// ============================================================================ K8: IH4 init
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ bf16 ih4_value(uint64_t key, uint64_t i, float scale) {
+  const uint64_t h = mix64(key + i);
+  const int S = static_cast<int>((h & 0xFFFF) + ((h >> 16) & 0xFFFF) + ((h >> 32) & 0xFFFF) + (h >> 48));
+  return __float2bfloat16_rn(__fmul_rn(static_cast<float>(S - 131070), scale));
+}
+// dst[(row_off + r) * cols + c] = IH4(key, (src_row(r)) * cols + c); rows listed by an optional
+// interleave: il > 0 -> dst row r belongs to stream A if (r % (2*il)) < il else stream B, with
+// source row (r / (2*il)) * il + r % il  (gate/up interleave of the SwiGLU GEMM, blocks of il).
+__global__ void ih4_fill_kernel(bf16 *__restrict__ dst, int64_t rows, int cols, uint64_t keyA, uint64_t keyB,
+                                int il, float scale) {
+  const int64_t n = rows * cols;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = e / cols, c = e - r * cols;
+    uint64_t key = keyA;
+    int64_t sr = r;
+    if (il > 0) {
+      const int64_t blk = r / (2 * il), w = r % (2 * il);
+      key = (w < il) ? keyA : keyB;
+      sr = blk * il + (w % il);
+    }
+    dst[e] = ih4_value(key, static_cast<uint64_t>(sr * cols + c), scale);
+  }
+}
+__global__ void fill_const_kernel(bf16 *__restrict__ dst, int64_t n, float v) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[e] = __float2bfloat16_rn(v);
+}
+
+// ============================================================================ launch wrappers
+static inline int grid_for(int64_t work, int per_block, int cap = 148 * 16) {
+  int64_t g = (work + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  return static_cast<int>(g < cap ? g : cap);
+}
+
+void launch_embed_rows(const int *tokens, const int *rows, const int *M_ptr, int M_cap, const bf16 *emb, bf16 *H0,
+                       int d, cudaStream_t st) {
+  embed_rows_kernel<<<grid_for(M_cap, 8), 256, 0, st>>>(tokens, rows, M_ptr, M_cap, emb, H0, d);
+}
+void launch_gather_rmsnorm(const bf16 *src, const int *idx, const int *M_ptr, int M_cap, const bf16 *g, float eps,
+                           bf16 *dst, int d, cudaStream_t st) {
+  gather_rmsnorm_kernel<<<grid_for(M_cap, 8), 256, 0, st>>>(src, idx, M_ptr, M_cap, g, eps, dst, d);
+}
+void launch_gather_rows(const bf16 *src, const int *idx, const int *M_ptr, int M_cap, bf16 *dst, int width,
+                        cudaStream_t st) {
+  gather_rows_kernel<<<grid_for(M_cap, 8), 256, 0, st>>>(src, idx, M_ptr, M_cap, dst, width);
+}
+void launch_scatter_rows(const bf16 *src, const int *idx, const int *M_ptr, int M_cap, bf16 *dst, int width,
+                         cudaStream_t st) {
+  scatter_rows_kernel<<<grid_for(M_cap, 8), 256, 0, st>>>(src, idx, M_ptr, M_cap, dst, width);
+}
+void launch_rmsnorm_rows(const bf16 *src, const int *M_ptr, int M_cap, const bf16 *g, float eps, bf16 *dst, int d,
+                         cudaStream_t st) {
+  gather_rmsnorm_kernel<<<grid_for(M_cap, 8), 256, 0, st>>>(src, nullptr, M_ptr, M_cap, g, eps, dst, d);
+}
+void launch_qkv_post(const bf16 *qkv, const int *idx, const int *M_ptr, int M_cap, const bf16 *bias, int N, int H,
+                     int KVH, int hd, float theta, bf16 *Qc, bf16 *Kc, bf16 *Vc, bf16 *dV, cudaStream_t st) {
+  const int g = M_cap < 148 * 8 ? M_cap : 148 * 8;
+  qkv_post_kernel<<<g > 0 ? g : 1, 256, 0, st>>>(qkv, idx, M_ptr, M_cap, bias, N, H, KVH, hd, log2f(theta), Qc, Kc,
+                                                 Vc, dV);
+}
+void launch_approx_rows(const int *idx_in, const int *off_in, int batch, int N, int row_lo, int *ap_rows,
+                        int *ap_off, cudaStream_t st) {
+  approx_rows_kernel<<<batch, 256, N, st>>>(idx_in, off_in, N, row_lo, ap_rows, ap_off, batch);
+}
+void launch_build_list(int mode, const int *carried, const int *carried_off, const int *dec_pos, int n_u, int policy,
+                       int batch, int N, int row_lo, int resp_lo, int *out, int *out_off, cudaStream_t st) {
+  build_list_kernel<<<1, 1024, N, st>>>(mode, carried, carried_off, dec_pos, n_u, policy, batch, N, row_lo, resp_lo,
+                                        out, out_off);
+}
+void launch_select(const bf16 *c_new, bf16 *c_cache, int batch, int N, int row_lo, int width, float tau, int cmp,
+                   int *idx_out, int *off_out, float *sim_out, unsigned *masks, unsigned *ticket, int *counts,
+                   cudaStream_t st) {
+  const int L = N - row_lo;
+  dim3 grid((L + kSelRowsPerCta - 1) / kSelRowsPerCta, batch);
+  select_salient_kernel<<<grid, 256, 0, st>>>(c_new, c_cache, N, row_lo, width, tau, cmp, idx_out, off_out, sim_out,
+                                              masks, ticket, counts);
+}
+void launch_lm_candidates(const int *tokens, int batch, int L_P, int L_R, int block, int mask_id, int *rows, int *off,
+                          cudaStream_t st) {
+  lm_candidates_kernel<<<1, 1024, 0, st>>>(tokens, batch, L_P, L_R, block, mask_id, rows, off);
+}
+void launch_lm_select_commit(const float4 *partials, int n_tiles, const int *rows, const int *off, int batch, int n_u,
+                             int *tokens, int *dec_pos, int *dec_tok, const bf16 *emb, bf16 *H0, int d,
+                             cudaStream_t st) {
+  lm_select_commit_kernel<<<batch, 256, 0, st>>>(partials, n_tiles, rows, off, n_u, tokens, dec_pos, dec_tok, emb, H0,
+                                                 d);
+}
+void launch_ih4_fill(bf16 *dst, int64_t rows, int cols, uint64_t keyA, uint64_t keyB, int il, float scale,
+                     cudaStream_t st) {
+  ih4_fill_kernel<<<148 * 8, 256, 0, st>>>(dst, rows, cols, keyA, keyB, il, scale);
+}
+void launch_fill_const(bf16 *dst, int64_t n, float v, cudaStream_t st) {
+  fill_const_kernel<<<148 * 4, 256, 0, st>>>(dst, n, v);
+}
+
+}  // namespace dy

@@ -1,0 +1,37 @@
+// kernels.h — launch wrappers of kernels.cu (all asynchronous on `st`).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+typedef __nv_bfloat16 bf16;
+
+namespace dy {
+void launch_embed_rows(const int *tokens, const int *rows, const int *M_ptr, int M_cap, const bf16 *emb, bf16 *H0,
+                       int d, cudaStream_t st);
+void launch_gather_rmsnorm(const bf16 *src, const int *idx, const int *M_ptr, int M_cap, const bf16 *g, float eps,
+                           bf16 *dst, int d, cudaStream_t st);
+void launch_gather_rows(const bf16 *src, const int *idx, const int *M_ptr, int M_cap, bf16 *dst, int width,
+                        cudaStream_t st);
+void launch_scatter_rows(const bf16 *src, const int *idx, const int *M_ptr, int M_cap, bf16 *dst, int width,
+                         cudaStream_t st);
+void launch_rmsnorm_rows(const bf16 *src, const int *M_ptr, int M_cap, const bf16 *g, float eps, bf16 *dst, int d,
+                         cudaStream_t st);
+void launch_qkv_post(const bf16 *qkv, const int *idx, const int *M_ptr, int M_cap, const bf16 *bias, int N, int H,
+                     int KVH, int hd, float theta, bf16 *Qc, bf16 *Kc, bf16 *Vc, bf16 *dV, cudaStream_t st);
+void launch_approx_rows(const int *idx_in, const int *off_in, int batch, int N, int row_lo, int *ap_rows,
+                        int *ap_off, cudaStream_t st);
+void launch_build_list(int mode, const int *carried, const int *carried_off, const int *dec_pos, int n_u, int policy,
+                       int batch, int N, int row_lo, int resp_lo, int *out, int *out_off, cudaStream_t st);
+void launch_select(const bf16 *c_new, bf16 *c_cache, int batch, int N, int row_lo, int width, float tau, int cmp,
+                   int *idx_out, int *off_out, float *sim_out, unsigned *masks, unsigned *ticket, int *counts,
+                   cudaStream_t st);
+void launch_lm_candidates(const int *tokens, int batch, int L_P, int L_R, int block, int mask_id, int *rows, int *off,
+                          cudaStream_t st);
+void launch_lm_select_commit(const float4 *partials, int n_tiles, const int *rows, const int *off, int batch, int n_u,
+                             int *tokens, int *dec_pos, int *dec_tok, const bf16 *emb, bf16 *H0, int d,
+                             cudaStream_t st);
+void launch_ih4_fill(bf16 *dst, int64_t rows, int cols, uint64_t keyA, uint64_t keyB, int il, float scale,
+                     cudaStream_t st);
+void launch_fill_const(bf16 *dst, int64_t n, float v, cudaStream_t st);
+}  // namespace dy

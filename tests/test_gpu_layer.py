@@ -1,0 +1,168 @@
+"""GPU parity of FullStep and the teacher-forced per-layer SparseStep against the oracle
+(north_star bars: salient sets bit-exact outside |s - tau| < 1e-3, hidden
+states / contexts within 2e-2 max relative error per row in bf16)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from synth import gen
+from gpu_helpers import (Model, bf16_round, from_dev, import_states, oracle_states, pack_lists,
+                               round_states, row_rel_err, to_dev_bf16, unpack_lists)
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+BAND = 1e-3
+
+
+@pytest.mark.parametrize("name", ["tiny", "small128", "small128_gqa"])
+def test_full_step_caches_match_oracle(name):
+    m = Model(name)
+    run = m.run
+    prompts = gen.prompt_tokens(11, run.batch, run.L_P, m.cfg.mask_id)
+    states = [O.init_state(p, m.cfg, run) for p in prompts]
+    for st in states:
+        st.tokens[run.L_P + 3] = 17                       # a few decoded tokens
+        O.full_step(st, m.W, m.cfg)
+    cache = m.new_cache()
+    toks = torch.tensor(np.stack([st.tokens for st in states]), dtype=torch.int32).cuda()
+    cache.init(toks)
+    torch.cuda.synchronize()
+    dy = m.dyllm
+    for l in range(m.cfg.n_layers):
+        for which, f in [(dy.K, "K"), (dy.V, "V"), (dy.Q, "Q"), (dy.CTX, "C"), (dy.H, "H")]:
+            got = from_dev(cache.tensor(l + 1 if which == dy.H else l, which))
+            ref = np.stack([getattr(st.caches[l], f) for st in states])
+            err = row_rel_err(got, ref).max()
+            assert err < TOL, (l, f, err)
+
+
+def _teacher_forced_layer(name, layer, mode, frac_in=0.4, seed=0):
+    m = Model(name, seed=seed)
+    cfg, run = m.cfg, m.run
+    N = run.N
+    prompts = gen.prompt_tokens(seed + 5, run.batch, run.L_P, cfg.mask_id)
+    states = round_states(oracle_states(m, prompts, steps=max(run.T_full, 1)))
+    rng = np.random.default_rng(seed + 99)
+    row_lo = 0 if mode == "fi" else run.L_P
+    input_rows = np.arange(row_lo, N)
+    idx_lists = [np.sort(rng.choice(input_rows, max(1, int(frac_in * len(input_rows))), replace=False))
+                 for _ in range(run.batch)]
+    # the previous layer changed the idx_in rows: perturb H_{layer} there (same values to both sides)
+    for st, idx in zip(states, idx_lists):
+        x = st.H0 if layer == 0 else st.caches[layer - 1].H
+        noise = rng.standard_normal((len(idx), cfg.d_model)) * 0.5 * np.abs(x[idx]).max(axis=1, keepdims=True)
+        x[idx] = bf16_round(x[idx] + noise)
+    cache = m.new_cache()
+    import_states(m, cache, states)
+    h_before = from_dev(cache.tensor(layer + 1, m.dyllm.H))
+    # oracle reference from the same (rounded) state
+    refs = []
+    for st, idx in zip(states, idx_lists):
+        x_all = st.H0 if layer == 0 else st.caches[layer - 1].H
+        lc = st.caches[layer].copy()
+        r = O.sparse_layer(x_all, lc, m.W["layers"][layer], cfg, idx, np.inf, input_rows,
+                           q_mode="cache")
+        refs.append((r, lc))
+    s_all = np.concatenate([r.s for r, _ in refs])
+    tau = float(np.quantile(s_all, 0.5))
+    # rerun the oracle with the chosen tau (tau only affects selection and the FFN rows)
+    refs = []
+    for st, idx in zip(states, idx_lists):
+        x_all = st.H0 if layer == 0 else st.caches[layer - 1].H
+        lc = st.caches[layer].copy()
+        r = O.sparse_layer(x_all, lc, m.W["layers"][layer], cfg, idx, tau, input_rows, q_mode="cache")
+        refs.append((r, lc))
+    idx_d, off_d = pack_lists(idx_lists, N)
+    out_d = torch.zeros(run.batch * N, dtype=torch.int32, device="cuda")
+    oof_d = torch.zeros(run.batch + 1, dtype=torch.int32, device="cuda")
+    sim_d = torch.full((run.batch * N,), -9.0, device="cuda")
+    cache.layer_step(layer, 0 if mode == "fi" else 1, idx_d, off_d, tau, out_d, oof_d, sim_d)
+    torch.cuda.synchronize()
+    got_lists = unpack_lists(out_d, oof_d, N)
+    sim = sim_d.cpu().numpy().reshape(run.batch, N)
+    dy = m.dyllm
+    C_gpu = from_dev(cache.tensor(layer, dy.CTX))
+    H_gpu = from_dev(cache.tensor(layer + 1, dy.H))
+    K_gpu = from_dev(cache.tensor(layer, dy.K))
+    V_gpu = from_dev(cache.tensor(layer, dy.V))
+    n_band = 0
+    for s, ((r, lc), idx) in enumerate(zip(refs, idx_lists)):
+        assert np.abs(sim[s, row_lo:] - r.s).max() < 2e-2
+        band = set(input_rows[np.abs(r.s - tau) < BAND].tolist())
+        n_band += len(band)
+        got, ref = set(got_lists[s].tolist()), set(r.idx_out.tolist())
+        assert got - band == ref - band, (s, sorted(got ^ ref))
+        # contexts of all input rows
+        assert row_rel_err(C_gpu[s, row_lo:], r.C).max() < TOL
+        # K/V rows of idx_in
+        assert row_rel_err(K_gpu[s, idx], lc.K[idx]).max() < TOL
+        assert row_rel_err(V_gpu[s, idx], lc.V[idx]).max() < TOL
+        # hidden rows: recomputed for the agreed selection, bit-unchanged elsewhere
+        agreed = sorted((got & ref))
+        sel = np.searchsorted(r.idx_out, agreed)
+        if len(agreed):
+            assert row_rel_err(H_gpu[s, agreed], r.out[sel]).max() < TOL
+        untouched = sorted(set(range(N)) - got)
+        assert np.array_equal(H_gpu[s, untouched], h_before[s, untouched])
+    assert n_band <= 0.05 * run.batch * len(input_rows) + 1
+    return m
+
+
+@pytest.mark.parametrize("name", ["tiny", "small128", "small128_gqa"])
+@pytest.mark.parametrize("layer", [0, 1])
+@pytest.mark.parametrize("mode", ["fi", "ro"])
+def test_layer_step_teacher_forced(name, layer, mode):
+    _teacher_forced_layer(name, layer, mode)
+
+
+def test_layer_step_all_salient_equals_full(name="small128"):
+    """tau > 1 and idx_in = all input rows -> the layer reproduces full recompute (GPU path)."""
+    m = Model(name)
+    cfg, run = m.cfg, m.run
+    N = run.N
+    prompts = gen.prompt_tokens(3, run.batch, run.L_P, cfg.mask_id)
+    toks = np.stack([np.concatenate([p, np.full(run.L_R, cfg.mask_id)]) for p in prompts])
+    cache = m.new_cache()
+    cache.init(torch.tensor(toks, dtype=torch.int32).cuda())
+    # change two tokens, refresh H0 rows, run all-salient layer steps, compare with a fresh full step
+    toks2 = toks.copy()
+    toks2[:, run.L_P + 1] = 5
+    H0 = cache.tensor(0, m.dyllm.H)
+    emb = to_dev_bf16(m.W["emb"])
+    H0.copy_(emb[torch.tensor(toks2, dtype=torch.long).cuda()])
+    idx, off = pack_lists([np.arange(N)] * run.batch, N)
+    outs = [(torch.zeros_like(idx), torch.zeros_like(off)) for _ in range(cfg.n_layers)]
+    cur = (idx, off)
+    for l in range(cfg.n_layers):
+        cache.layer_step(l, 0, cur[0], cur[1], 2.0, outs[l][0], outs[l][1])
+        cur = outs[l]
+    torch.cuda.synchronize()
+    assert int(cur[1][-1]) == run.batch * N
+    HL = from_dev(cache.tensor(cfg.n_layers, m.dyllm.H))
+    ref = m.new_cache()
+    ref.init(torch.tensor(toks2, dtype=torch.int32).cuda())
+    torch.cuda.synchronize()
+    HR = from_dev(ref.tensor(cfg.n_layers, m.dyllm.H))
+    assert row_rel_err(HL, HR).max() < TOL
+
+
+def test_layer_step_none_salient_keeps_hidden():
+    m = Model("small128")
+    cfg, run = m.cfg, m.run
+    N = run.N
+    prompts = gen.prompt_tokens(4, run.batch, run.L_P, cfg.mask_id)
+    toks = np.stack([np.concatenate([p, np.full(run.L_R, cfg.mask_id)]) for p in prompts])
+    cache = m.new_cache()
+    cache.init(torch.tensor(toks, dtype=torch.int32).cuda())
+    torch.cuda.synchronize()
+    before = [cache.tensor(l + 1, m.dyllm.H).clone() for l in range(cfg.n_layers)]
+    idx, off = pack_lists([np.arange(run.L_P, N)] * run.batch, N)
+    o_idx, o_off = torch.zeros_like(idx), torch.zeros_like(off)
+    for l in range(cfg.n_layers):
+        cache.layer_step(l, 1, idx, off, -2.0, o_idx, o_off)
+        torch.cuda.synchronize()
+        assert int(o_off[-1]) == 0
+        idx, off = o_idx.clone(), o_off.clone()
+    for l in range(cfg.n_layers):
+        assert torch.equal(cache.tensor(l + 1, m.dyllm.H), before[l])
