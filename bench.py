@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (0 = config)")
     ap.add_argument("--frac", type=float, default=0.10, help="target salient fraction for tau calibration")
     ap.add_argument("--tau", type=float, default=None, help="fixed tau for all layers (skips calibration)")
+    ap.add_argument("--select-mode", default="fraction", choices=["fraction", "tau"],
+                    help="fraction: per-layer salient fraction --frac (D19); tau: fixed/calibrated threshold")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
@@ -244,6 +246,29 @@ def calibrate_tau(eng, dy, cfg, run, frac, n_sparse=2):
     return taus, fracs
 
 
+def algo_cost(cls, cfg, run, M_in, M_out, L_tot):
+    """Algorithmic HBM bytes and flops of one launch of a kernel class."""
+    d, qw, kw, F = cfg.d_model, cfg.q_width, cfg.kv_width, cfg.d_ff
+    b, N = run.batch, run.N
+    if cls == "qkv_gemm":
+        return 2 * d * (qw + 2 * kw) + M_in * 2 * (d + qw + 2 * kw), 2.0 * M_in * d * (qw + 2 * kw)
+    if cls == "o_gemm":
+        return 2 * qw * d + M_out * 2 * (qw + 2 * d), 2.0 * M_out * qw * d
+    if cls == "gu_gemm":
+        return 2 * d * 2 * F + M_out * 2 * (d + F), 2.0 * M_out * d * 2 * F
+    if cls == "down_gemm":
+        return 2 * F * d + M_out * 2 * (F + 2 * d), 2.0 * M_out * F * d
+    if cls == "attn":
+        sal = M_in / b
+        return (b * N * 2 * kw * 2 + L_tot * 3 * qw * 2,
+                2.0 * L_tot * N * qw + 2.0 * M_in * N * qw + 2.0 * (L_tot - M_in) * sal * qw * 2)
+    if cls == "select":
+        return L_tot * 3 * qw * 2, 6.0 * L_tot * qw
+    if cls == "lm_gemm":
+        return 2 * d * cfg.vocab + M_in * 2 * d, 2.0 * M_in * d * cfg.vocab
+    return None, None
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -255,33 +280,38 @@ def main():
 
     from synth import configs, gen
     from paper_2603_08026_b200 import dyllm as dy
+    from paper_2603_08026_b200 import dist as pd
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    rank, world, local = pd.env_rank()
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     torch.cuda.set_device(local)
     cfg, run = configs.preset(args.config)
     if args.batch:
         run = replace(run, batch=args.batch)
+    fmode = args.select_mode == "fraction"
+    run = replace(run, select_mode=1 if fmode else 0)
     b, N = run.batch, run.N
 
     ctx = dy.Context(local)
     w = dy.Weights.random(ctx, cfg, seed=args.seed)
     eng = dy.Engine(ctx, w, run)
-    # per-rank shard of the global batch: sequences [rank*b, (rank+1)*b) of the synthetic set
-    prompts_all = gen.prompt_tokens(args.seed + 1000 * rank, b, run.L_P, cfg.mask_id)
+    # per-rank shard of the global batch (weak scaling: b sequences per GPU)
+    lo, hi = pd.shard_range(b * world, world, rank)
+    prompts_all = gen.prompt_tokens(args.seed, b * world, run.L_P, cfg.mask_id)[lo:hi]
     prompts_dev = torch.tensor(prompts_all, dtype=torch.int32, device=f"cuda:{local}")
     prompts_host = torch.tensor(prompts_all, dtype=torch.int32).pin_memory()
     out_host = torch.empty((b, N), dtype=torch.int32).pin_memory()
 
-    # ---- tau calibration (untimed)
-    eng.tokens[:, : run.L_P].copy_(prompts_dev)
-    if args.tau is None:
-        taus, cal_fracs = calibrate_tau(eng, dy, cfg, run, args.frac)
+    # ---- selection thresholds (untimed)
+    cal_fracs = []
+    if fmode:
+        taus = np.full(cfg.n_layers, args.frac, np.float32)
+    elif args.tau is not None:
+        taus = np.full(cfg.n_layers, args.tau, np.float32)
     else:
-        taus, cal_fracs = np.full(cfg.n_layers, args.tau, np.float32), []
+        eng.tokens[:, : run.L_P].copy_(prompts_dev)
+        taus, cal_fracs = calibrate_tau(eng, dy, cfg, run, args.frac)
 
     stream = ctx.stream
 
@@ -307,10 +337,9 @@ def main():
     launches = (dy.lib().dyllm_launch_count() - l0) // max(args.steps, 1)
     ms = ev0.elapsed_time(ev1)
     clk = clocks.stop()
-    sal = eng.sal_counts.cpu().numpy()                   # [T][n_layers][b] of the last generation
     if world > 1:
         dist.barrier()
-    # ---- e2e through the public API (pinned H2D prompts, D2H tokens)
+    # ---- e2e through the public API (pinned H2D prompts, D2H tokens) — same workload
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -319,25 +348,21 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     ms_e2e = e0.elapsed_time(e1)
-    # ---- per-kernel events (separate untimed generation, same workload)
+    # ---- per-kernel CUDA events (one extra generation, same workload, untimed)
     ctx.profile(True)
-    for _ in range(args.profile_steps):
+    for _ in range(max(args.profile_steps, 1)):
         one_generation()
     torch.cuda.synchronize()
-    kc = {}
     names = ["qkv_gemm", "qkv_post", "attn", "select", "o_gemm", "gu_gemm", "down_gemm", "gather", "scatter",
              "lm_gemm", "other"]
+    kc = {}
     for i, n in enumerate(names):
         kc[n] = ctx.profile_read(i)
         kc["full_" + n] = ctx.profile_read(16 + i)
     ctx.profile(False)
-    sal_prof = eng.sal_counts.cpu().numpy()
+    sal = eng.sal_counts.cpu().numpy().astype(np.float64)     # [T][n_layers][b] of the profiled generation
 
-    # ---- max over ranks
-    t_dev = torch.tensor([ms, ms_e2e], dtype=torch.float64, device=f"cuda:{local}")
-    if world > 1:
-        dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
-    ms, ms_e2e = t_dev.tolist()
+    ms, ms_e2e = pd.max_over_ranks([ms, ms_e2e], device=f"cuda:{local}")
     tokens = world * b * run.L_R * args.steps
     value = tokens / (ms / 1000.0)
     e2e = tokens / (ms_e2e / 1000.0)
@@ -345,51 +370,61 @@ def main():
     if rank == 0:
         hbm, tf_burst, tf_sus, src = peaks()
         T = run.T_total
+        nsteps = args.profile_steps
         sparse_t = [t for t in range(T) if t >= run.T_full]
-        in_rows = np.array([b * (N if t % run.full_period == 0 else run.L_R) for t in sparse_t], dtype=np.float64)
-        sel = sal_prof[sparse_t].sum(axis=2).astype(np.float64)        # [steps][layers] selected rows
-        f_layer = (sel / in_rows[:, None]).mean(axis=0)
-        # dominant kernel of the timed workload = the class with the largest total event time
+        L_in = np.array([b * (N if t % run.full_period == 0 else run.L_R) for t in sparse_t], dtype=np.float64)
+        m_out = sal[sparse_t].sum(axis=2)                          # [steps][layers]
+        m_in = np.zeros_like(m_out)
+        m_in[:, 1:] = m_out[:, :-1]
+        prev_last = np.concatenate([[b * run.L_R], m_out[:-1, -1]])
+        m_in[:, 0] = np.minimum(L_in, prev_last + b * run.n_u)
+        f_layer = (m_out / L_in[:, None]).mean(axis=0)
         totals = {k: float(v.sum()) for k, v in kc.items() if len(v)}
-        dom = max(totals, key=totals.get)
-        lb = layer_bytes_flops(cfg)
-        # algorithmic bytes / flops per launch for the sparse-step GEMMs (M = rows of the launch)
-        d, F, qw, kw = cfg.d_model, cfg.d_ff, cfg.q_width, cfg.kv_width
-        m_out = sel.ravel()                                           # launch order: step-major, layer-minor
-        m_in_layers = np.concatenate([[0], np.zeros(0)])
-        roof = None
-        if dom in ("gu_gemm", "down_gemm", "o_gemm"):
-            wbytes = {"gu_gemm": lb["gu_w"], "down_gemm": lb["down_w"], "o_gemm": lb["o_w"]}[dom]
-            act = {"gu_gemm": (2 * d + 2 * F), "down_gemm": (2 * F + 4 * d), "o_gemm": (2 * qw + 4 * d)}[dom]
-            flop = {"gu_gemm": 2 * d * 2 * F, "down_gemm": 2 * F * d, "o_gemm": 2 * qw * d}[dom]
-            times = kc[dom] / 1000.0
-            n = min(len(times), len(m_out))
-            byts = wbytes + act * m_out[:n]
-            flops = flop * m_out[:n]
-            t_hbm = byts / (hbm * 1e9)
-            t_tc = flops / (tf_sus * 1e12)
-            bound = "hbm" if t_hbm.sum() >= t_tc.sum() else "tensor"
-            if bound == "hbm":
-                ach = byts.sum() / times[:n].sum() / 1e9
-                roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm}
+        tot_all = sum(totals.values())
+        per_class = {}
+        for k, v in kc.items():
+            if not len(v):
+                continue
+            full = k.startswith("full_")
+            base = k[5:] if full else k
+            if full:
+                Mi = Mo = float(b * N)
+                Lt = np.full(len(v), float(b * N))
+                by, fl = algo_cost(base, cfg, run, Mi, Mo, b * N)
+                if base == "lm_gemm":
+                    by, fl = algo_cost(base, cfg, run, b * run.n_u * run.block, 0, 0)
+                if by is None:
+                    continue
+                bys, fls = np.full(len(v), by), np.full(len(v), fl)
+            elif base == "lm_gemm":
+                by, fl = algo_cost(base, cfg, run, float(b * run.block), 0, 0)
+                bys, fls = np.full(len(v), by), np.full(len(v), fl)
             else:
-                ach = flops.sum() / times[:n].sum() / 1e12
-                roof = {"bound": "tensor", "achieved": ach, "peak": tf_sus, "unit": "TFLOP/s", "frac": ach / tf_sus}
-        elif dom.startswith("full_") and dom.endswith("gemm"):
-            k = dom[5:]
-            Mrows = b * N
-            flop = {"qkv_gemm": 2 * d * (qw + 2 * kw), "o_gemm": 2 * qw * d, "gu_gemm": 4 * d * F,
-                    "down_gemm": 2 * F * d, "lm_gemm": 2 * d * cfg.vocab}[k] * Mrows
-            ach = flop * len(kc[dom]) / (kc[dom].sum() / 1000.0) / 1e12
-            roof = {"bound": "tensor", "achieved": ach, "peak": tf_sus, "unit": "TFLOP/s", "frac": ach / tf_sus}
-        if roof is None:
-            roof = {"bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None}
-        roof.update({"kernel": dom, "traffic": None, "peak_source": src + (" sustained" if roof["unit"] == "TFLOP/s" else ""),
-                     "launches_timed": int(len(kc[dom])), "avg_launch_us": float(kc[dom].mean() * 1000.0)})
-        share = {k: round(v / sum(totals.values()), 4) for k, v in sorted(totals.items(), key=lambda x: -x[1])}
-        # per-mode step times from the profiled generation are in `share`; full-recompute extrapolation
-        full_ms = sum(float(v.sum()) for k, v in kc.items() if k.startswith("full_")) / max(run.T_full, 1)
-        full_tok_s = b * run.L_R / (T * full_ms / 1000.0) * world if full_ms > 0 else None
+                Mi, Mo = m_in.ravel(), m_out.ravel()
+                Lt = np.repeat(L_in, cfg.n_layers)
+                n = min(len(v), len(Mi) * nsteps)
+                Mi, Mo, Lt = np.tile(Mi, nsteps)[:n], np.tile(Mo, nsteps)[:n], np.tile(Lt, nsteps)[:n]
+                by, fl = algo_cost(base, cfg, run, Mi, Mo, Lt)
+                if by is None:
+                    continue
+                bys, fls = np.broadcast_to(by, (n,)).astype(np.float64), np.broadcast_to(fl, (n,)).astype(np.float64)
+                v = v[:n]
+            t_s = v.sum() / 1000.0
+            B, Fl = float(bys.sum()), float(fls.sum())
+            bound = "hbm" if B / (hbm * 1e9) >= Fl / (tf_sus * 1e12) else "tensor"
+            if bound == "hbm":
+                ach, peak, unit = B / t_s / 1e9, hbm, "GB/s"
+            else:
+                ach, peak, unit = Fl / t_s / 1e12, tf_sus, "TFLOP/s"
+            per_class[k] = {"bound": bound, "achieved": round(ach, 1), "peak": peak, "unit": unit,
+                            "frac": round(ach / peak, 4), "share": round(totals[k] / tot_all, 4),
+                            "avg_us": round(float(v.mean()) * 1000.0, 2), "launches": int(len(v))}
+        dom = max(per_class, key=lambda k: totals[k])
+        roof = dict(per_class[dom])
+        roof.update({"kernel": dom, "traffic": None,
+                     "peak_source": src + (" sustained bf16" if roof["unit"] == "TFLOP/s" else " HBM copy")})
+        full_ms = sum(float(v.sum()) for k, v in kc.items() if k.startswith("full_")) / max(run.T_full * nsteps, 1)
+        full_tok_s = world * b * run.L_R / (T * full_ms / 1000.0) if full_ms > 0 else None
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             cpu = cpu_oracle_sample(cfg, run, args.cpu_seconds, args.frac)
@@ -398,13 +433,13 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"{args.config}: L_P={run.L_P} L_R={run.L_R} block={run.block} "
-                                   f"n_u={run.n_u} T={T} (T_full={run.T_full}, period={run.full_period}) "
-                                   f"random-init bf16 weights, one step = one full generation",
+                                   f"n_u={run.n_u} T={T} (T_full={run.T_full}, period={run.full_period}); "
+                                   f"random-init bf16 weights; one step = one full generation",
                        "global_batch": b * world, "per_gpu_batch": b, "seq_len": N,
                        "parallelism": f"dp{world} (batch-parallel replicas)",
                        "l2": "inputs larger than L2 (14 GB of weights streamed per denoising step)",
-                       "tau": "per-layer, calibrated to salient fraction %.2f" % args.frac if args.tau is None
-                       else args.tau},
+                       "selection": (f"fraction-controlled f={args.frac} per layer and sequence (D19)" if fmode
+                                     else f"fixed tau per layer {np.round(taus, 6).tolist()}")},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(b * run.L_P * 4),
                     "d2h_bytes_per_step": int(b * N * 4)},
             "gpu_launches": int(launches),
@@ -412,9 +447,9 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
             "salient_fraction": {"per_layer_mean": [round(float(x), 4) for x in f_layer],
-                                 "run_mean": float(f_layer.mean()),
+                                 "run_mean": round(float(f_layer.mean()), 4),
                                  "calibration": [[round(x, 4) for x in fr] for fr in cal_fracs]},
-            "kernel_time_share": share,
+            "kernels": per_class,
             "full_recompute": {"ms_per_full_step": full_ms, "tokens_per_s_extrapolated": full_tok_s,
                                "speedup": (value / full_tok_s) if full_tok_s else None},
         }

@@ -68,6 +68,10 @@ typedef struct {
   int32_t full_period;   /* sparse step takes Concat(P,R) when t % full_period == 0 */
   int32_t layer1_policy; /* 0: carried (Alg. 1 literal); 1: carried ∪ decoded (D5, default) */
   int32_t cmp;           /* 0: s < tau (Alg. 3, D1); 1: s <= tau (§3.2) */
+  int32_t select_mode;   /* 0: fixed threshold, the `tau` arguments are tau (the paper's rule);
+                            1: fraction-controlled (D19), the `tau` arguments are fractions f in [0,1]
+                               and every layer of every sequence thresholds at its own f-quantile of s
+                               (tau* = similarity of rank round(f*L), strict '<') */
 } dyllm_run_cfg;
 
 /* input_mode of dyllm_layer_step / dyllm_select_salient */

@@ -225,6 +225,16 @@ class SparseLayerResult:
     dV: np.ndarray               # V_new[idx_in] - V_cache[idx_in]
 
 
+def quantile_threshold(s_all, frac):
+    """Fraction-controlled threshold (DESIGN D19, the bench's stand-in for a calibrated tau):
+    tau* = the (k+1)-th smallest similarity with k = round(frac * n), so that the strict rule
+    s < tau* selects exactly the k least similar rows when there are no ties (+inf if k >= n)."""
+    s_all = np.sort(np.asarray(s_all, dtype=np.float64).ravel())
+    n = s_all.size
+    k = int(np.floor(frac * n + 0.5))
+    return np.inf if k >= n else float(s_all[k])
+
+
 def sparse_layer(x_all, cache, w, cfg, idx_in, tau, input_rows, cmp=0, q_mode="literal",
                  q_extra=()):
     """One layer of SparseStep (Alg. 3 lines 3-17), in Alg. 3's order.
@@ -235,6 +245,7 @@ def sparse_layer(x_all, cache, w, cfg, idx_in, tau, input_rows, cmp=0, q_mode="l
     input_rows : global positions that form this step's input (all N, or the response)
     q_mode     : "literal" -> Q for all input rows (P:876);
                  "cache"   -> Q recomputed only for idx_in ∪ q_extra, rest from the Q cache (D6)
+    tau        : a float, or a callable s -> tau (used by the fraction-controlled mode)
     """
     input_rows = np.asarray(input_rows, dtype=np.int64)
     idx_in = np.asarray(idx_in, dtype=np.int64)
@@ -271,6 +282,8 @@ def sparse_layer(x_all, cache, w, cfg, idx_in, tau, input_rows, cmp=0, q_mode="l
     C[pos_in_input] = c_sal
     # line 12: idx <- Where(CosSim(C, C_cache) < tau)
     s = cosine_rows(C, cache.C[input_rows])
+    if callable(tau):
+        tau = tau(s)
     idx_out = select_salient(s, tau, input_rows, cmp)
     # lines 13-15: x <- LN(OutProj(C)); x[idx] <- FFN(x[idx]); x[~idx] <- FFN_OUT_cache[~idx]
     #  (D8: OutProj / FFN evaluated only on the rows whose result is used)
@@ -393,7 +406,10 @@ def sparse_step(st, W, cfg, run, mode, tau, q_mode="cache"):
     counts = []
     taus = np.broadcast_to(np.asarray(tau, dtype=np.float64), (cfg.n_layers,))
     for l, lw in enumerate(W["layers"]):
-        r = sparse_layer(x_all, st.caches[l], lw, cfg, idx, taus[l], input_rows, run.cmp,
+        thr = taus[l]
+        if getattr(run, "select_mode", 0) == 1:              # fraction-controlled (D19)
+            thr = (lambda s, f=taus[l]: quantile_threshold(s, f))
+        r = sparse_layer(x_all, st.caches[l], lw, cfg, idx, thr, input_rows, run.cmp,
                          q_mode=q_mode, q_extra=q_extra if l == 0 else ())
         idx = r.idx_out
         counts.append(len(idx))

@@ -116,6 +116,7 @@ struct dyllm_cache {
   bool carried_valid = false;
   int *ap_rows, *ap_off, *all_rows, *all_off, *zero_off, *lm_rows, *lm_off;
   int *dec_prev;
+  float *sim;  // per-row similarity scratch (fraction mode)
   bool have_dec_prev = false;
   bool initialized = false;
   std::vector<void *> allocs;
@@ -368,7 +369,8 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
   const dyllm_model_cfg &m = w->cfg;
   if (r->batch < 1 || r->batch > 1024 || r->L_P < 1 || r->L_R < 1 || r->block < 1 || r->block > 256 ||
       r->L_R % r->block || r->n_u < 1 || r->n_u > 64 || r->n_u > r->block || r->T_full < 0 || r->full_period < 1 ||
-      r->layer1_policy < 0 || r->layer1_policy > 1 || r->cmp < 0 || r->cmp > 1 || r->L_P + r->L_R > 32768) {
+      r->layer1_policy < 0 || r->layer1_policy > 1 || r->cmp < 0 || r->cmp > 1 || r->L_P + r->L_R > 32768 ||
+      r->select_mode < 0 || r->select_mode > 1) {
     set_error("run cfg out of range (batch<=1024, block<=256 | L_R, n_u<=min(64,block), N<=32768)");
     return DYLLM_E_ARG;
   }
@@ -425,6 +427,7 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
   AL(c->lm_rows, lm_cap);
   AL(c->lm_off, r->batch + 1);
   AL(c->dec_prev, static_cast<int64_t>(r->batch) * r->n_u);
+  AL(c->sim, rows);
 #undef AL
   cudaStream_t st = ctx->stream;
   if (cudaMemsetAsync(c->zero_off, 0, (r->batch + 1) * sizeof(int), st) != cudaSuccess) {
@@ -580,8 +583,9 @@ static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *
   a.scale = 1.f / sqrtf(static_cast<float>(m.head_dim));
   KL(ATTN, RET(attention_launch(a, st)));
   // a5: cosine similarity + threshold + compaction; C_cache <- Cn for the input rows
-  KL(SELECT, launch_select(c->Cn, C.C, b, N, row_lo, qw, tau, c->r.cmp, idx_out, off_out, sim, ctx->masks, ctx->ticket,
-                           counts, st));
+  const bool fmode = c->r.select_mode == 1;
+  KL(SELECT, launch_select(c->Cn, C.C, b, N, row_lo, qw, fmode ? 2.f : tau, c->r.cmp, fmode ? tau : -1.f, idx_out,
+                           off_out, (fmode && !sim) ? c->sim : sim, ctx->masks, ctx->ticket, counts, st));
   const int *M_out = off_out + b;
   // a6 + a7 on idx_out, a8 scatter-back into H_l (other rows keep FFN_OUT_cache)
   KL(GATHER, launch_gather_rows(C.C, idx_out, M_out, rows, c->Cg, qw, st));
@@ -790,7 +794,7 @@ int dyllm_select_salient(dyllm_ctx *ctx, int batch, int N, int row_lo, int width
   CHECK_ARG(words <= kMaskCap, "select_salient: too many rows");
   RET(sticky(ctx));
   KL(SELECT, launch_select(static_cast<const bf16 *>(d_c_new), static_cast<bf16 *>(d_c_cache), batch, N, row_lo, width,
-                           tau, cmp, d_idx_out, d_off_out, d_sim_out, ctx->masks, ctx->ticket, nullptr, ctx->stream));
+                           tau, cmp, -1.f, d_idx_out, d_off_out, d_sim_out, ctx->masks, ctx->ticket, nullptr, ctx->stream));
   DY_CUDA(cudaGetLastError());
   return DYLLM_OK;
 }

@@ -229,7 +229,7 @@ constexpr int kSelRowsPerCta = 32;
 
 __global__ void __launch_bounds__(256) select_salient_kernel(
     const bf16 *__restrict__ c_new, bf16 *__restrict__ c_cache, int N, int row_lo, int width, float tau,
-    int cmp, int *__restrict__ idx_out, int *__restrict__ off_out, float *__restrict__ sim_out,
+    int cmp, float frac, int *__restrict__ idx_out, int *__restrict__ off_out, float *__restrict__ sim_out,
     unsigned *__restrict__ masks, unsigned *__restrict__ ticket, int *__restrict__ counts_out) {
   __shared__ unsigned row_flag[kSelRowsPerCta];
   __shared__ bool is_last;
@@ -291,6 +291,73 @@ __global__ void __launch_bounds__(256) select_salient_kernel(
   const int batch = gridDim.y;
   const int nwords = batch * nchunks;
   __shared__ int seq_base[1025];
+  if (frac >= 0.f) {
+    // fraction-controlled mode (D19): per sequence, tau* = the similarity of rank k = round(f*L)
+    // (0-based) found by an 8-bit radix select over the order-preserving uint32 keys of s, then
+    // the masks are rebuilt as s < tau* (k rows when there are no ties).
+    __shared__ unsigned hist[8][256];
+    for (int sq = warp; sq < batch; sq += 8) {
+      const float *sv = sim_out + static_cast<int64_t>(sq) * N + row_lo;
+      const int k = static_cast<int>(floorf(frac * L + 0.5f));
+      float thr = INFINITY;
+      if (k < L) {
+        uint32_t prefix = 0, pmask = 0;
+        int rank = k;
+        for (int shift = 24; shift >= 0; shift -= 8) {
+          for (int i = lane; i < 256; i += 32) hist[warp][i] = 0;
+          __syncwarp();
+          for (int i = lane; i < L; i += 32) {
+            const uint32_t u = __float_as_uint(__ldcg(sv + i));
+            const uint32_t key = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+            if ((key & pmask) == prefix) atomicAdd(&hist[warp][(key >> shift) & 255u], 1u);
+          }
+          __syncwarp();
+          unsigned loc[8], sum = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            loc[j] = hist[warp][lane * 8 + j];
+            sum += loc[j];
+          }
+          unsigned incl = sum;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+          }
+          const unsigned excl = incl - sum;
+          const bool mine = static_cast<unsigned>(rank) >= excl && static_cast<unsigned>(rank) < incl;
+          const unsigned bal = __ballot_sync(0xffffffffu, mine);
+          const int src = __ffs(bal) - 1;
+          int digit = 0, nrank = 0;
+          if (lane == src) {
+            unsigned c = excl;
+            for (int j = 0; j < 8; ++j) {
+              if (static_cast<unsigned>(rank) < c + loc[j]) {
+                digit = lane * 8 + j;
+                nrank = rank - static_cast<int>(c);
+                break;
+              }
+              c += loc[j];
+            }
+          }
+          digit = __shfl_sync(0xffffffffu, digit, src);
+          rank = __shfl_sync(0xffffffffu, nrank, src);
+          prefix |= static_cast<uint32_t>(digit) << shift;
+          pmask |= 255u << shift;
+          __syncwarp();
+        }
+        const uint32_t u = (prefix & 0x80000000u) ? (prefix & 0x7FFFFFFFu) : ~prefix;
+        thr = __uint_as_float(u);
+      }
+      for (int w = 0; w < nchunks; ++w) {
+        const int i = w * kSelRowsPerCta + lane;
+        const bool fl = i < L && __ldcg(sv + i) < thr;
+        const unsigned m = __ballot_sync(0xffffffffu, fl);
+        if (lane == 0) masks[sq * nchunks + w] = m;
+      }
+    }
+    __syncthreads();
+  }
   // per-sequence counts (one warp per sequence, strided)
   for (int sq = warp; sq < batch; sq += 8) {
     int c = 0;
@@ -549,12 +616,12 @@ void launch_build_list(int mode, const int *carried, const int *carried_off, con
                                         out, out_off);
 }
 void launch_select(const bf16 *c_new, bf16 *c_cache, int batch, int N, int row_lo, int width, float tau, int cmp,
-                   int *idx_out, int *off_out, float *sim_out, unsigned *masks, unsigned *ticket, int *counts,
-                   cudaStream_t st) {
+                   float frac, int *idx_out, int *off_out, float *sim_out, unsigned *masks, unsigned *ticket,
+                   int *counts, cudaStream_t st) {
   const int L = N - row_lo;
   dim3 grid((L + kSelRowsPerCta - 1) / kSelRowsPerCta, batch);
-  select_salient_kernel<<<grid, 256, 0, st>>>(c_new, c_cache, N, row_lo, width, tau, cmp, idx_out, off_out, sim_out,
-                                              masks, ticket, counts);
+  select_salient_kernel<<<grid, 256, 0, st>>>(c_new, c_cache, N, row_lo, width, tau, cmp, frac, idx_out, off_out,
+                                              sim_out, masks, ticket, counts);
 }
 void launch_lm_candidates(const int *tokens, int batch, int L_P, int L_R, int block, int mask_id, int *rows, int *off,
                           cudaStream_t st) {

@@ -24,8 +24,8 @@ void launch_approx_rows(const int *idx_in, const int *off_in, int batch, int N, 
 void launch_build_list(int mode, const int *carried, const int *carried_off, const int *dec_pos, int n_u, int policy,
                        int batch, int N, int row_lo, int resp_lo, int *out, int *out_off, cudaStream_t st);
 void launch_select(const bf16 *c_new, bf16 *c_cache, int batch, int N, int row_lo, int width, float tau, int cmp,
-                   int *idx_out, int *off_out, float *sim_out, unsigned *masks, unsigned *ticket, int *counts,
-                   cudaStream_t st);
+                   float frac, int *idx_out, int *off_out, float *sim_out, unsigned *masks, unsigned *ticket,
+                   int *counts, cudaStream_t st);
 void launch_lm_candidates(const int *tokens, int batch, int L_P, int L_R, int block, int mask_id, int *rows, int *off,
                           cudaStream_t st);
 void launch_lm_select_commit(const float4 *partials, int n_tiles, const int *rows, const int *off, int batch, int n_u,

@@ -40,11 +40,12 @@ class ModelCfg(C.Structure):
 class RunCfg(C.Structure):
     _fields_ = [("batch", C.c_int32), ("L_P", C.c_int32), ("L_R", C.c_int32), ("block", C.c_int32),
                 ("n_u", C.c_int32), ("T_full", C.c_int32), ("full_period", C.c_int32),
-                ("layer1_policy", C.c_int32), ("cmp", C.c_int32)]
+                ("layer1_policy", C.c_int32), ("cmp", C.c_int32), ("select_mode", C.c_int32)]
 
     @classmethod
     def from_py(cls, r):
-        return cls(r.batch, r.L_P, r.L_R, r.block, r.n_u, r.T_full, r.full_period, r.layer1_policy, r.cmp)
+        return cls(r.batch, r.L_P, r.L_R, r.block, r.n_u, r.T_full, r.full_period, r.layer1_policy, r.cmp,
+                   getattr(r, "select_mode", 0))
 
 
 def _load():

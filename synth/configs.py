@@ -23,6 +23,7 @@ class ModelCfg:
     qkv_bias: bool = False
     residual_mode: int = 0      # 0 = pre-norm residual block (LLaDA/Dream), 1 = paper_literal Alg.2/3
     w_std: float = 0.02         # std of every projection / embedding / lm-head weight
+    qk_std: float = 0.0         # std of W_q / W_k (0 -> w_std); the sigma_qk sharpness knob
     name: str = ""
 
     @property
@@ -48,6 +49,7 @@ class RunCfg:
     full_period: int = 4        # full-input sparse step when t % period == 0
     layer1_policy: int = 1      # 0 = carried (Alg.1 literal), 1 = carried ∪ decoded (DESIGN D5)
     cmp: int = 0                # 0 = strict '<' (Alg.3), 1 = '<=' (§3.2)
+    select_mode: int = 0        # 0 = fixed threshold tau (paper); 1 = per-sequence fraction f (D19)
 
     @property
     def N(self) -> int:

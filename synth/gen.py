@@ -3,7 +3,8 @@
 Every element of every tensor is a pure function of (seed, stream, element
 index), so any element can be regenerated independently (used for sampled
 parity at full size). The CUDA library implements the same generator in
-csrc/init.cu ("input recipe"); nothing here is DyLLM arithmetic.
+csrc/kernels.cu:ih4_fill_kernel ("input recipe"); nothing here is DyLLM
+arithmetic.
 
 Definition (all integer arithmetic mod 2**64):
     mix64(x):  z = x + 0x9E3779B97F4A7C15
@@ -117,9 +118,10 @@ def layer_weights(cfg, seed: int, layer: int, dtype=np.float64) -> dict:
     """One layer's weights in torch-Linear layout W[out][in] (y = x @ W.T)."""
     d, qw, kw, F = cfg.d_model, cfg.q_width, cfg.kv_width, cfg.d_ff
     s = cfg.w_std
+    sqk = cfg.qk_std or cfg.w_std
     w = {
-        "wq": ih4_normal(seed, stream_id(layer, "wq"), (qw, d), s, dtype),
-        "wk": ih4_normal(seed, stream_id(layer, "wk"), (kw, d), s, dtype),
+        "wq": ih4_normal(seed, stream_id(layer, "wq"), (qw, d), sqk, dtype),
+        "wk": ih4_normal(seed, stream_id(layer, "wk"), (kw, d), sqk, dtype),
         "wv": ih4_normal(seed, stream_id(layer, "wv"), (kw, d), s, dtype),
         "wo": ih4_normal(seed, stream_id(layer, "wo"), (d, qw), s, dtype),
         "w_gate": ih4_normal(seed, stream_id(layer, "w_gate"), (F, d), s, dtype),

@@ -63,7 +63,7 @@ def test_gemm_residual_and_bias(dy, ctx):
 def test_select_salient_vs_oracle(dy, ctx, b, N, row_lo, width):
     rng = np.random.default_rng(b * 1000 + N)
     old = rng.standard_normal((b, N, width))
-    new = old + rng.standard_normal((b, N, width)) * rng.uniform(0.0, 0.3, (b, N, 1))
+    new = old + rng.standard_normal((b, N, width)) * rng.uniform(0.0, 1.5, (b, N, 1))
     new[:, row_lo::7] = old[:, row_lo::7]                     # identical rows -> s == 1 exactly
     new_d = torch.tensor(new, dtype=torch.float32).bfloat16().cuda()
     old_d = torch.tensor(old, dtype=torch.float32).bfloat16().cuda()

@@ -37,8 +37,11 @@ def test_full_step_caches_match_oracle(name):
             assert err < TOL, (l, f, err)
 
 
-def _teacher_forced_layer(name, layer, mode, frac_in=0.4, seed=0):
-    m = Model(name, seed=seed)
+QK_STD = {"tiny": 0.18, "small128": 0.09, "small128_gqa": 0.09}   # sharper attention
+
+
+def _teacher_forced_layer(name, layer, mode, frac_in=0.4, seed=0, select_mode=0, frac=0.3):
+    m = Model(name, seed=seed, qk_std=QK_STD[name], select_mode=select_mode)
     cfg, run = m.cfg, m.run
     N = run.N
     prompts = gen.prompt_tokens(seed + 5, run.batch, run.L_P, cfg.mask_id)
@@ -66,18 +69,22 @@ def _teacher_forced_layer(name, layer, mode, frac_in=0.4, seed=0):
         refs.append((r, lc))
     s_all = np.concatenate([r.s for r, _ in refs])
     tau = float(np.quantile(s_all, 0.5))
-    # rerun the oracle with the chosen tau (tau only affects selection and the FFN rows)
-    refs = []
-    for st, idx in zip(states, idx_lists):
+    # rerun the oracle with the chosen tau (tau only affects selection and the FFN rows);
+    # in fraction mode every sequence thresholds at its own quantile (D19)
+    first, refs, taus = refs, [], []
+    for st, idx, (r0, _) in zip(states, idx_lists, first):
         x_all = st.H0 if layer == 0 else st.caches[layer - 1].H
         lc = st.caches[layer].copy()
-        r = O.sparse_layer(x_all, lc, m.W["layers"][layer], cfg, idx, tau, input_rows, q_mode="cache")
+        t_seq = O.quantile_threshold(r0.s, frac) if select_mode == 1 else tau
+        r = O.sparse_layer(x_all, lc, m.W["layers"][layer], cfg, idx, t_seq, input_rows, q_mode="cache")
         refs.append((r, lc))
+        taus.append(t_seq)
     idx_d, off_d = pack_lists(idx_lists, N)
     out_d = torch.zeros(run.batch * N, dtype=torch.int32, device="cuda")
     oof_d = torch.zeros(run.batch + 1, dtype=torch.int32, device="cuda")
     sim_d = torch.full((run.batch * N,), -9.0, device="cuda")
-    cache.layer_step(layer, 0 if mode == "fi" else 1, idx_d, off_d, tau, out_d, oof_d, sim_d)
+    cache.layer_step(layer, 0 if mode == "fi" else 1, idx_d, off_d, frac if select_mode == 1 else tau,
+                     out_d, oof_d, sim_d)
     torch.cuda.synchronize()
     got_lists = unpack_lists(out_d, oof_d, N)
     sim = sim_d.cpu().numpy().reshape(run.batch, N)
@@ -89,7 +96,7 @@ def _teacher_forced_layer(name, layer, mode, frac_in=0.4, seed=0):
     n_band = 0
     for s, ((r, lc), idx) in enumerate(zip(refs, idx_lists)):
         assert np.abs(sim[s, row_lo:] - r.s).max() < 2e-2
-        band = set(input_rows[np.abs(r.s - tau) < BAND].tolist())
+        band = set(input_rows[np.abs(r.s - taus[s]) < BAND].tolist())
         n_band += len(band)
         got, ref = set(got_lists[s].tolist()), set(r.idx_out.tolist())
         assert got - band == ref - band, (s, sorted(got ^ ref))
@@ -114,6 +121,13 @@ def _teacher_forced_layer(name, layer, mode, frac_in=0.4, seed=0):
 @pytest.mark.parametrize("mode", ["fi", "ro"])
 def test_layer_step_teacher_forced(name, layer, mode):
     _teacher_forced_layer(name, layer, mode)
+
+
+@pytest.mark.parametrize("name", ["tiny", "small128_gqa"])
+@pytest.mark.parametrize("mode", ["fi", "ro"])
+@pytest.mark.parametrize("frac", [0.1, 0.5])
+def test_layer_step_fraction_mode(name, mode, frac):
+    _teacher_forced_layer(name, 1, mode, select_mode=1, frac=frac)
 
 
 def test_layer_step_all_salient_equals_full(name="small128"):

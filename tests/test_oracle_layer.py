@@ -202,3 +202,14 @@ def test_saliency_monotone_in_tau():
         O.sparse_step(st, W, cfg, run, O.MODE_FI, tau)
         counts.append(st.sal_counts[-1][0])
     assert counts == sorted(counts)
+
+
+def test_fraction_mode_generation_counts():
+    """select_mode=1: every sparse layer selects round(f * L) rows of each sequence (no ties)."""
+    cfg, run, W = _model("small128", qk_std=0.09)
+    run = replace(run, L_R=32, block=16, select_mode=1)
+    prompts = gen.prompt_tokens(5, 1, run.L_P, cfg.mask_id)
+    _, states = O.generate(prompts, W, cfg, run, 0.25)
+    for t, counts in zip(range(run.T_full, run.T_total), states[0].sal_counts):
+        L = run.N if O.step_mode(t, run) == O.MODE_FI else run.L_R
+        assert counts == [int(np.floor(0.25 * L + 0.5))] * cfg.n_layers

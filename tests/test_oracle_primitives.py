@@ -242,3 +242,21 @@ def test_cost_example_from_paper():
     assert O.fastdllm_computed_tokens(g["L_P"], g["L_R"], g["B"], g["n_u"], dual=False) == g["prefix_per_step"]
     assert O.fastdllm_computed_tokens(g["L_P"], g["L_R"], g["B"], g["n_u"], dual=True) == g["dual_per_step"]
     assert (g["prefix_avg_block_tokens"] * 31 + g["refresh_tokens"]) / 32 == g["prefix_per_step"]
+
+
+# ---------------------------------------------------------------- fraction-controlled threshold (D19)
+
+def test_quantile_threshold_brute_force():
+    rng = np.random.default_rng(12)
+    for n in (1, 5, 64, 257):
+        s = rng.uniform(0.5, 1.0, n)
+        for f in (0.0, 0.05, 0.1, 0.37, 0.5, 1.0):
+            tau = O.quantile_threshold(s, f)
+            k = int(np.floor(f * n + 0.5))
+            got = O.select_salient(s, tau, np.arange(n))
+            assert sorted(got.tolist()) == sorted(np.argsort(s)[:k].tolist())
+
+
+def test_quantile_threshold_ties_select_fewer():
+    s = np.array([0.9, 1.0, 1.0, 1.0])           # identical rows give s == 1 exactly (D9)
+    assert O.select_salient(s, O.quantile_threshold(s, 0.75), np.arange(4)).tolist() == [0]
