@@ -187,7 +187,7 @@ def run_reference(args):
                          "sample": base["sample"]},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line, default=float), flush=True)
 
 
 # ----------------------------------------------------------------------------- GPU leg
@@ -453,7 +453,7 @@ def main():
             "full_recompute": {"ms_per_full_step": full_ms, "tokens_per_s_extrapolated": full_tok_s,
                                "speedup": (value / full_tok_s) if full_tok_s else None},
         }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line, default=float), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

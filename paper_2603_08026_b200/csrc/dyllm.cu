@@ -117,6 +117,7 @@ struct dyllm_cache {
   int *ap_rows, *ap_off, *all_rows, *all_off, *zero_off, *lm_rows, *lm_off;
   int *dec_prev;
   float *sim;  // per-row similarity scratch (fraction mode)
+  float2 *rope_cs;  // [N][head_dim/2] (cos, sin) table
   bool have_dec_prev = false;
   bool initialized = false;
   std::vector<void *> allocs;
@@ -428,6 +429,7 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
   AL(c->lm_off, r->batch + 1);
   AL(c->dec_prev, static_cast<int64_t>(r->batch) * r->n_u);
   AL(c->sim, rows);
+  AL(c->rope_cs, static_cast<int64_t>(c->N) * (m.head_dim / 2));
 #undef AL
   cudaStream_t st = ctx->stream;
   if (cudaMemsetAsync(c->zero_off, 0, (r->batch + 1) * sizeof(int), st) != cudaSuccess) {
@@ -436,6 +438,7 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
     return DYLLM_E_CUDA;
   }
   launch_build_list(0, nullptr, nullptr, nullptr, 0, 0, r->batch, c->N, 0, 0, c->all_rows, c->all_off, st);
+  launch_rope_table(c->rope_cs, c->N, m.head_dim, static_cast<double>(m.rope_theta), st);
   if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
     set_error("cache_create: CUDA error");
     dyllm_cache_destroy(c);
@@ -504,7 +507,7 @@ static int full_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c
     KL(GATHER, launch_gather_rmsnorm(Hprev, nullptr, nullptr, rows, L.g_attn, m.rms_eps, c->Xn, d, st));
     KL(QKV_GEMM, RET(gemm(ctx, nullptr, rows, qw + 2 * kw, d, c->Xn, L.wqkv, c->qkv, qw + 2 * kw, EPI_BF16)));
     KL(QKV_POST, launch_qkv_post(c->qkv, nullptr, nullptr, rows, L.bqkv, c->N, m.n_heads, m.n_kv_heads, m.head_dim,
-                                 m.rope_theta, C.Q, C.K, C.V, nullptr, st));
+                                 c->rope_cs, C.Q, C.K, C.V, nullptr, st));
     AttnArgs a{};
     a.batch = c->r.batch;
     a.N = c->N;
@@ -559,7 +562,7 @@ static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *
   KL(QKV_GEMM, RET(gemm(ctx, M_in, rows, qw + 2 * kw, d, c->Xn, L.wqkv, c->qkv, qw + 2 * kw, EPI_BF16)));
   // a3: RoPE, dV (before overwrite), in-place K/V/Q cache rows
   KL(QKV_POST, launch_qkv_post(c->qkv, idx_in, M_in, rows, L.bqkv, N, m.n_heads, m.n_kv_heads, m.head_dim,
-                               m.rope_theta, C.Q, C.K, C.V, c->dV, st));
+                               c->rope_cs, C.Q, C.K, C.V, c->dV, st));
   // a4: exact rows + approximate rows (Alg. 4) -> Cn
   AttnArgs a{};
   a.batch = b;

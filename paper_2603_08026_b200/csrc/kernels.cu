@@ -88,48 +88,78 @@ __global__ void scatter_rows_kernel(const bf16 *__restrict__ src, const int *__r
 // Q_cache[r], K_cache[r], V_cache[r] <- q, k, v (D6).
 __global__ void qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restrict__ idx,
                                 const int *__restrict__ M_ptr, int M_cap, const bf16 *__restrict__ bias, int N,
-                                int H, int KVH, int hd, float log2_theta, bf16 *__restrict__ Qc,
+                                int H, int KVH, int hd, const float2 *__restrict__ rope_cs, bf16 *__restrict__ Qc,
                                 bf16 *__restrict__ Kc, bf16 *__restrict__ Vc, bf16 *__restrict__ dV) {
   const int M = M_ptr ? *M_ptr : M_cap;
   const int qw = H * hd, kw = KVH * hd, W = qw + 2 * kw;
-  const int half = hd / 2;
+  const int half = hd / 2, hv = half / 8;  // 8 rotation pairs per thread (16-byte vectors)
   for (int i = blockIdx.x; i < M; i += gridDim.x) {
     const int r = idx ? idx[i] : i;
-    const float pos = static_cast<float>(r % N);
+    const int pos = r % N;
     const bf16 *src = qkv + static_cast<int64_t>(i) * W;
-    // q and k: one thread per rotation pair
-    const int npairs = (H + KVH) * half;
-    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
-      const int head = p / half, k = p - head * half;
-      const int col = head * hd + k;  // q cols [0,qw), k cols [qw, qw+kw) — heads are contiguous
-      float x1 = bf2f(src[col]), x2 = bf2f(src[col + half]);
+    const float2 *cs = rope_cs + static_cast<int64_t>(pos) * half;
+    // q and k heads: pairs (x[k], x[k + hd/2]) rotated by pos * theta^(-2k/hd) (table, fp64-derived)
+    for (int v = threadIdx.x; v < (H + KVH) * hv; v += blockDim.x) {
+      const int head = v / hv, k0 = (v - head * hv) * 8;
+      const int col = head * hd + k0;  // q cols [0,qw), k cols [qw, qw+kw): heads contiguous
+      float x1[8], x2[8];
+      unpack8(*reinterpret_cast<const uint4 *>(src + col), x1);
+      unpack8(*reinterpret_cast<const uint4 *>(src + col + half), x2);
       if (bias) {
-        x1 += bf2f(bias[col]);
-        x2 += bf2f(bias[col + half]);
+        float b1[8], b2[8];
+        unpack8(*reinterpret_cast<const uint4 *>(bias + col), b1);
+        unpack8(*reinterpret_cast<const uint4 *>(bias + col + half), b2);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          x1[j] += b1[j];
+          x2[j] += b2[j];
+        }
       }
-      const float inv = exp2f(-(2.f * k / hd) * log2_theta);
-      float sn, cs;
-      sincosf(pos * inv, &sn, &cs);
-      const bf16 y1 = f2bf(x1 * cs - x2 * sn), y2 = f2bf(x2 * cs + x1 * sn);
-      if (col < qw) {
-        bf16 *q = Qc + static_cast<int64_t>(r) * qw;
-        q[col] = y1;
-        q[col + half] = y2;
-      } else {
-        bf16 *kk = Kc + static_cast<int64_t>(r) * kw;
-        kk[col - qw] = y1;
-        kk[col - qw + half] = y2;
+      float y1[8], y2[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float2 c = cs[k0 + j];
+        y1[j] = x1[j] * c.x - x2[j] * c.y;
+        y2[j] = x2[j] * c.x + x1[j] * c.y;
       }
+      bf16 *dst = (col < qw) ? Qc + static_cast<int64_t>(r) * qw + col : Kc + static_cast<int64_t>(r) * kw + (col - qw);
+      *reinterpret_cast<uint4 *>(dst) = pack8(y1);
+      *reinterpret_cast<uint4 *>(dst + half) = pack8(y2);
     }
-    // v: one thread per element
-    for (int c = threadIdx.x; c < kw; c += blockDim.x) {
-      float v = bf2f(src[qw + kw + c]);
-      if (bias) v += bf2f(bias[qw + kw + c]);
-      const bf16 vb = f2bf(v);
-      bf16 *vc = Vc + static_cast<int64_t>(r) * kw + c;
-      if (dV) dV[static_cast<int64_t>(i) * kw + c] = f2bf(bf2f(vb) - bf2f(*vc));
+    // v: dV = v_new - V_cache (read before the overwrite), then V_cache <- v_new
+    for (int c = threadIdx.x * 8; c < kw; c += blockDim.x * 8) {
+      float v[8];
+      unpack8(*reinterpret_cast<const uint4 *>(src + qw + kw + c), v);
+      if (bias) {
+        float bb[8];
+        unpack8(*reinterpret_cast<const uint4 *>(bias + qw + kw + c), bb);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] += bb[j];
+      }
+      const uint4 vb = pack8(v);
+      uint4 *vc = reinterpret_cast<uint4 *>(Vc + static_cast<int64_t>(r) * kw + c);
+      if (dV) {
+        float vn[8], vo[8], dd[8];
+        unpack8(vb, vn);
+        unpack8(*vc, vo);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dd[j] = vn[j] - vo[j];
+        *reinterpret_cast<uint4 *>(dV + static_cast<int64_t>(i) * kw + c) = pack8(dd);
+      }
       *vc = vb;
     }
+  }
+}
+
+// RoPE table cs[pos][k] = (cos, sin)(pos * theta^(-2k/hd)), computed in fp64 once per cache.
+__global__ void rope_table_kernel(float2 *__restrict__ cs, int N, int hd, double theta) {
+  const int half = hd / 2;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < N * half; e += gridDim.x * blockDim.x) {
+    const int pos = e / half, k = e - pos * half;
+    const double ang = static_cast<double>(pos) * pow(theta, -2.0 * k / hd);
+    double sn, c;
+    sincos(ang, &sn, &c);
+    cs[e] = make_float2(static_cast<float>(c), static_cast<float>(sn));
   }
 }
 
@@ -601,10 +631,13 @@ void launch_rmsnorm_rows(const bf16 *src, const int *M_ptr, int M_cap, const bf1
   gather_rmsnorm_kernel<<<grid_for(M_cap, 8), 256, 0, st>>>(src, nullptr, M_ptr, M_cap, g, eps, dst, d);
 }
 void launch_qkv_post(const bf16 *qkv, const int *idx, const int *M_ptr, int M_cap, const bf16 *bias, int N, int H,
-                     int KVH, int hd, float theta, bf16 *Qc, bf16 *Kc, bf16 *Vc, bf16 *dV, cudaStream_t st) {
+                     int KVH, int hd, const float2 *rope_cs, bf16 *Qc, bf16 *Kc, bf16 *Vc, bf16 *dV, cudaStream_t st) {
   const int g = M_cap < 148 * 8 ? M_cap : 148 * 8;
-  qkv_post_kernel<<<g > 0 ? g : 1, 256, 0, st>>>(qkv, idx, M_ptr, M_cap, bias, N, H, KVH, hd, log2f(theta), Qc, Kc,
-                                                 Vc, dV);
+  qkv_post_kernel<<<g > 0 ? g : 1, 256, 0, st>>>(qkv, idx, M_ptr, M_cap, bias, N, H, KVH, hd, rope_cs, Qc, Kc, Vc,
+                                                 dV);
+}
+void launch_rope_table(float2 *cs, int N, int hd, double theta, cudaStream_t st) {
+  rope_table_kernel<<<148, 256, 0, st>>>(cs, N, hd, theta);
 }
 void launch_approx_rows(const int *idx_in, const int *off_in, int batch, int N, int row_lo, int *ap_rows,
                         int *ap_off, cudaStream_t st) {

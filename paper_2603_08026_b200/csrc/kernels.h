@@ -18,7 +18,8 @@ void launch_scatter_rows(const bf16 *src, const int *idx, const int *M_ptr, int 
 void launch_rmsnorm_rows(const bf16 *src, const int *M_ptr, int M_cap, const bf16 *g, float eps, bf16 *dst, int d,
                          cudaStream_t st);
 void launch_qkv_post(const bf16 *qkv, const int *idx, const int *M_ptr, int M_cap, const bf16 *bias, int N, int H,
-                     int KVH, int hd, float theta, bf16 *Qc, bf16 *Kc, bf16 *Vc, bf16 *dV, cudaStream_t st);
+                     int KVH, int hd, const float2 *rope_cs, bf16 *Qc, bf16 *Kc, bf16 *Vc, bf16 *dV, cudaStream_t st);
+void launch_rope_table(float2 *cs, int N, int hd, double theta, cudaStream_t st);
 void launch_approx_rows(const int *idx_in, const int *off_in, int batch, int N, int row_lo, int *ap_rows,
                         int *ap_off, cudaStream_t st);
 void launch_build_list(int mode, const int *carried, const int *carried_off, const int *dec_pos, int n_u, int policy,

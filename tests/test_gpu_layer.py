@@ -112,7 +112,9 @@ def _teacher_forced_layer(name, layer, mode, frac_in=0.4, seed=0, select_mode=0,
             assert row_rel_err(H_gpu[s, agreed], r.out[sel]).max() < TOL
         untouched = sorted(set(range(N)) - got)
         assert np.array_equal(H_gpu[s, untouched], h_before[s, untouched])
-    assert n_band <= 0.05 * run.batch * len(input_rows) + 1
+    # the excluded band must stay small, else the comparison is vacuous (in fraction mode tau* is
+    # itself one of the similarities, so its row and a neighbour are always in the band)
+    assert n_band <= 0.05 * run.batch * len(input_rows) + (2 * run.batch if select_mode == 1 else 1)
     return m
 
 
