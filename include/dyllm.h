@@ -200,6 +200,12 @@ int dyllm_ctx_profile_read(dyllm_ctx *ctx, int kclass, float *h_ms, int max_n);
 /* Process-wide number of kernels libdyllm has launched so far. */
 uint64_t dyllm_launch_count(void);
 
+/* Process-wide kernel-path options (A/B testing and parity of alternative kernels).
+ * DYLLM_OPT_SKINNY_GEMM (default 1): route GEMMs whose device row count is <= 512 to the 2-CTA
+ * weight-stationary kernel; 0 = always the 1-CTA kernel. Returns the previous value. */
+enum { DYLLM_OPT_SKINNY_GEMM = 1 };
+int dyllm_set_option(int option, int value);
+
 #ifdef __cplusplus
 }
 #endif

@@ -118,6 +118,7 @@ struct dyllm_cache {
   int *dec_prev;
   float *sim;  // per-row similarity scratch (fraction mode)
   float2 *rope_cs;  // [N][head_dim/2] (cos, sin) table
+  float2 *stats;    // [b*N][H] attention row statistics scratch
   bool have_dec_prev = false;
   bool initialized = false;
   std::vector<void *> allocs;
@@ -289,11 +290,13 @@ int dyllm_weights_load(dyllm_ctx *ctx, const dyllm_model_cfg *m, const uint16_t 
     if (m->qkv_bias) PUT(L.bqkv, qw + 2 * kw);
     PUT(L.wo, d * qw);
     PUT(L.g_ffn, d);
-    // gate / up interleaved in blocks of 128 rows: [gate blk][up blk] (SwiGLU GEMM epilogue)
+    // gate / up interleaved in blocks of kGuIl rows: [gate blk][up blk] (SwiGLU GEMM epilogues)
     const uint16_t *gate = p, *up = p + F * d;
-    for (int64_t b = 0; b < F / 128; ++b) {
-      cudaError_t e1 = cudaMemcpy(L.wgu + (2 * b) * 128 * d, gate + b * 128 * d, 128 * d * 2, cudaMemcpyHostToDevice);
-      cudaError_t e2 = cudaMemcpy(L.wgu + (2 * b + 1) * 128 * d, up + b * 128 * d, 128 * d * 2, cudaMemcpyHostToDevice);
+    for (int64_t b = 0; b < F / kGuIl; ++b) {
+      cudaError_t e1 =
+          cudaMemcpy(L.wgu + (2 * b) * kGuIl * d, gate + b * kGuIl * d, kGuIl * d * 2, cudaMemcpyHostToDevice);
+      cudaError_t e2 =
+          cudaMemcpy(L.wgu + (2 * b + 1) * kGuIl * d, up + b * kGuIl * d, kGuIl * d * 2, cudaMemcpyHostToDevice);
       if (e1 != cudaSuccess || e2 != cudaSuccess) {
         set_error("cudaMemcpy gate/up failed");
         dyllm_weights_destroy(w);
@@ -350,7 +353,7 @@ int dyllm_weights_init_random(dyllm_ctx *ctx, const dyllm_model_cfg *m, uint64_t
       launch_ih4_fill(L.bqkv + qw + kw, 1, kw, key(l, T_BV), 0, 0, scale, st);
     }
     launch_ih4_fill(L.wo, d, qw, key(l, T_WO), 0, 0, scale, st);
-    launch_ih4_fill(L.wgu, 2 * F, d, key(l, T_GATE), key(l, T_UP), 128, scale, st);
+    launch_ih4_fill(L.wgu, 2 * F, d, key(l, T_GATE), key(l, T_UP), kGuIl, scale, st);
     launch_ih4_fill(L.wd, d, F, key(l, T_DOWN), 0, 0, scale, st);
   }
   cudaError_t e = cudaStreamSynchronize(st);
@@ -430,6 +433,7 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
   AL(c->dec_prev, static_cast<int64_t>(r->batch) * r->n_u);
   AL(c->sim, rows);
   AL(c->rope_cs, static_cast<int64_t>(c->N) * (m.head_dim / 2));
+  AL(c->stats, rows * m.n_heads);
 #undef AL
   cudaStream_t st = ctx->stream;
   if (cudaMemsetAsync(c->zero_off, 0, (r->batch + 1) * sizeof(int), st) != cudaSuccess) {
@@ -528,6 +532,9 @@ static int full_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c
     a.sal_off = c->zero_off;
     a.max_rows_per_seq = c->N;
     a.scale = 1.f / sqrtf(static_cast<float>(m.head_dim));
+    a.row_lo = 0;
+    a.stats = c->stats;
+    a.num_sms = ctx->num_sms;
     KL(ATTN, RET(attention_launch(a, st)));
     int prc = post_attention(ctx, w, c, l, nullptr, C.C, Hprev, nullptr, C.H);
     if (prc) {
@@ -584,6 +591,9 @@ static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *
   a.sal_off = off_in;
   a.max_rows_per_seq = N - row_lo;
   a.scale = 1.f / sqrtf(static_cast<float>(m.head_dim));
+  a.row_lo = row_lo;
+  a.stats = c->stats;
+  a.num_sms = ctx->num_sms;
   KL(ATTN, RET(attention_launch(a, st)));
   // a5: cosine similarity + threshold + compaction; C_cache <- Cn for the input rows
   const bool fmode = c->r.select_mode == 1;
@@ -731,6 +741,16 @@ int dyllm_ctx_profile_read(dyllm_ctx *ctx, int kclass, float *h_ms, int max_n) {
 }
 
 uint64_t dyllm_launch_count(void) { return g_launches.load(); }
+
+int dyllm_set_option(int option, int value) {
+  if (option == DYLLM_OPT_SKINNY_GEMM) {
+    const int prev = g_skinny_enabled ? 1 : 0;
+    g_skinny_enabled = value != 0;
+    return prev;
+  }
+  set_error("unknown option");
+  return DYLLM_E_ARG;
+}
 
 // ------------------------------------------------------------------ ABI: cache access
 int dyllm_cache_tensor(const dyllm_cache *c, int layer, int which, void **d_ptr, int64_t *n_elems) {

@@ -49,6 +49,7 @@ struct GemmParams {
   const int *resid_rows;
   const bf16 *bias;
   float4 *partials;
+  int m_skip_le;
 };
 
 __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int &m, int &n) {
@@ -82,7 +83,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int M = p.M_ptr ? min(*p.M_ptr, p.M_cap) : p.M_cap;
   const int num_m = (M + BM - 1) / BM;
   const int num_n = (p.N + BN - 1) / BN;
-  const int total = num_m * num_n;
+  const int total = (M <= p.m_skip_le) ? 0 : num_m * num_n;  // small M: the skinny kernel runs
   const int num_kb = p.K / BK;
 
   if (warp == 0 && lane == 0) {
@@ -172,12 +173,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const bool row_ok = row < M;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN;
       if constexpr (EPI == EPI_SWIGLU) {
-        // tile = [128 gate cols | 128 up cols] of the same 128 FFN channels
+        // tile = [g64 | u64 | g64 | u64] (kGuIl = 64): channels nb*128 + [0,64) and + [64,128)
 #pragma unroll 1
         for (int c0 = 0; c0 < BN / 2; c0 += 32) {
+          const int gcol = (c0 < kGuIl) ? c0 : c0 + kGuIl;  // gate column in the tile
           float g[32], u[32];
-          tmem_ld32(tbase + c0, g);
-          tmem_ld32(tbase + BN / 2 + c0, u);
+          tmem_ld32(tbase + gcol, g);
+          tmem_ld32(tbase + gcol + kGuIl, u);
           if (row_ok) {
             const int col = nb * (BN / 2) + c0;
             bf16 *dst = p.D + static_cast<int64_t>(row) * p.ldd + col;
@@ -268,7 +270,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 static std::once_flag g_encode_once;
 
-static int make_tmap(CUtensorMap *m, const void *ptr, int rows, int K, int box_rows) {
+int make_tmap(CUtensorMap *m, const void *ptr, int rows, int K, int box_rows) {
   std::call_once(g_encode_once, [] {
     cudaDriverEntryPointQueryResult q;
     void *fn = nullptr;
@@ -309,7 +311,7 @@ static int launch_t(const GemmCall &g, int num_sms, cudaStream_t st) {
   if (rc) return rc;
   rc = make_tmap(&tb, g.W, g.N, g.K, BN);
   if (rc) return rc;
-  GemmParams p{g.M_ptr, g.M_cap, g.N, g.K, g.D, g.ldd, g.resid, g.ldr, g.resid_rows, g.bias, g.partials};
+  GemmParams p{g.M_ptr, g.M_cap, g.N, g.K, g.D, g.ldd, g.resid, g.ldr, g.resid_rows, g.bias, g.partials, g.m_skip_le};
   const int max_tiles = ((g.M_cap + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   const int grid = max_tiles < num_sms ? max_tiles : num_sms;
   kern<<<grid, kGemmThreads, C::SMEM_BYTES, st>>>(ta, tb, p);
@@ -325,20 +327,33 @@ int gemm_launch(const GemmCall &g, int num_sms, cudaStream_t st) {
               " K=" + std::to_string(g.K));
     return DYLLM_E_SHAPE;
   }
-  switch (g.epi) {
+  if (g.epi == EPI_SWIGLU && g.N % 256 != 0) {
+    set_error("gemm swiglu: N must be a multiple of 256");
+    return DYLLM_E_SHAPE;
+  }
+  // Small row counts (<= 512) go to the 2-CTA weight-stationary kernel. With a device-resident
+  // count both kernels are enqueued and each exits unless the count is in its regime.
+  GemmCall s = g;
+  if (g_skinny_enabled && skinny_eligible(g)) {
+    if (!g.M_ptr && g.M_cap <= kSkinnyMaxM) return gemm_skinny_launch(g, num_sms, st);
+    if (g.M_ptr) {
+      int rc = gemm_skinny_launch(g, num_sms, st);
+      if (rc) return rc;
+      s.m_skip_le = kSkinnyMaxM;
+    }
+  }
+  switch (s.epi) {
     case EPI_SWIGLU:
-      if (g.N % 256 != 0) {
-        set_error("gemm swiglu: N must be a multiple of 256");
-        return DYLLM_E_SHAPE;
-      }
-      return launch_t<256, EPI_SWIGLU>(g, num_sms, st);
+      return launch_t<256, EPI_SWIGLU>(s, num_sms, st);
     case EPI_LMHEAD:
-      return launch_t<256, EPI_LMHEAD>(g, num_sms, st);
+      return launch_t<256, EPI_LMHEAD>(s, num_sms, st);
     case EPI_RESID:
-      return g.N >= 8192 ? launch_t<256, EPI_RESID>(g, num_sms, st) : launch_t<128, EPI_RESID>(g, num_sms, st);
+      return s.N >= 8192 ? launch_t<256, EPI_RESID>(s, num_sms, st) : launch_t<128, EPI_RESID>(s, num_sms, st);
     default:
-      return g.N >= 8192 ? launch_t<256, EPI_BF16>(g, num_sms, st) : launch_t<128, EPI_BF16>(g, num_sms, st);
+      return s.N >= 8192 ? launch_t<256, EPI_BF16>(s, num_sms, st) : launch_t<128, EPI_BF16>(s, num_sms, st);
   }
 }
+
+bool g_skinny_enabled = true;
 
 }  // namespace dy

@@ -28,6 +28,9 @@ void set_error(const std::string &msg);
 
 // ------------------------------------------------------------------ GEMM (gemm.cu)
 enum Epi { EPI_BF16 = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_LMHEAD = 3 };
+// gate/up rows of W_gu are interleaved in blocks of kGuIl rows ([gate x64][up x64] ...), so a
+// 128-row weight tile holds the gate and up rows of the same 64 FFN channels.
+constexpr int kGuIl = 64;
 
 struct GemmCall {
   const int *M_ptr = nullptr;  // device row count (nullable -> M_cap)
@@ -44,9 +47,16 @@ struct GemmCall {
   const bf16 *bias = nullptr;       // nullable [N]
   float4 *partials = nullptr;       // EPI_LMHEAD: [M_cap][n_tiles] (max, sumexp, argmax, 0)
   int epi = EPI_BF16;
+  int m_skip_le = 0;  // standard kernel: do nothing when the device row count is <= this
 };
 int gemm_launch(const GemmCall &g, int num_sms, cudaStream_t st);
+// 2D bf16 tensor map [rows][K] (K contiguous), box {64, box_rows}, SWIZZLE_128B
+int make_tmap(CUtensorMap *m, const void *ptr, int rows, int K, int box_rows);
 int gemm_lmhead_ntiles(int N);
+bool skinny_eligible(const GemmCall &g);
+constexpr int kSkinnyMaxM = 512;
+extern bool g_skinny_enabled;  // test hook (dyllm_set_option)
+int gemm_skinny_launch(const GemmCall &g, int num_sms, cudaStream_t st);  // gemm_skinny.cu
 
 // ------------------------------------------------------------------ kernels (kernels.cu)
 struct AttnArgs {
@@ -61,6 +71,9 @@ struct AttnArgs {
   const int *sal_rows, *sal_off;  // idx_in (salient keys) + offsets
   int max_rows_per_seq;         // upper bound of rows per list per sequence
   float scale;
+  int row_lo;                   // first input position (0 full input, L_P response-only)
+  float2 *stats;                // [b*N][H] (row max, sum-exp) scratch in the exp2 domain
+  int num_sms;
 };
 int attention_launch(const AttnArgs &a, cudaStream_t st);
 

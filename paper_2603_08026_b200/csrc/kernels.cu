@@ -30,9 +30,40 @@ __global__ void gather_rmsnorm_kernel(const bf16 *__restrict__ src, const int *_
   const int M = M_ptr ? *M_ptr : M_cap;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
   const int nv = d / 8;
+  constexpr int VMAX = 16;  // rows up to 4096 wide stay in registers (16 x 16 B per lane)
   for (int i = warp; i < M; i += gridDim.x * blockDim.x / 32) {
     const int r = idx ? idx[i] : i;
     const uint4 *s = reinterpret_cast<const uint4 *>(src + static_cast<int64_t>(r) * d);
+    uint4 *o = reinterpret_cast<uint4 *>(dst + static_cast<int64_t>(i) * d);
+    const uint4 *gv = reinterpret_cast<const uint4 *>(g);
+    if (nv <= 32 * VMAX) {
+      uint4 v[VMAX];
+#pragma unroll
+      for (int u = 0; u < VMAX; ++u)
+        if (lane + u * 32 < nv) v[u] = ld_nc_v4(s + lane + u * 32);
+      float ss = 0.f;
+#pragma unroll
+      for (int u = 0; u < VMAX; ++u)
+        if (lane + u * 32 < nv) {
+          float f[8];
+          unpack8(v[u], f);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) ss += f[j] * f[j];
+        }
+      ss = warp_sum(ss);
+      const float inv = rsqrtf(ss / d + eps);
+#pragma unroll
+      for (int u = 0; u < VMAX; ++u)
+        if (lane + u * 32 < nv) {
+          float f[8], w[8];
+          unpack8(v[u], f);
+          unpack8(gv[lane + u * 32], w);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) f[j] = f[j] * inv * w[j];
+          o[lane + u * 32] = pack8(f);
+        }
+      continue;
+    }
     float ss = 0.f;
     for (int c = lane; c < nv; c += 32) {
       float f[8];
@@ -42,8 +73,6 @@ __global__ void gather_rmsnorm_kernel(const bf16 *__restrict__ src, const int *_
     }
     ss = warp_sum(ss);
     const float inv = rsqrtf(ss / d + eps);
-    uint4 *o = reinterpret_cast<uint4 *>(dst + static_cast<int64_t>(i) * d);
-    const uint4 *gv = reinterpret_cast<const uint4 *>(g);
     for (int c = lane; c < nv; c += 32) {
       float f[8], w[8];
       unpack8(s[c], f);
@@ -52,6 +81,20 @@ __global__ void gather_rmsnorm_kernel(const bf16 *__restrict__ src, const int *_
       for (int j = 0; j < 8; ++j) f[j] = f[j] * inv * w[j];
       o[c] = pack8(f);
     }
+  }
+}
+
+// warp-cooperative row copy with 8 independent 16-byte loads in flight per lane
+__device__ __forceinline__ void copy_row(uint4 *__restrict__ o, const uint4 *__restrict__ s, int nv, int lane) {
+  constexpr int U = 8;
+  for (int c0 = lane; c0 < nv; c0 += 32 * U) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (c0 + u * 32 < nv) v[u] = ld_nc_v4(s + c0 + u * 32);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (c0 + u * 32 < nv) o[c0 + u * 32] = v[u];
   }
 }
 
@@ -64,7 +107,7 @@ __global__ void gather_rows_kernel(const bf16 *__restrict__ src, const int *__re
   for (int i = warp; i < M; i += gridDim.x * blockDim.x / 32) {
     const uint4 *s = reinterpret_cast<const uint4 *>(src + static_cast<int64_t>(idx[i]) * width);
     uint4 *o = reinterpret_cast<uint4 *>(dst + static_cast<int64_t>(i) * width);
-    for (int c = lane; c < nv; c += 32) o[c] = ld_nc_v4(s + c);
+    copy_row(o, s, nv, lane);
   }
 }
 
@@ -78,7 +121,7 @@ __global__ void scatter_rows_kernel(const bf16 *__restrict__ src, const int *__r
   for (int i = warp; i < M; i += gridDim.x * blockDim.x / 32) {
     const uint4 *s = reinterpret_cast<const uint4 *>(src + static_cast<int64_t>(i) * width);
     uint4 *o = reinterpret_cast<uint4 *>(dst + static_cast<int64_t>(idx[i]) * width);
-    for (int c = lane; c < nv; c += 32) o[c] = ld_nc_v4(s + c);
+    copy_row(o, s, nv, lane);
   }
 }
 
@@ -257,7 +300,10 @@ __global__ void build_list_kernel(int mode, const int *__restrict__ carried, con
 // sequences and writes the packed list + offsets (no second launch, no host sync).
 constexpr int kSelRowsPerCta = 32;
 
-__global__ void __launch_bounds__(256) select_salient_kernel(
+constexpr int kSelThreads = 1024;  // 32 warps: one input row per warp
+constexpr int kSelWarps = kSelThreads / 32;
+
+__global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
     const bf16 *__restrict__ c_new, bf16 *__restrict__ c_cache, int N, int row_lo, int width, float tau,
     int cmp, float frac, int *__restrict__ idx_out, int *__restrict__ off_out, float *__restrict__ sim_out,
     unsigned *__restrict__ masks, unsigned *__restrict__ ticket, int *__restrict__ counts_out) {
@@ -269,7 +315,8 @@ __global__ void __launch_bounds__(256) select_salient_kernel(
   const int nchunks = gridDim.x;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nv = width / 8;
-  for (int rr = warp; rr < kSelRowsPerCta; rr += 8) {
+  {
+    const int rr = warp;  // one row per warp (32 warps = the CTA's 32 rows)
     const int p = row_lo + chunk * kSelRowsPerCta + rr;
     unsigned f = 0;
     if (p < N) {
@@ -277,19 +324,33 @@ __global__ void __launch_bounds__(256) select_salient_kernel(
       const uint4 *a = reinterpret_cast<const uint4 *>(c_new + r * width);
       uint4 *b = reinterpret_cast<uint4 *>(c_cache + r * width);
       float dot = 0.f, na = 0.f, nb = 0.f;
-      for (int c = lane; c < nv; c += 32) {
-        const uint4 ua = ld_nc_v4(a + c);
-        const uint4 ub = b[c];
-        float fa[8], fb[8];
-        unpack8(ua, fa);
-        unpack8(ub, fb);
+      constexpr int U = 4;  // 2*U independent 16-byte loads in flight per lane
+      for (int c0 = lane; c0 < nv; c0 += 32 * U) {
+        uint4 ua[U], ub[U];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          dot = fmaf(fa[j], fb[j], dot);
-          na = fmaf(fa[j], fa[j], na);
-          nb = fmaf(fb[j], fb[j], nb);
+        for (int u = 0; u < U; ++u) {
+          const int c = c0 + u * 32;
+          if (c < nv) {
+            ua[u] = ld_nc_v4(a + c);
+            ub[u] = b[c];
+          }
         }
-        b[c] = ua;  // commit C_cache <- C (Alg. 3 line 16)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int c = c0 + u * 32;
+          if (c < nv) {
+            float fa[8], fb[8];
+            unpack8(ua[u], fa);
+            unpack8(ub[u], fb);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              dot = fmaf(fa[j], fb[j], dot);
+              na = fmaf(fa[j], fa[j], na);
+              nb = fmaf(fb[j], fb[j], nb);
+            }
+            b[c] = ua[u];  // commit C_cache <- C (Alg. 3 line 16)
+          }
+        }
       }
       dot = warp_sum(dot);
       na = warp_sum(na);
@@ -325,8 +386,8 @@ __global__ void __launch_bounds__(256) select_salient_kernel(
     // fraction-controlled mode (D19): per sequence, tau* = the similarity of rank k = round(f*L)
     // (0-based) found by an 8-bit radix select over the order-preserving uint32 keys of s, then
     // the masks are rebuilt as s < tau* (k rows when there are no ties).
-    __shared__ unsigned hist[8][256];
-    for (int sq = warp; sq < batch; sq += 8) {
+    __shared__ unsigned hist[kSelWarps][256];
+    for (int sq = warp; sq < batch; sq += kSelWarps) {
       const float *sv = sim_out + static_cast<int64_t>(sq) * N + row_lo;
       const int k = static_cast<int>(floorf(frac * L + 0.5f));
       float thr = INFINITY;
@@ -389,7 +450,7 @@ __global__ void __launch_bounds__(256) select_salient_kernel(
     __syncthreads();
   }
   // per-sequence counts (one warp per sequence, strided)
-  for (int sq = warp; sq < batch; sq += 8) {
+  for (int sq = warp; sq < batch; sq += kSelWarps) {
     int c = 0;
     for (int w = lane; w < nchunks; w += 32) c += __popc(__ldcg(masks + sq * nchunks + w));
     c = warp_sum_i(c);
@@ -406,7 +467,7 @@ __global__ void __launch_bounds__(256) select_salient_kernel(
     if (counts_out && sq < batch) counts_out[sq] = seq_base[sq + 1] - seq_base[sq];
   }
   // each warp handles one sequence at a time: prefix over its words via ballots of popcounts
-  for (int sq = warp; sq < batch; sq += 8) {
+  for (int sq = warp; sq < batch; sq += kSelWarps) {
     int base = seq_base[sq];
     for (int w0 = 0; w0 < nchunks; w0 += 32) {
       const int w = w0 + lane;
@@ -653,7 +714,7 @@ void launch_select(const bf16 *c_new, bf16 *c_cache, int batch, int N, int row_l
                    int *counts, cudaStream_t st) {
   const int L = N - row_lo;
   dim3 grid((L + kSelRowsPerCta - 1) / kSelRowsPerCta, batch);
-  select_salient_kernel<<<grid, 256, 0, st>>>(c_new, c_cache, N, row_lo, width, tau, cmp, frac, idx_out, off_out,
+  select_salient_kernel<<<grid, kSelThreads, 0, st>>>(c_new, c_cache, N, row_lo, width, tau, cmp, frac, idx_out, off_out,
                                               sim_out, masks, ticket, counts);
 }
 void launch_lm_candidates(const int *tokens, int batch, int L_P, int L_R, int block, int mask_id, int *rows, int *off,

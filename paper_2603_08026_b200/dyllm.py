@@ -80,6 +80,7 @@ def _load():
         "dyllm_ctx_profile": (I, [P, I]),
         "dyllm_ctx_profile_read": (I, [P, I, P, I]),
         "dyllm_launch_count": (U64, []),
+        "dyllm_set_option": (I, [I, I]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -94,6 +95,14 @@ EXPORTED = [n for n in dir(_lib) if n.startswith("dyllm_")]
 
 def lib():
     return _lib
+
+
+OPT_SKINNY_GEMM = 1
+
+
+def set_option(option: int, value: int) -> int:
+    """Process-wide kernel-path option; returns the previous value."""
+    return _check(_lib.dyllm_set_option(option, value))
 
 
 def _check(rc):

@@ -44,6 +44,37 @@ def test_gemm_vs_torch(dy, ctx, M_cap, M, N, K):
     assert torch.all(D[M:] == 7.0)            # rows beyond the device count untouched
 
 
+@pytest.mark.parametrize("skinny", [1, 0])
+@pytest.mark.parametrize("M_cap,M,N,K", [
+    (512, 16, 256, 64),         # one activation MMA, one weight pair
+    (512, 205, 4096, 4096),     # f = 5% row count
+    (512, 410, 12288, 4096),    # two activation MMAs (256 + 160)
+    (512, 512, 512, 12288),     # maximum skinny M, long K
+    (1024, 700, 1024, 256),     # device M > 512: skinny exits, standard kernel computes
+])
+def test_gemm_skinny_vs_torch(dy, ctx, skinny, M_cap, M, N, K):
+    prev = dy.set_option(dy.OPT_SKINNY_GEMM, skinny)
+    try:
+        g = torch.Generator(device="cuda").manual_seed(M + N + K)
+        A = (torch.randn(M_cap, K, device="cuda", generator=g) * 0.5).bfloat16()
+        W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+        R = torch.randn(M_cap, N, device="cuda", generator=g).bfloat16()
+        B = torch.randn(N, device="cuda", generator=g).bfloat16()
+        Md = torch.tensor([M], dtype=torch.int32, device="cuda")
+        for resid in (None, R):
+            D = torch.full((M_cap, N), 7.0, device="cuda").bfloat16()
+            ctx.gemm_bf16(A, W, D, M_dev=Md, resid=resid, bias=B)
+            torch.cuda.synchronize()
+            ref = A[:M].float() @ W.float().T + B.float()
+            if resid is not None:
+                ref = ref + R[:M].float()
+            err = ((D[:M].float() - ref).abs().max() / ref.abs().max()).item()
+            assert err < 1e-2, (resid is not None, err)
+            assert torch.all(D[M:] == 7.0)
+    finally:
+        dy.set_option(dy.OPT_SKINNY_GEMM, prev)
+
+
 def test_gemm_residual_and_bias(dy, ctx):
     M, N, K = 200, 256, 192
     A = torch.randn(M, K, device="cuda").bfloat16()
