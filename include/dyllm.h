@@ -84,8 +84,9 @@ enum { DYLLM_K = 0, DYLLM_V = 1, DYLLM_Q = 2, DYLLM_C = 3, DYLLM_H = 4 };
 const char *dyllm_last_error(void);
 int dyllm_version(void);                 /* returns an integer version, e.g. 100 */
 
-/* Create a context on `device`; `cuda_stream` is a cudaStream_t (NULL = a new stream owned by
- * the ctx). Synchronous. */
+/* Create a context on `device`; `cuda_stream` is a cudaStream_t every call of the ctx launches on
+ * (NULL = a new non-blocking stream owned by the ctx; pass cudaStreamLegacy, 0x1, for the legacy
+ * default stream). Synchronous. */
 int dyllm_ctx_create(int device, void *cuda_stream, dyllm_ctx **out);
 int dyllm_ctx_sync(dyllm_ctx *ctx);      /* synchronous: waits for the ctx stream */
 void dyllm_ctx_destroy(dyllm_ctx *ctx);
@@ -203,8 +204,16 @@ uint64_t dyllm_launch_count(void);
 /* Process-wide kernel-path options (A/B testing and parity of alternative kernels).
  * DYLLM_OPT_SKINNY_GEMM (default 1): route GEMMs whose device row count is <= 512 to the 2-CTA
  * weight-stationary kernel; 0 = always the 1-CTA kernel. Returns the previous value. */
-enum { DYLLM_OPT_SKINNY_GEMM = 1 };
+/* DYLLM_OPT_SKINNY_SPLIT (default 0 = auto): split-K granularity of the skinny kernel, in units
+ * per 256-row weight block (clamped to a divisor of K/64); results are identical for every value
+ * up to fp32 summation order. */
+enum { DYLLM_OPT_SKINNY_GEMM = 1, DYLLM_OPT_SKINNY_SPLIT = 2 };
 int dyllm_set_option(int option, int value);
+
+/* Debug hook: when d_buf != NULL, kernels of family `which` (0 = skinny GEMM) write %globaltimer
+ * stamps of their phases to d_buf ([grid][16] uint64, caller-owned device memory, must hold one
+ * row per CTA of every traced launch). NULL disables. Process-wide; not thread-safe. */
+int dyllm_debug_trace_buffer(int which, void *d_buf);
 
 #ifdef __cplusplus
 }

@@ -45,6 +45,8 @@ struct dyllm_ctx {
   int num_sms = 148;
   unsigned *masks = nullptr;   // K1 ballot words (capacity kMaskCap)
   unsigned *ticket = nullptr;  // K1 last-CTA ticket
+  float *sk_ws = nullptr;      // skinny GEMM split-K partials
+  int *sk_ctr = nullptr;       // skinny GEMM split-K counters
   // instrumentation
   bool prof = false;
   int cls_offset = 0;          // DYLLM_KC_FULL while a FullStep enqueues
@@ -195,6 +197,9 @@ int dyllm_ctx_create(int device, void *cuda_stream, dyllm_ctx **out) {
   DY_CUDA(cudaMalloc(&c->masks, kMaskCap * sizeof(unsigned)));
   DY_CUDA(cudaMalloc(&c->ticket, sizeof(unsigned)));
   DY_CUDA(cudaMemset(c->ticket, 0, sizeof(unsigned)));
+  DY_CUDA(cudaMalloc(&c->sk_ws, skinny_ws_floats(c->num_sms) * sizeof(float)));
+  DY_CUDA(cudaMalloc(&c->sk_ctr, kSkinnyCtrCap * sizeof(int)));
+  DY_CUDA(cudaMemset(c->sk_ctr, 0, kSkinnyCtrCap * sizeof(int)));
   *out = c;
   return DYLLM_OK;
 }
@@ -210,6 +215,8 @@ void dyllm_ctx_destroy(dyllm_ctx *ctx) {
   cudaStreamSynchronize(ctx->stream);
   cudaFree(ctx->masks);
   cudaFree(ctx->ticket);
+  cudaFree(ctx->sk_ws);
+  cudaFree(ctx->sk_ctr);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -477,6 +484,8 @@ static int gemm(dyllm_ctx *ctx, const int *M_ptr, int M_cap, int N, int K, const
   g.bias = bias;
   g.partials = partials;
   g.epi = epi;
+  g.ws = ctx->sk_ws;
+  g.ctr = ctx->sk_ctr;
   return gemm_launch(g, ctx->num_sms, ctx->stream);
 }
 
@@ -748,7 +757,21 @@ int dyllm_set_option(int option, int value) {
     g_skinny_enabled = value != 0;
     return prev;
   }
+  if (option == DYLLM_OPT_SKINNY_SPLIT) {
+    const int prev = g_skinny_split;
+    g_skinny_split = value < 0 ? 0 : value;
+    return prev;
+  }
   set_error("unknown option");
+  return DYLLM_E_ARG;
+}
+
+int dyllm_debug_trace_buffer(int which, void *d_buf) {
+  if (which == 0) {
+    g_skinny_trace = static_cast<unsigned long long *>(d_buf);
+    return DYLLM_OK;
+  }
+  set_error("unknown trace buffer");
   return DYLLM_E_ARG;
 }
 

@@ -28,6 +28,7 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 bytes = one SWIZZLE_128B row
 constexpr int kGemmThreads = 192;
 constexpr int kGroupN = 8;
+constexpr int kPrefetchKb = 8;
 
 template <int BN>
 struct GemmCfg {
@@ -85,6 +86,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int num_n = (p.N + BN - 1) / BN;
   const int total = (M <= p.m_skip_le) ? 0 : num_m * num_n;  // small M: the skinny kernel runs
   const int num_kb = p.K / BK;
+  if (total == 0) return;  // uniform: the skinny kernel owns this row count (or M == 0)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -113,7 +115,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         int mb, nb;
         tile_coords(t, num_m, num_n, mb, nb);
+        // weight tiles: L2 prefetch kPrefetchKb k-blocks ahead of the shared-memory ring
+        for (int kb = 0; kb < kPrefetchKb && kb < num_kb; ++kb) tma_prefetch_l2_2d(&tmB, kb * BK, nb * BN);
         for (int kb = 0; kb < num_kb; ++kb) {
+          if (kb + kPrefetchKb < num_kb) tma_prefetch_l2_2d(&tmB, (kb + kPrefetchKb) * BK, nb * BN);
           mbar_wait(&empty_bar[stage], phase ^ 1);
           mbar_expect_tx(&full_bar[stage], C::STAGE_BYTES);
           tma_load_2d(smA + stage * C::A_BYTES, &tmA, &full_bar[stage], kb * BK, mb * BM);

@@ -48,6 +48,8 @@ struct GemmCall {
   float4 *partials = nullptr;       // EPI_LMHEAD: [M_cap][n_tiles] (max, sumexp, argmax, 0)
   int epi = EPI_BF16;
   int m_skip_le = 0;  // standard kernel: do nothing when the device row count is <= this
+  float *ws = nullptr;  // skinny split-K workspace (skinny_ws_floats(num_sms) floats per ctx)
+  int *ctr = nullptr;   // skinny split-K counters (kSkinnyCtrCap, zero between launches)
 };
 int gemm_launch(const GemmCall &g, int num_sms, cudaStream_t st);
 // 2D bf16 tensor map [rows][K] (K contiguous), box {64, box_rows}, SWIZZLE_128B
@@ -55,7 +57,11 @@ int make_tmap(CUtensorMap *m, const void *ptr, int rows, int K, int box_rows);
 int gemm_lmhead_ntiles(int N);
 bool skinny_eligible(const GemmCall &g);
 constexpr int kSkinnyMaxM = 512;
+constexpr int kSkinnyCtrCap = 4096;  // 2 counters per 256-row weight block
+inline int64_t skinny_ws_floats(int num_sms) { return static_cast<int64_t>(num_sms) * 512 * 256; }
 extern bool g_skinny_enabled;  // test hook (dyllm_set_option)
+extern unsigned long long *g_skinny_trace;
+extern int g_skinny_split;  // test hook: units per weight block (0 = auto)  // debug hook (dyllm_debug_trace_buffer)
 int gemm_skinny_launch(const GemmCall &g, int num_sms, cudaStream_t st);  // gemm_skinny.cu
 
 // ------------------------------------------------------------------ kernels (kernels.cu)

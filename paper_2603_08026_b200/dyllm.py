@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libdyllm.so")
 OK, DONE = 0, 1
 INPUT_FULL, INPUT_RESPONSE = 0, 1
 K, V, Q, CTX, H = 0, 1, 2, 3, 4
+_CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
 
 
 class DyllmError(RuntimeError):
@@ -81,6 +82,7 @@ def _load():
         "dyllm_ctx_profile_read": (I, [P, I, P, I]),
         "dyllm_launch_count": (U64, []),
         "dyllm_set_option": (I, [I, I]),
+        "dyllm_debug_trace_buffer": (I, [I, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -97,7 +99,7 @@ def lib():
     return _lib
 
 
-OPT_SKINNY_GEMM = 1
+OPT_SKINNY_GEMM, OPT_SKINNY_SPLIT = 1, 2
 
 
 def set_option(option: int, value: int) -> int:
@@ -148,7 +150,11 @@ class Context:
         self.device = device
         self.stream = stream if stream is not None else torch.cuda.current_stream(device)
         h = C.c_void_p()
-        _check(_lib.dyllm_ctx_create(device, C.c_void_p(self.stream.cuda_stream), C.byref(h)))
+        # The library launches on the caller's stream so its kernels are ordered with torch's
+        # copies and events. torch's default stream has handle 0, which the ABI reads as "create
+        # a private stream"; pass cudaStreamLegacy (0x1), the same legacy default stream, instead.
+        handle = self.stream.cuda_stream or _CUDA_STREAM_LEGACY
+        _check(_lib.dyllm_ctx_create(device, C.c_void_p(handle), C.byref(h)))
         self.h = h
 
     def sync(self):

@@ -49,7 +49,9 @@ def test_gemm_vs_torch(dy, ctx, M_cap, M, N, K):
     (512, 16, 256, 64),         # one activation MMA, one weight pair
     (512, 205, 4096, 4096),     # f = 5% row count
     (512, 410, 12288, 4096),    # two activation MMAs (256 + 160)
-    (512, 512, 512, 12288),     # maximum skinny M, long K
+    (512, 512, 512, 12288),     # maximum skinny M, long K (dozens of split-K contributors per block)
+    (512, 300, 4096, 12288),    # FFN-down shape: 16 weight blocks split over all SM pairs
+    (512, 100, 24576, 4096),    # gate/up width, M <= 256 (double-buffered TMEM accumulator)
     (1024, 700, 1024, 256),     # device M > 512: skinny exits, standard kernel computes
 ])
 def test_gemm_skinny_vs_torch(dy, ctx, skinny, M_cap, M, N, K):
@@ -71,8 +73,35 @@ def test_gemm_skinny_vs_torch(dy, ctx, skinny, M_cap, M, N, K):
             err = ((D[:M].float() - ref).abs().max() / ref.abs().max()).item()
             assert err < 1e-2, (resid is not None, err)
             assert torch.all(D[M:] == 7.0)
+            # split-K partials are reduced in a fixed contributor order: bit-identical reruns
+            D2 = torch.full((M_cap, N), 7.0, device="cuda").bfloat16()
+            ctx.gemm_bf16(A, W, D2, M_dev=Md, resid=resid, bias=B)
+            torch.cuda.synchronize()
+            assert torch.equal(D, D2)
     finally:
         dy.set_option(dy.OPT_SKINNY_GEMM, prev)
+
+
+@pytest.mark.parametrize("S", [1, 2, 3, 4, 16, 64])
+@pytest.mark.parametrize("M,N,K", [(410, 4096, 4096), (100, 12288, 4096), (257, 512, 1024)])
+def test_gemm_skinny_split_granularity(dy, ctx, S, M, N, K):
+    """Every split-K granularity gives the same result (fixed-order fp32 reduction)."""
+    prev = dy.set_option(dy.OPT_SKINNY_SPLIT, S)
+    try:
+        g = torch.Generator(device="cuda").manual_seed(S * 7 + M)
+        A = (torch.randn(512, K, device="cuda", generator=g) * 0.5).bfloat16()
+        W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+        R = torch.randn(512, N, device="cuda", generator=g).bfloat16()
+        Md = torch.tensor([M], dtype=torch.int32, device="cuda")
+        D = torch.full((512, N), 7.0, device="cuda").bfloat16()
+        ctx.gemm_bf16(A, W, D, M_dev=Md, resid=R)
+        torch.cuda.synchronize()
+        ref = A[:M].float() @ W.float().T + R[:M].float()
+        err = ((D[:M].float() - ref).abs().max() / ref.abs().max()).item()
+        assert err < 1e-2, err
+        assert torch.all(D[M:] == 7.0)
+    finally:
+        dy.set_option(dy.OPT_SKINNY_SPLIT, prev)
 
 
 def test_gemm_residual_and_bias(dy, ctx):
