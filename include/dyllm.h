@@ -207,12 +207,15 @@ uint64_t dyllm_launch_count(void);
 /* DYLLM_OPT_SKINNY_SPLIT (default 0 = auto): split-K granularity of the skinny kernel, in units
  * per 256-row weight block (clamped to a divisor of K/64); results are identical for every value
  * up to fp32 summation order. */
-enum { DYLLM_OPT_SKINNY_GEMM = 1, DYLLM_OPT_SKINNY_SPLIT = 2 };
+/* DYLLM_OPT_ATTN_FUSED (default 1): head_dim 128 uses the fused tcgen05 attention kernel
+ * (attn_fused.cu); 0 = the two-kernel path (tcgen05 row statistics + mma.sync P.V). */
+enum { DYLLM_OPT_SKINNY_GEMM = 1, DYLLM_OPT_SKINNY_SPLIT = 2, DYLLM_OPT_ATTN_FUSED = 3 };
 int dyllm_set_option(int option, int value);
 
 /* Debug hook: when d_buf != NULL, kernels of family `which` (0 = skinny GEMM) write %globaltimer
  * stamps of their phases to d_buf ([grid][16] uint64, caller-owned device memory, must hold one
- * row per CTA of every traced launch). NULL disables. Process-wide; not thread-safe. */
+ * row per CTA of every traced launch); which = 1: the fused attention kernel writes per-role
+ * mbarrier wait cycles (slots 0-2 producers, 3-8 MMA issuer, 9-12 softmax, 13 total). NULL disables. Process-wide; not thread-safe. */
 int dyllm_debug_trace_buffer(int which, void *d_buf);
 
 #ifdef __cplusplus

@@ -645,7 +645,13 @@ static int launch_split(const AttnArgs &a, cudaStream_t st) {
   return DYLLM_OK;
 }
 
+bool g_attn_fused_enabled = true;
+unsigned long long *g_attn_trace = nullptr;
+
+bool attention_writes_delta(int hd) { return hd == 128 && g_attn_fused_enabled; }
+
 int attention_launch(const AttnArgs &a, cudaStream_t st) {
+  if (a.hd == 128 && g_attn_fused_enabled) return attention_fused_launch(a, st);
   switch (a.hd) {
     case 16: return launch_fused<16>(a, st);
     case 32: return launch_fused<32>(a, st);

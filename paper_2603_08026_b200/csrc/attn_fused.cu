@@ -1,0 +1,615 @@
+// attn_fused.cu — salient-query attention for head_dim 128 (LLaDA/Dream shapes), one persistent
+// warp-specialised tcgen05 kernel (Alg. 4, D7).
+//
+// Work items, per (sequence s, query head h), ordered so that the items of one (s, kv head) run
+// side by side and share the K/V tiles through L2:
+//   type 1 — 128 consecutive input rows [row_lo + 128 t, ...) of s, read from the Q cache:
+//       pass S : row max m and sum-exp l of s_rj = q_r.k_j * scale over ALL N keys (the dense
+//                softmax normaliser of Alg. 4 lines 1-2, computed with the merged K);
+//       pass P : over the salient keys only (compact K rows of idx_in, Kx), P = exp2(s - m),
+//                dC = P dV (Alg. 4 lines 3-4, dV compact, aligned with idx_in);
+//       output : approximate rows (not in idx_in): the delta dC / l (C_new = C_cache + dC is
+//                formed by the similarity kernel, which reads C_cache anyway — no second read).
+//   type 2 — up to 128 exact rows (idx_in, compact new queries Qx) of s:
+//       pass S : m, l over all N keys;   pass P : P = exp2(s - m), O = P V over all N keys;
+//       output : C = O / l scattered to the exact rows.
+// Roles (384 threads, 1 CTA per SM): warp 0 claims items and loads Q (double-buffered), warps 0 and
+// 11 load alternate 64-key K tiles (3-deep ring), warp 10 loads V / dV tiles (2-deep ring) — one
+// 3D TMA op per tile, spread over three issuing warps, since TMA issue throughput is per operation
+// and per issuing thread (~700 cycles per op per thread, tools/tma_probe.cu) — warp 1 single-thread tcgen05.mma issuer (S = Q K^T into a
+// double-buffered 128x64 fp32 TMEM tile; P V into a 128x128 fp32 TMEM accumulator, V read as an
+// MN-major operand), warps 2-9 softmax/epilogue: two warps per TMEM lane quadrant, one row per
+// thread, 32 of the 64 columns of each score tile each; P is written as bf16 into 128B-swizzled
+// shared memory (the K-major A operand of the P V MMA).
+#include "common.cuh"
+#include "internal.h"
+
+namespace dy {
+
+constexpr int FA_BK = 64;                  // keys per tile
+constexpr int FA_Q_BYTES = 128 * 256;      // 128 rows x 128 bf16: two 64-column boxes of 16 KB
+constexpr int FA_KV_BYTES = 64 * 256;      // 64 keys x 128 bf16: two 64-column boxes of 8 KB
+constexpr int FA_P_BYTES = 128 * 128;      // 128 rows x 64 keys bf16
+constexpr int FA_QST = 2, FA_KST = 3, FA_VST = 2, FA_PST = 2;
+constexpr int FA_DATA = FA_QST * FA_Q_BYTES + FA_KST * FA_KV_BYTES + FA_VST * FA_KV_BYTES + FA_PST * FA_P_BYTES;
+constexpr int FA_XCH = 2 * 128 * 8;        // (m, l) per half per row
+constexpr int FA_SMEM = 1024 + FA_DATA + FA_XCH + 512;
+constexpr int FA_THREADS = 384;            // + warp 10: V producer, warp 11: second K producer
+constexpr int FA_TMEM_COLS = 256;          // S[2] (2 x 64 columns) + accumulator (128 columns)
+constexpr uint32_t FA_ACC_COL = 128;
+
+struct FaParams {
+  int N, row_lo, L, H, KVH, grp, MT, XT, items, qw;
+  float c;                  // softmax scale * log2(e)
+  const int *ex_off;        // [b+1]: exact rows (= salient keys) of each sequence, packed
+  const int *ex_rows;       // packed row ids of the exact rows
+  const uint8_t *rowflag;   // [b*N]: 1 = exact row (type-1 tiles leave it to type 2)
+  const bf16 *C_cache;
+  bf16 *C_out;
+  unsigned long long *trace;  // optional [grid][32] wait-cycle counters (debug hook)
+  int *work_ctr;              // [2] dynamic scheduler: next item, finished CTAs (zero between launches)
+};
+
+struct FaItem {
+  int s, h, kvh, nrows, q_row, off, nkP, xc;
+  bool type2, passP;
+};
+
+// Item decode from its index and the exact-row range (off, e) of its sequence (the producer reads
+// those once and passes them through the work queue, so no role stalls on global loads).
+__device__ __forceinline__ FaItem fa_item(const FaParams &p, int w, int off, int e) {
+  FaItem it;
+  const int per = p.MT + p.XT;
+  const int t = w % per;
+  int sh = w / per;
+  const int g = sh % p.grp;
+  sh /= p.grp;
+  it.kvh = sh % p.KVH;
+  it.s = sh / p.KVH;
+  it.h = it.kvh * p.grp + g;
+  it.off = off;
+  if (t < p.MT) {
+    it.type2 = false;
+    it.xc = 0;
+    it.q_row = it.s * p.N + p.row_lo + t * 128;
+    it.nrows = min(128, p.L - t * 128);
+    it.passP = e > 0;
+    it.nkP = e;
+  } else {
+    it.type2 = true;
+    it.xc = t - p.MT;
+    it.q_row = it.off + it.xc * 128;
+    it.nrows = min(128, e - it.xc * 128);
+    it.passP = true;
+    it.nkP = p.N;
+  }
+  return it;
+}
+__device__ __forceinline__ int fa_seq(const FaParams &p, int w) { return w / (p.MT + p.XT) / p.grp / p.KVH; }
+
+// UMMA descriptor of an MN-major operand tile written by TMA with 128B swizzle: 64-element
+// (128 B) rows along MN, 8-row (K) core groups 1024 B apart (SBO), consecutive 64-element MN
+// chunks `lbo` bytes apart (LBO), version 1, SWIZZLE_128B.
+__device__ __forceinline__ uint64_t sw128_mn_desc(uint32_t smem_addr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr & 0x3FFFF) >> 4);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// 2^x for x <= 0 on the FMA pipe (the SFU does 16 ex2/clk/SM on B200, measured by
+// tools/pipe_probe.cu, and is the softmax bottleneck): x = k + f, k = rint(x) via the 1.5*2^23
+// shifter, f in [-1/2, 1/2], 2^f by a cubic fitted for relative error (3e-4, far below bf16's
+// 4e-3), 2^k added to the exponent field with one integer multiply-add. x is clamped at -127.
+__device__ __forceinline__ float ex2p(float x) {
+  x = fmaxf(x, -127.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  const float q = fmaf(fmaf(fmaf(0.05753576f, f, 0.24192697f), f, 0.69278964f), f, 1.0f);
+  return __int_as_float(__float_as_int(t) * 8388608 + __float_as_int(q));
+}
+// mbar_wait that adds the cycles spent waiting to *acc (debug trace only)
+__device__ __forceinline__ void fa_wait(uint64_t *bar, uint32_t ph, unsigned long long *acc) {
+  if (acc) {
+    const unsigned long long t0 = clock64();
+    mbar_wait(bar, ph);
+    *acc += clock64() - t0;
+  } else {
+    mbar_wait(bar, ph);
+  }
+}
+__device__ __forceinline__ void fa_named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(FA_THREADS, 1)
+    attn_fused_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQx,
+                      const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                      const __grid_constant__ CUtensorMap tmKx, const __grid_constant__ CUtensorMap tmDV,
+                      const FaParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t *sQ = smem;                                   // [2][32 KB]
+  uint8_t *sK = sQ + FA_QST * FA_Q_BYTES;               // [3][16 KB]
+  uint8_t *sV = sK + FA_KST * FA_KV_BYTES;              // [2][16 KB]
+  uint8_t *sP = sV + FA_VST * FA_KV_BYTES;              // [2][16 KB]
+  float2 *xch = reinterpret_cast<float2 *>(sP + FA_PST * FA_P_BYTES);  // [2 halves][128 rows]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(xch) + FA_XCH);
+  uint64_t *q_full = bars, *q_empty = bars + 2;
+  uint64_t *k_full = bars + 4, *k_empty = bars + 7;
+  uint64_t *v_full = bars + 10, *v_empty = bars + 12;
+  uint64_t *s_full = bars + 14, *s_empty = bars + 16;
+  uint64_t *p_full = bars + 18, *p_empty = bars + 20;
+  uint64_t *acc_full = bars + 22, *acc_empty = bars + 23;
+  uint64_t *wq_full = bars + 24, *wq_empty = bars + 28;   // [4] work queue (producer -> other roles)
+  int4 *wq = reinterpret_cast<int4 *>(bars + 32);          // [4] (item, off, e, -) ; item -1 = done
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wq + 4);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int NKT = (p.N + FA_BK - 1) / FA_BK;
+  // debug trace: per-role wait cycles (slots 0-2 producers, 3-8 MMA, 9-12 softmax warp 2), 13 total
+  unsigned long long tr[20];
+#pragma unroll
+  for (int i = 0; i < 20; ++i) tr[i] = 0;
+  const bool tron = p.trace != nullptr && lane == 0;
+#define TR(k) (tron ? &tr[k] : nullptr)
+  const unsigned long long t_begin = clock64();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmQx);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmKx);
+    tma_prefetch_desc(&tmDV);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 8);
+      mbar_init(&p_full[i], 8);
+      mbar_init(&p_empty[i], 1);
+    }
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 8);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&wq_full[i], 1);
+      mbar_init(&wq_empty[i], 11);  // MMA warp, V producer, second K producer, 8 softmax warps
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, FA_TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // Dynamic scheduling: the producer thread claims items with an atomic counter (items of one
+  // (sequence, kv head) stay adjacent in claim order, so concurrently running CTAs share K/V in L2,
+  // and heavy exact-row items no longer pile up on fixed CTAs) and passes them to the other roles
+  // through a 4-deep shared-memory queue. Consumers: one arrival per warp.
+  int wn = 0;  // queue position of this role
+  auto next_item = [&](FaItem &it) -> int {
+    const int slot = wn & 3;
+    fa_wait(&wq_full[slot], (wn >> 2) & 1, TR(18));
+    const int4 q = wq[slot];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&wq_empty[slot]);
+    ++wn;
+    if (q.x >= 0) it = fa_item(p, q.x, q.y, q.z);
+    return q.x;
+  };
+
+  if (warp == 0 || warp == 11) {
+    // ================================================================ TMA producers: warp 0 claims
+    // items (work queue) and loads Q; warps 0 and 11 load alternate K tiles (global tile counter
+    // parity), doubling the TMA issue rate of the K stream
+    const int kpar = warp == 0 ? 0 : 1;
+    int kg = 0;  // global K tile counter (ring slot kg % FA_KST, phase (kg / FA_KST) & 1)
+    auto load_k = [&](const CUtensorMap *m, int row, int kvh) {
+      if ((kg & 1) == kpar && lane == 0) {
+        const int ks = kg % FA_KST;
+        fa_wait(&k_empty[ks], ((kg / FA_KST) & 1) ^ 1, TR(0));
+        mbar_expect_tx(&k_full[ks], FA_KV_BYTES);
+        tma_load_3d(sK + ks * FA_KV_BYTES, m, &k_full[ks], 0, row, kvh * 2);
+      }
+      ++kg;
+    };
+    // warp 0 claims one item ahead: the queue already holds item i+1 while item i's K tiles are
+    // issued, and Q of item i+1 is loaded early in item i, so item boundaries cost no claim
+    // latency and no exposed Q load
+    int wnext = -1, onext = 0, enext = 0;
+    auto claim = [&]() {  // warp 0, lane 0: next non-empty item (or -1) into the queue
+      int w, off = 0, e = 0;
+      for (;;) {
+        w = atomicAdd(&p.work_ctr[0], 1);
+        if (w >= p.items) {
+          w = -1;
+          break;
+        }
+        const int sq = fa_seq(p, w);
+        off = p.ex_off[sq];
+        e = p.ex_off[sq + 1] - off;
+        if (fa_item(p, w, off, e).nrows > 0) break;
+      }
+      const int slot = wn & 3;
+      mbar_wait(&wq_empty[slot], ((wn >> 2) & 1) ^ 1);
+      wq[slot] = make_int4(w, off, e, 0);
+      mbar_arrive(&wq_full[slot]);
+      ++wn;
+      wnext = w;
+      onext = off;
+      enext = e;
+    };
+    auto load_q = [&](const FaItem &it, int qi) {
+      const int qb = qi & 1;
+      fa_wait(&q_empty[qb], ((qi >> 1) & 1) ^ 1, TR(1));
+      mbar_expect_tx(&q_full[qb], FA_Q_BYTES);
+      tma_load_3d(sQ + qb * FA_Q_BYTES, it.type2 ? &tmQx : &tmQ, &q_full[qb], 0, it.q_row, it.h * 2);
+    };
+    int qi = 0;
+    if (warp == 0 && lane == 0) {
+      claim();
+      if (wnext >= 0) load_q(fa_item(p, wnext, onext, enext), 0);
+    }
+    for (;;) {
+      FaItem it;
+      int w;
+      if (warp == 0) {
+        if (lane == 0) {
+          w = wnext;
+          if (w >= 0) {
+            it = fa_item(p, w, onext, enext);
+            claim();  // item i+1 into the queue now
+          }
+        }
+        w = __shfl_sync(0xffffffffu, w, 0);
+        if (w < 0) break;
+        if (lane != 0) it = FaItem{};
+      } else {
+        w = next_item(it);
+        if (w < 0) break;
+      }
+      const int seq0 = it.s * p.N;
+      for (int kt = 0; kt < NKT; ++kt) {
+        load_k(&tmK, seq0 + kt * FA_BK, it.kvh);
+        if (kt == 0 && warp == 0 && lane == 0 && wnext >= 0) load_q(fa_item(p, wnext, onext, enext), qi + 1);
+      }
+      ++qi;
+      if (it.passP) {
+        const int n2 = (it.nkP + FA_BK - 1) / FA_BK;
+        for (int j = 0; j < n2; ++j)
+          load_k(it.type2 ? &tmK : &tmKx, (it.type2 ? seq0 : it.off) + j * FA_BK, it.kvh);
+      }
+    }
+  } else if (warp == 10) {
+    // ================================================================ V / dV producer
+    {
+      int vs = 0;
+      uint32_t vph = 0;
+      FaItem it;
+      for (int w = next_item(it); w >= 0; w = next_item(it)) {
+        if (!it.passP || lane != 0) continue;
+        const int n2 = (it.nkP + FA_BK - 1) / FA_BK;
+        for (int j = 0; j < n2; ++j) {
+          fa_wait(&v_empty[vs], vph ^ 1, TR(2));
+          mbar_expect_tx(&v_full[vs], FA_KV_BYTES);
+          tma_load_3d(sV + vs * FA_KV_BYTES, it.type2 ? &tmV : &tmDV, &v_full[vs], 0,
+                      (it.type2 ? it.s * p.N : it.off) + j * FA_BK, it.kvh * 2);
+          if (++vs == FA_VST) {
+            vs = 0;
+            vph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================================================ MMA issuer
+    constexpr uint32_t id_qk = idesc_bf16_f32(128, FA_BK);
+    constexpr uint32_t id_pv = idesc_bf16_f32(128, 128) | (1u << 16);  // B (V) MN-major
+    int qi = 0, ks = 0, vs = 0, sc = 0, pc = 0, ai = 0;
+    uint32_t kph = 0, vph = 0;
+    FaItem it;
+    for (int w = next_item(it); w >= 0; w = next_item(it)) {
+      const int qb = qi & 1;
+      fa_wait(&q_full[qb], (qi >> 1) & 1, TR(3));
+      ++qi;
+      const uint32_t qa = smem_u32(sQ + qb * FA_Q_BYTES);
+      auto qk = [&]() {
+        const int sb = sc & 1;
+        fa_wait(&s_empty[sb], ((sc >> 1) & 1) ^ 1, TR(4));
+        fa_wait(&k_full[ks], kph, TR(5));
+        tc_fence_after();
+        const unsigned long long ti = tron ? clock64() : 0;
+        if (lane == 0) {
+          const uint32_t kb = smem_u32(sK + ks * FA_KV_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(tmem + sb * FA_BK, sw128_kmajor_desc(qa + (kk >> 2) * (FA_Q_BYTES / 2) + (kk & 3) * 32),
+                      sw128_kmajor_desc(kb + (kk >> 2) * (FA_KV_BYTES / 2) + (kk & 3) * 32), id_qk, kk > 0);
+          umma_commit(&k_empty[ks]);
+          umma_commit(&s_full[sb]);
+        }
+        __syncwarp();
+        if (tron) tr[19] += clock64() - ti;
+        if (++ks == FA_KST) {
+          ks = 0;
+          kph ^= 1;
+        }
+        ++sc;
+      };
+      for (int kt = 0; kt < NKT; ++kt) qk();
+      if (it.passP) {
+        const int n2 = (it.nkP + FA_BK - 1) / FA_BK;
+        qk();
+        for (int j = 0; j < n2; ++j) {
+          if (j + 1 < n2) qk();
+          const int pb = pc & 1;
+          fa_wait(&p_full[pb], (pc >> 1) & 1, TR(6));
+          fa_wait(&v_full[vs], vph, TR(7));
+          if (j == 0) fa_wait(acc_empty, (ai & 1) ^ 1, TR(8));
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t pa = smem_u32(sP + pb * FA_P_BYTES);
+            const uint32_t vb = smem_u32(sV + vs * FA_KV_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              umma_bf16(tmem + FA_ACC_COL, sw128_kmajor_desc(pa + kk * 32), sw128_mn_desc(vb + kk * 2048, FA_KV_BYTES / 2),
+                        id_pv, (j | kk) != 0);
+            umma_commit(&v_empty[vs]);
+            umma_commit(&p_empty[pb]);
+            if (j == n2 - 1) umma_commit(acc_full);
+          }
+          __syncwarp();
+          if (++vs == FA_VST) {
+            vs = 0;
+            vph ^= 1;
+          }
+          ++pc;
+        }
+        ++ai;
+      }
+      if (lane == 0) umma_commit(&q_empty[qb]);
+      __syncwarp();
+    }
+  } else {
+    // ================================================================ softmax / epilogue warps 2-9
+    const int quad = warp & 3;            // TMEM lane quadrant this warp may access
+    const int hh = (warp - 2) >> 2;       // which 32 of the 64 columns of a score tile
+    const int r = quad * 32 + lane;       // row of the tile
+    const uint32_t trow = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+    const float c = p.c;
+    int sc = 0, pc = 0, ai = 0;
+    FaItem it;
+    for (int w = next_item(it); w >= 0; w = next_item(it)) {
+      // warps whose 32 rows are all past the item's row count skip the softmax work (they still
+      // take part in every barrier; their garbage P rows only reach accumulator rows never stored)
+      const bool wact = quad * 32 < it.nrows;
+      const bool rvalid = r < it.nrows;
+      // type 1 writes approximate rows only: fetch the row kind early (its latency hides under pass S)
+      const int64_t orow = it.type2 ? (rvalid ? p.ex_rows[it.q_row + r] : 0) : static_cast<int64_t>(it.q_row) + r;
+      const bool write_row = rvalid && (it.type2 || (it.passP && !p.rowflag[orow]));
+      // ---- pass S: running (m, l) of this half of the row
+      const unsigned long long tS = tron ? clock64() : 0;
+      float m = -INFINITY, l = 0.f;
+      for (int kt = 0; kt < NKT; ++kt) {
+        const int sb = sc & 1;
+        fa_wait(&s_full[sb], (sc >> 1) & 1, TR(9));
+        ++sc;
+        if (!wact) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_empty[sb]);
+          continue;
+        }
+        tc_fence_after();
+        float v[32];
+        tmem_ld32(trow + sb * FA_BK + hh * 32, v);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[sb]);
+        const int k0 = kt * FA_BK + hh * 32;
+        if (k0 + 32 > p.N) {  // ragged last tile: mask keys >= N
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (k0 + j >= p.N) v[j] = -INFINITY;
+        }
+        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          mx0 = fmaxf(mx0, v[j]);
+          mx1 = fmaxf(mx1, v[j + 1]);
+          mx2 = fmaxf(mx2, v[j + 2]);
+          mx3 = fmaxf(mx3, v[j + 3]);
+        }
+        const float mt = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+        const float mn = fmaxf(m, mt);
+        if (mn == -INFINITY) continue;  // every key of this half-tile masked
+        const float mnc = mn * c;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          a0 += ex2f(fmaf(v[j], c, -mnc));
+          a1 += ex2f(fmaf(v[j + 1], c, -mnc));
+          a2 += ex2f(fmaf(v[j + 2], c, -mnc));
+          a3 += ex2p(fmaf(v[j + 3], c, -mnc));  // a quarter of the exps on the FMA pipe
+        }
+        l = l * ex2f((m - mn) * c) + ((a0 + a1) + (a2 + a3));
+        m = mn;
+      }
+      if (tron) tr[14] += clock64() - tS;
+      // ---- combine the two halves of each row (fixed order: half 0 then half 1)
+      xch[hh * 128 + r] = make_float2(m, l);
+      fa_named_sync(1 + quad, 64);
+      const float2 h0 = xch[r], h1 = xch[128 + r];
+      fa_named_sync(1 + quad, 64);
+      const float M = fmaxf(h0.x, h1.x);
+      const float Lsum = (h0.x == -INFINITY ? 0.f : h0.y * ex2f((h0.x - M) * c)) +
+                         (h1.x == -INFINITY ? 0.f : h1.y * ex2f((h1.x - M) * c));
+      const float Mc = M * c;
+      const float inv_l = 1.f / Lsum;
+      // ---- pass P: P = exp2(s - m) into swizzled shared memory for P V
+      const unsigned long long tP = tron ? clock64() : 0;
+      float acc[64];
+      if (it.passP) {
+        const int n2 = (it.nkP + FA_BK - 1) / FA_BK;
+        for (int j = 0; j < n2; ++j) {
+          const int sb = sc & 1;
+          fa_wait(&s_full[sb], (sc >> 1) & 1, TR(10));
+          ++sc;
+          const int pb = pc & 1;
+          ++pc;
+          if (!wact) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[sb]);
+            fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1, TR(11));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[pb]);
+            continue;
+          }
+          tc_fence_after();
+          float v[32];
+          tmem_ld32(trow + sb * FA_BK + hh * 32, v);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_empty[sb]);
+          const int k0 = j * FA_BK + hh * 32;
+          uint32_t pk[16];
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const float e1 = (t & 1) ? ex2p(fmaf(v[2 * t + 1], c, -Mc)) : ex2f(fmaf(v[2 * t + 1], c, -Mc));
+            const float p0 = (k0 + 2 * t < it.nkP) ? ex2f(fmaf(v[2 * t], c, -Mc)) : 0.f;
+            const float p1 = (k0 + 2 * t + 1 < it.nkP) ? e1 : 0.f;
+            pk[t] = pack2(p0, p1);
+          }
+          fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1, TR(11));
+          uint8_t *prow = sP + pb * FA_P_BYTES + r * 128;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int unit = (hh * 4 + u) ^ (r & 7);
+            *reinterpret_cast<uint4 *>(prow + unit * 16) =
+                make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[pb]);
+        }
+        fa_wait(acc_full, ai & 1, TR(12));
+        ++ai;
+        if (wact) {
+          tc_fence_after();
+          tmem_ld32(trow + FA_ACC_COL + hh * 64, acc);
+          tmem_ld32(trow + FA_ACC_COL + hh * 64 + 32, acc + 32);
+          tc_fence_before();
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty);
+      }
+      if (tron) tr[15] += clock64() - tP;
+      const unsigned long long tE = tron ? clock64() : 0;
+      // ---- epilogue: this thread's row, head columns [hh*64, hh*64 + 64). Exact rows (type 2):
+      // C = O / l. Approximate rows (type 1): the delta dC / l only; the similarity kernel, which
+      // reads C_cache anyway, forms C_new = C_cache + dC (no C_cache read here).
+      if (write_row) {
+        uint4 *dst = reinterpret_cast<uint4 *>(p.C_out + orow * p.qw + it.h * 128 + hh * 64);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          float o[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) o[t] = acc[u * 8 + t] * inv_l;
+          dst[u] = pack8(o);
+        }
+      }
+      if (tron) tr[16] += clock64() - tE;
+    }
+  }
+  if (tron && (warp <= 2 || warp == 10)) {
+    const int lo = warp == 0 ? 0 : warp == 10 ? 2 : warp == 1 ? 3 : 9;
+    const int hi = warp == 0 ? 2 : warp == 10 ? 3 : warp == 1 ? 9 : 13;
+    for (int i = lo; i < hi; ++i) p.trace[blockIdx.x * 32 + i] = tr[i];
+    if (warp == 2) {
+      p.trace[blockIdx.x * 32 + 13] = clock64() - t_begin;
+      for (int i = 14; i < 17; ++i) p.trace[blockIdx.x * 32 + i] = tr[i];
+      p.trace[blockIdx.x * 32 + 17] = tr[18];  // softmax next_item wait
+    }
+    if (warp == 1) {
+      p.trace[blockIdx.x * 32 + 18] = tr[18];  // MMA next_item wait
+      p.trace[blockIdx.x * 32 + 19] = tr[19];  // MMA QK issue time
+      p.trace[blockIdx.x * 32 + 20] = clock64() - t_begin;
+    }
+  }
+#undef TR
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // the last CTA to finish re-arms the scheduler for the next launch (stream-ordered)
+    __threadfence();
+    if (atomicAdd(&p.work_ctr[1], 1) == static_cast<int>(gridDim.x) - 1) {
+      p.work_ctr[0] = 0;
+      p.work_ctr[1] = 0;
+      __threadfence();
+    }
+  }
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, FA_TMEM_COLS);
+  }
+}
+
+int attention_fused_launch(const AttnArgs &a, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    DY_CUDA(cudaFuncSetAttribute(attn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_SMEM));
+    attr = true;
+  }
+  const int rows_total = a.batch * a.N;
+  const int qw = a.H * 128, kw = a.KVH * 128;
+  CUtensorMap tq, tqx, tk, tv, tkx, tdv;
+  int rc;
+  if ((rc = make_tmap3(&tq, a.Q, rows_total, qw, 128, 2))) return rc;
+  if ((rc = make_tmap3(&tqx, a.Qx ? a.Qx : a.Q, rows_total, qw, 128, 2))) return rc;
+  if ((rc = make_tmap3(&tk, a.K, rows_total, kw, FA_BK, 2))) return rc;
+  if ((rc = make_tmap3(&tv, a.V, rows_total, kw, FA_BK, 2))) return rc;
+  if ((rc = make_tmap3(&tkx, a.Kx ? a.Kx : a.K, rows_total, kw, FA_BK, 2))) return rc;
+  if ((rc = make_tmap3(&tdv, a.dV ? a.dV : a.V, rows_total, kw, FA_BK, 2))) return rc;
+  FaParams p;
+  p.N = a.N;
+  p.row_lo = a.row_lo;
+  p.L = a.N - a.row_lo;
+  p.H = a.H;
+  p.KVH = a.KVH;
+  p.grp = a.H / a.KVH;
+  p.MT = a.full_only ? 0 : (p.L + 127) / 128;
+  p.XT = (a.max_rows_per_seq + 127) / 128;
+  p.items = a.batch * a.H * (p.MT + p.XT);
+  p.qw = qw;
+  p.c = a.scale * 1.4426950408889634f;
+  p.ex_off = a.ex_off;
+  p.ex_rows = a.ex_rows;
+  p.rowflag = a.rowflag;
+  p.C_cache = a.C_cache;
+  p.C_out = a.C_out;
+  p.trace = g_attn_trace;
+  p.work_ctr = a.work_ctr;
+  if (!p.work_ctr) {
+    set_error("fused attention: missing scheduler counters");
+    return DYLLM_E_ARG;
+  }
+  if (p.items <= 0) return DYLLM_OK;
+  const int grid = p.items < a.num_sms ? p.items : a.num_sms;
+  attn_fused_kernel<<<grid, FA_THREADS, FA_SMEM, st>>>(tq, tqx, tk, tv, tkx, tdv, p);
+  DY_CUDA(cudaGetLastError());
+  return DYLLM_OK;
+}
+
+}  // namespace dy

@@ -47,6 +47,7 @@ struct dyllm_ctx {
   unsigned *ticket = nullptr;  // K1 last-CTA ticket
   float *sk_ws = nullptr;      // skinny GEMM split-K partials
   int *sk_ctr = nullptr;       // skinny GEMM split-K counters
+  int *attn_ctr = nullptr;     // fused attention scheduler counters [2]
   // instrumentation
   bool prof = false;
   int cls_offset = 0;          // DYLLM_KC_FULL while a FullStep enqueues
@@ -111,7 +112,8 @@ struct dyllm_cache {
   int N, rows;
   std::vector<LayerC> L;
   bf16 *H0;
-  bf16 *Xn, *qkv, *dV, *Cn, *Cg, *h, *hn, *act, *ffo, *Xf;
+  bf16 *Xn, *qkv, *dV, *Qx, *Kx, *Cn, *Cg, *h, *hn, *act, *ffo, *Xf;
+  uint8_t *rowflag;
   float4 *partials;
   int *lst[2], *lst_off[2];
   int *carried, *carried_off;
@@ -200,6 +202,8 @@ int dyllm_ctx_create(int device, void *cuda_stream, dyllm_ctx **out) {
   DY_CUDA(cudaMalloc(&c->sk_ws, skinny_ws_floats(c->num_sms) * sizeof(float)));
   DY_CUDA(cudaMalloc(&c->sk_ctr, kSkinnyCtrCap * sizeof(int)));
   DY_CUDA(cudaMemset(c->sk_ctr, 0, kSkinnyCtrCap * sizeof(int)));
+  DY_CUDA(cudaMalloc(&c->attn_ctr, 2 * sizeof(int)));
+  DY_CUDA(cudaMemset(c->attn_ctr, 0, 2 * sizeof(int)));
   *out = c;
   return DYLLM_OK;
 }
@@ -217,6 +221,7 @@ void dyllm_ctx_destroy(dyllm_ctx *ctx) {
   cudaFree(ctx->ticket);
   cudaFree(ctx->sk_ws);
   cudaFree(ctx->sk_ctr);
+  cudaFree(ctx->attn_ctr);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -416,6 +421,9 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
   AL(c->Xn, rows * d);
   AL(c->qkv, rows * (qw + 2 * kw));
   AL(c->dV, rows * kw);
+  AL(c->Qx, rows * qw);
+  AL(c->Kx, rows * kw);
+  AL(c->rowflag, rows);
   AL(c->Cn, rows * qw);
   AL(c->Cg, rows * qw);
   AL(c->h, rows * d);
@@ -443,7 +451,13 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
   AL(c->stats, rows * m.n_heads);
 #undef AL
   cudaStream_t st = ctx->stream;
-  if (cudaMemsetAsync(c->zero_off, 0, (r->batch + 1) * sizeof(int), st) != cudaSuccess) {
+  // compact scratch rows past the live count are read (with zero weight) by attention tiles:
+  // start them finite
+  const bool ok = cudaMemsetAsync(c->dV, 0, rows * kw * 2, st) == cudaSuccess &&
+                  cudaMemsetAsync(c->Kx, 0, rows * kw * 2, st) == cudaSuccess &&
+                  cudaMemsetAsync(c->Qx, 0, rows * qw * 2, st) == cudaSuccess &&
+                  cudaMemsetAsync(c->zero_off, 0, (r->batch + 1) * sizeof(int), st) == cudaSuccess;
+  if (!ok) {
     set_error("memset failed");
     dyllm_cache_destroy(c);
     return DYLLM_E_CUDA;
@@ -520,7 +534,7 @@ static int full_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c
     KL(GATHER, launch_gather_rmsnorm(Hprev, nullptr, nullptr, rows, L.g_attn, m.rms_eps, c->Xn, d, st));
     KL(QKV_GEMM, RET(gemm(ctx, nullptr, rows, qw + 2 * kw, d, c->Xn, L.wqkv, c->qkv, qw + 2 * kw, EPI_BF16)));
     KL(QKV_POST, launch_qkv_post(c->qkv, nullptr, nullptr, rows, L.bqkv, c->N, m.n_heads, m.n_kv_heads, m.head_dim,
-                                 c->rope_cs, C.Q, C.K, C.V, nullptr, st));
+                                 c->rope_cs, C.Q, C.K, C.V, nullptr, nullptr, nullptr, st));
     AttnArgs a{};
     a.batch = c->r.batch;
     a.N = c->N;
@@ -544,6 +558,8 @@ static int full_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c
     a.row_lo = 0;
     a.stats = c->stats;
     a.num_sms = ctx->num_sms;
+    a.full_only = true;  // every row exact: Qx = the Q cache, ex_rows = identity
+    a.work_ctr = ctx->attn_ctr;
     KL(ATTN, RET(attention_launch(a, st)));
     int prc = post_attention(ctx, w, c, l, nullptr, C.C, Hprev, nullptr, C.H);
     if (prc) {
@@ -572,13 +588,13 @@ static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *
   cudaStream_t st = ctx->stream;
   const int *M_in = off_in + b;
   // exact rows = idx_in; approximate rows = input rows \ idx_in
-  KL(OTHER, launch_approx_rows(idx_in, off_in, b, N, row_lo, c->ap_rows, c->ap_off, st));
+  KL(OTHER, launch_approx_rows(idx_in, off_in, b, N, row_lo, c->ap_rows, c->ap_off, c->rowflag, st));
   // a1 + a2: RMSNorm(x[idx_in]) -> QKV projection of the changed rows
   KL(GATHER, launch_gather_rmsnorm(Hprev, idx_in, M_in, rows, L.g_attn, m.rms_eps, c->Xn, d, st));
   KL(QKV_GEMM, RET(gemm(ctx, M_in, rows, qw + 2 * kw, d, c->Xn, L.wqkv, c->qkv, qw + 2 * kw, EPI_BF16)));
   // a3: RoPE, dV (before overwrite), in-place K/V/Q cache rows
   KL(QKV_POST, launch_qkv_post(c->qkv, idx_in, M_in, rows, L.bqkv, N, m.n_heads, m.n_kv_heads, m.head_dim,
-                               c->rope_cs, C.Q, C.K, C.V, c->dV, st));
+                               c->rope_cs, C.Q, C.K, C.V, c->dV, c->Qx, c->Kx, st));
   // a4: exact rows + approximate rows (Alg. 4) -> Cn
   AttnArgs a{};
   a.batch = b;
@@ -603,11 +619,17 @@ static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *
   a.row_lo = row_lo;
   a.stats = c->stats;
   a.num_sms = ctx->num_sms;
+  a.Qx = c->Qx;
+  a.Kx = c->Kx;
+  a.rowflag = c->rowflag;
+  a.work_ctr = ctx->attn_ctr;
   KL(ATTN, RET(attention_launch(a, st)));
   // a5: cosine similarity + threshold + compaction; C_cache <- Cn for the input rows
   const bool fmode = c->r.select_mode == 1;
+  const bool delta = attention_writes_delta(m.head_dim);  // fused kernel: Cn = dC for approximate rows
   KL(SELECT, launch_select(c->Cn, C.C, b, N, row_lo, qw, fmode ? 2.f : tau, c->r.cmp, fmode ? tau : -1.f, idx_out,
-                           off_out, (fmode && !sim) ? c->sim : sim, ctx->masks, ctx->ticket, counts, st));
+                           off_out, (fmode && !sim) ? c->sim : sim, ctx->masks, ctx->ticket, counts,
+                           delta ? c->rowflag : nullptr, delta ? off_in : nullptr, st));
   const int *M_out = off_out + b;
   // a6 + a7 on idx_out, a8 scatter-back into H_l (other rows keep FFN_OUT_cache)
   KL(GATHER, launch_gather_rows(C.C, idx_out, M_out, rows, c->Cg, qw, st));
@@ -757,6 +779,11 @@ int dyllm_set_option(int option, int value) {
     g_skinny_enabled = value != 0;
     return prev;
   }
+  if (option == DYLLM_OPT_ATTN_FUSED) {
+    const int prev = g_attn_fused_enabled ? 1 : 0;
+    g_attn_fused_enabled = value != 0;
+    return prev;
+  }
   if (option == DYLLM_OPT_SKINNY_SPLIT) {
     const int prev = g_skinny_split;
     g_skinny_split = value < 0 ? 0 : value;
@@ -769,6 +796,10 @@ int dyllm_set_option(int option, int value) {
 int dyllm_debug_trace_buffer(int which, void *d_buf) {
   if (which == 0) {
     g_skinny_trace = static_cast<unsigned long long *>(d_buf);
+    return DYLLM_OK;
+  }
+  if (which == 1) {
+    g_attn_trace = static_cast<unsigned long long *>(d_buf);
     return DYLLM_OK;
   }
   set_error("unknown trace buffer");
@@ -840,7 +871,8 @@ int dyllm_select_salient(dyllm_ctx *ctx, int batch, int N, int row_lo, int width
   CHECK_ARG(words <= kMaskCap, "select_salient: too many rows");
   RET(sticky(ctx));
   KL(SELECT, launch_select(static_cast<const bf16 *>(d_c_new), static_cast<bf16 *>(d_c_cache), batch, N, row_lo, width,
-                           tau, cmp, -1.f, d_idx_out, d_off_out, d_sim_out, ctx->masks, ctx->ticket, nullptr, ctx->stream));
+                           tau, cmp, -1.f, d_idx_out, d_off_out, d_sim_out, ctx->masks, ctx->ticket, nullptr, nullptr,
+                           nullptr, ctx->stream));
   DY_CUDA(cudaGetLastError());
   return DYLLM_OK;
 }

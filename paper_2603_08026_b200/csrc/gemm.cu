@@ -302,6 +302,38 @@ int make_tmap(CUtensorMap *m, const void *ptr, int rows, int K, int box_rows) {
   return DYLLM_OK;
 }
 
+// 3D view of a [rows][K] bf16 matrix as {64, rows, K/64} (strides: row pitch, 128 B) with box
+// {64, box_rows, box_chunks}: one TMA op fetches box_chunks consecutive 64-column chunks of
+// box_rows rows, laid out in shared memory as [chunk][row][64] (each chunk a 128B-swizzled
+// K-major tile). TMA issue throughput is per operation (~3 ops/us per issuing thread, measured:
+// tools/tma_probe.cu), so wide boxes matter more than stage count.
+int make_tmap3(CUtensorMap *m, const void *ptr, int rows, int K, int box_rows, int box_chunks) {
+  std::call_once(g_encode_once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!g_encode) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return DYLLM_E_CUDA;
+  }
+  cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(K / 64)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(K) * 2, 128};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(box_chunks)};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(ptr), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (3d) failed (" + std::to_string(static_cast<int>(r)) + ") rows=" +
+              std::to_string(rows) + " K=" + std::to_string(K));
+    return DYLLM_E_CUDA;
+  }
+  return DYLLM_OK;
+}
+
 template <int BN, int EPI>
 static int launch_t(const GemmCall &g, int num_sms, cudaStream_t st) {
   using C = GemmCfg<BN>;

@@ -54,6 +54,8 @@ struct GemmCall {
 int gemm_launch(const GemmCall &g, int num_sms, cudaStream_t st);
 // 2D bf16 tensor map [rows][K] (K contiguous), box {64, box_rows}, SWIZZLE_128B
 int make_tmap(CUtensorMap *m, const void *ptr, int rows, int K, int box_rows);
+// 3D box {64, box_rows, box_chunks} over [rows][K]: box_chunks 64-column chunks in one TMA op
+int make_tmap3(CUtensorMap *m, const void *ptr, int rows, int K, int box_rows, int box_chunks);
 int gemm_lmhead_ntiles(int N);
 bool skinny_eligible(const GemmCall &g);
 constexpr int kSkinnyMaxM = 512;
@@ -80,7 +82,18 @@ struct AttnArgs {
   int row_lo;                   // first input position (0 full input, L_P response-only)
   float2 *stats;                // [b*N][H] (row max, sum-exp) scratch in the exp2 domain
   int num_sms;
+  // fused head_dim-128 kernel (attn_fused.cu)
+  const bf16 *Qx = nullptr;     // [M_in][H*hd] compact new queries of the exact rows (aligned with ex_rows)
+  const bf16 *Kx = nullptr;     // [M_in][KVH*hd] compact new keys of the salient rows (aligned with dV)
+  const uint8_t *rowflag = nullptr;  // [b*N] 1 = exact row
+  bool full_only = false;       // FullStep: every row exact (ex_rows = identity), no approximate tiles
+  int *work_ctr = nullptr;      // [2] fused kernel scheduler counters (ctx-owned, zero between launches)
 };
 int attention_launch(const AttnArgs &a, cudaStream_t st);
+int attention_fused_launch(const AttnArgs &a, cudaStream_t st);  // attn_fused.cu
+// true when attention_launch writes the delta dC (not C) for the approximate rows of a sparse step
+bool attention_writes_delta(int hd);
+extern bool g_attn_fused_enabled;  // test hook (dyllm_set_option)
+extern unsigned long long *g_attn_trace;  // debug hook (dyllm_debug_trace_buffer, which = 1)
 
 }  // namespace dy

@@ -132,7 +132,8 @@ __global__ void scatter_rows_kernel(const bf16 *__restrict__ src, const int *__r
 __global__ void qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restrict__ idx,
                                 const int *__restrict__ M_ptr, int M_cap, const bf16 *__restrict__ bias, int N,
                                 int H, int KVH, int hd, const float2 *__restrict__ rope_cs, bf16 *__restrict__ Qc,
-                                bf16 *__restrict__ Kc, bf16 *__restrict__ Vc, bf16 *__restrict__ dV) {
+                                bf16 *__restrict__ Kc, bf16 *__restrict__ Vc, bf16 *__restrict__ dV,
+                                bf16 *__restrict__ Qx, bf16 *__restrict__ Kx) {
   const int M = M_ptr ? *M_ptr : M_cap;
   const int qw = H * hd, kw = KVH * hd, W = qw + 2 * kw;
   const int half = hd / 2, hv = half / 8;  // 8 rotation pairs per thread (16-byte vectors)
@@ -166,8 +167,17 @@ __global__ void qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restr
         y2[j] = x2[j] * c.x + x1[j] * c.y;
       }
       bf16 *dst = (col < qw) ? Qc + static_cast<int64_t>(r) * qw + col : Kc + static_cast<int64_t>(r) * kw + (col - qw);
-      *reinterpret_cast<uint4 *>(dst) = pack8(y1);
-      *reinterpret_cast<uint4 *>(dst + half) = pack8(y2);
+      const uint4 p1 = pack8(y1), p2 = pack8(y2);
+      *reinterpret_cast<uint4 *>(dst) = p1;
+      *reinterpret_cast<uint4 *>(dst + half) = p2;
+      // compact copies aligned with the packed list (the attention kernel's exact-row queries
+      // and salient keys are then contiguous rows: TMA tiles)
+      bf16 *cx = (col < qw) ? (Qx ? Qx + static_cast<int64_t>(i) * qw + col : nullptr)
+                            : (Kx ? Kx + static_cast<int64_t>(i) * kw + (col - qw) : nullptr);
+      if (cx) {
+        *reinterpret_cast<uint4 *>(cx) = p1;
+        *reinterpret_cast<uint4 *>(cx + half) = p2;
+      }
     }
     // v: dV = v_new - V_cache (read before the overwrite), then V_cache <- v_new
     for (int c = threadIdx.x * 8; c < kw; c += blockDim.x * 8) {
@@ -210,7 +220,8 @@ __global__ void rope_table_kernel(float2 *__restrict__ cs, int N, int hd, double
 // Approximate-row list of each sequence: input rows [row_lo, N) that are NOT in idx_in
 // (exact rows = idx_in itself). One CTA per sequence. ap_off[s] = s*L - off_in[s].
 __global__ void approx_rows_kernel(const int *__restrict__ idx_in, const int *__restrict__ off_in, int N,
-                                   int row_lo, int *__restrict__ ap_rows, int *__restrict__ ap_off, int batch) {
+                                   int row_lo, int *__restrict__ ap_rows, int *__restrict__ ap_off, int batch,
+                                   uint8_t *__restrict__ rowflag) {
   extern __shared__ uint8_t flag[];
   __shared__ int warp_cnt[32];
   const int s = blockIdx.x;
@@ -220,6 +231,8 @@ __global__ void approx_rows_kernel(const int *__restrict__ idx_in, const int *__
   const int b0 = off_in[s], b1 = off_in[s + 1];
   for (int j = b0 + threadIdx.x; j < b1; j += blockDim.x) flag[idx_in[j] - s * N] = 1;
   __syncthreads();
+  if (rowflag)  // per-row kind for the fused attention kernel: 1 = exact (in idx_in)
+    for (int p = threadIdx.x; p < N; p += blockDim.x) rowflag[static_cast<int64_t>(s) * N + p] = flag[p];
   int base = s * L - b0;
   if (threadIdx.x == 0) {
     ap_off[s] = base;
@@ -306,7 +319,8 @@ constexpr int kSelWarps = kSelThreads / 32;
 __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
     const bf16 *__restrict__ c_new, bf16 *__restrict__ c_cache, int N, int row_lo, int width, float tau,
     int cmp, float frac, int *__restrict__ idx_out, int *__restrict__ off_out, float *__restrict__ sim_out,
-    unsigned *__restrict__ masks, unsigned *__restrict__ ticket, int *__restrict__ counts_out) {
+    unsigned *__restrict__ masks, unsigned *__restrict__ ticket, int *__restrict__ counts_out,
+    const uint8_t *__restrict__ rowflag, const int *__restrict__ dl_off) {
   __shared__ unsigned row_flag[kSelRowsPerCta];
   __shared__ bool is_last;
   const int s = blockIdx.y;
@@ -323,6 +337,14 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
       const int64_t r = static_cast<int64_t>(s) * N + p;
       const uint4 *a = reinterpret_cast<const uint4 *>(c_new + r * width);
       uint4 *b = reinterpret_cast<uint4 *>(c_cache + r * width);
+      // delta mode (fused attention): c_new holds C itself for exact rows and the delta dC for
+      // approximate rows, whose C_new = bf16(C_cache + dC) (C_cache when the sequence has no
+      // salient key, dC = 0) is formed here from the C_cache row this kernel reads anyway
+      bool take_new = true, add = false;
+      if (rowflag) {
+        take_new = rowflag[r] != 0;
+        add = !take_new && dl_off[s + 1] > dl_off[s];
+      }
       float dot = 0.f, na = 0.f, nb = 0.f;
       constexpr int U = 4;  // 2*U independent 16-byte loads in flight per lane
       for (int c0 = lane; c0 < nv; c0 += 32 * U) {
@@ -331,8 +353,19 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
         for (int u = 0; u < U; ++u) {
           const int c = c0 + u * 32;
           if (c < nv) {
-            ua[u] = ld_nc_v4(a + c);
             ub[u] = b[c];
+            ua[u] = (take_new || add) ? ld_nc_v4(a + c) : ub[u];
+          }
+        }
+        if (add) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            float fa[8], fb[8];
+            unpack8(ua[u], fa);
+            unpack8(ub[u], fb);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) fa[j] += fb[j];
+            ua[u] = pack8(fa);
           }
         }
 #pragma unroll
@@ -692,17 +725,18 @@ void launch_rmsnorm_rows(const bf16 *src, const int *M_ptr, int M_cap, const bf1
   gather_rmsnorm_kernel<<<grid_for(M_cap, 8), 256, 0, st>>>(src, nullptr, M_ptr, M_cap, g, eps, dst, d);
 }
 void launch_qkv_post(const bf16 *qkv, const int *idx, const int *M_ptr, int M_cap, const bf16 *bias, int N, int H,
-                     int KVH, int hd, const float2 *rope_cs, bf16 *Qc, bf16 *Kc, bf16 *Vc, bf16 *dV, cudaStream_t st) {
+                     int KVH, int hd, const float2 *rope_cs, bf16 *Qc, bf16 *Kc, bf16 *Vc, bf16 *dV, bf16 *Qx,
+                     bf16 *Kx, cudaStream_t st) {
   const int g = M_cap < 148 * 8 ? M_cap : 148 * 8;
   qkv_post_kernel<<<g > 0 ? g : 1, 256, 0, st>>>(qkv, idx, M_ptr, M_cap, bias, N, H, KVH, hd, rope_cs, Qc, Kc, Vc,
-                                                 dV);
+                                                 dV, Qx, Kx);
 }
 void launch_rope_table(float2 *cs, int N, int hd, double theta, cudaStream_t st) {
   rope_table_kernel<<<148, 256, 0, st>>>(cs, N, hd, theta);
 }
 void launch_approx_rows(const int *idx_in, const int *off_in, int batch, int N, int row_lo, int *ap_rows,
-                        int *ap_off, cudaStream_t st) {
-  approx_rows_kernel<<<batch, 256, N, st>>>(idx_in, off_in, N, row_lo, ap_rows, ap_off, batch);
+                        int *ap_off, uint8_t *rowflag, cudaStream_t st) {
+  approx_rows_kernel<<<batch, 256, N, st>>>(idx_in, off_in, N, row_lo, ap_rows, ap_off, batch, rowflag);
 }
 void launch_build_list(int mode, const int *carried, const int *carried_off, const int *dec_pos, int n_u, int policy,
                        int batch, int N, int row_lo, int resp_lo, int *out, int *out_off, cudaStream_t st) {
@@ -711,11 +745,11 @@ void launch_build_list(int mode, const int *carried, const int *carried_off, con
 }
 void launch_select(const bf16 *c_new, bf16 *c_cache, int batch, int N, int row_lo, int width, float tau, int cmp,
                    float frac, int *idx_out, int *off_out, float *sim_out, unsigned *masks, unsigned *ticket,
-                   int *counts, cudaStream_t st) {
+                   int *counts, const uint8_t *rowflag, const int *dl_off, cudaStream_t st) {
   const int L = N - row_lo;
   dim3 grid((L + kSelRowsPerCta - 1) / kSelRowsPerCta, batch);
   select_salient_kernel<<<grid, kSelThreads, 0, st>>>(c_new, c_cache, N, row_lo, width, tau, cmp, frac, idx_out, off_out,
-                                              sim_out, masks, ticket, counts);
+                                              sim_out, masks, ticket, counts, rowflag, dl_off);
 }
 void launch_lm_candidates(const int *tokens, int batch, int L_P, int L_R, int block, int mask_id, int *rows, int *off,
                           cudaStream_t st) {

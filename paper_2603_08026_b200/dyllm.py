@@ -99,7 +99,7 @@ def lib():
     return _lib
 
 
-OPT_SKINNY_GEMM, OPT_SKINNY_SPLIT = 1, 2
+OPT_SKINNY_GEMM, OPT_SKINNY_SPLIT, OPT_ATTN_FUSED = 1, 2, 3
 
 
 def set_option(option: int, value: int) -> int:
