@@ -14,29 +14,32 @@
 //       pass S : m, l over all N keys;   pass P : P = exp2(s - m), O = P V over all N keys;
 //       output : C = O / l scattered to the exact rows.
 // Roles (384 threads, 1 CTA per SM): warp 0 claims items and loads Q (double-buffered), warps 0 and
-// 11 load alternate 64-key K tiles (3-deep ring), warp 10 loads V / dV tiles (2-deep ring) — one
-// 3D TMA op per tile, spread over three issuing warps, since TMA issue throughput is per operation
-// and per issuing thread (~700 cycles per op per thread, tools/tma_probe.cu) — warp 1 single-thread tcgen05.mma issuer (S = Q K^T into a
-// double-buffered 128x64 fp32 TMEM tile; P V into a 128x128 fp32 TMEM accumulator, V read as an
-// MN-major operand), warps 2-9 softmax/epilogue: two warps per TMEM lane quadrant, one row per
-// thread, 32 of the 64 columns of each score tile each; P is written as bf16 into 128B-swizzled
-// shared memory (the K-major A operand of the P V MMA).
+// 11 load alternate 128-key K tiles (2-deep ring), warp 10 loads V / dV tiles (2-deep ring) — one
+// 32 KB 3D TMA op per tile, spread over three issuing warps, since TMA issue throughput is per
+// operation and per issuing thread (~700 cycles per op per thread, tools/tma_probe.cu) — warp 1
+// single-thread tcgen05.mma issuer (S = Q K^T, M = N = 128, into a double-buffered fp32 TMEM tile;
+// P V into a 128x128 fp32 TMEM accumulator with P read from TMEM and V as an MN-major smem
+// operand), warps 2-9 softmax/epilogue: two warps per TMEM lane quadrant, one row per thread, 64 of
+// the 128 columns of each score tile each; P is stored bf16x2-packed into TMEM with tcgen05.st.
 #include "common.cuh"
 #include "internal.h"
 
 namespace dy {
 
-constexpr int FA_BK = 64;                  // keys per tile
-constexpr int FA_Q_BYTES = 128 * 256;      // 128 rows x 128 bf16: two 64-column boxes of 16 KB
-constexpr int FA_KV_BYTES = 64 * 256;      // 64 keys x 128 bf16: two 64-column boxes of 8 KB
-constexpr int FA_P_BYTES = 128 * 128;      // 128 rows x 64 keys bf16
-constexpr int FA_QST = 2, FA_KST = 3, FA_VST = 2, FA_PST = 2;
-constexpr int FA_DATA = FA_QST * FA_Q_BYTES + FA_KST * FA_KV_BYTES + FA_VST * FA_KV_BYTES + FA_PST * FA_P_BYTES;
+constexpr int FA_BK = 128;                 // keys per tile (MMA N = 128: the Q operand read per
+                                           // instruction is amortised over 128 keys)
+constexpr int FA_Q_BYTES = 128 * 256;      // 128 rows x 128 bf16: two 64-column halves of 16 KB
+constexpr int FA_KV_BYTES = 128 * 256;     // 128 keys x 128 bf16: two 64-column halves of 16 KB
+constexpr int FA_QST = 2, FA_KST = 2, FA_VST = 2;
+constexpr int FA_DATA = FA_QST * FA_Q_BYTES + FA_KST * FA_KV_BYTES + FA_VST * FA_KV_BYTES;
 constexpr int FA_XCH = 2 * 128 * 8;        // (m, l) per half per row
 constexpr int FA_SMEM = 1024 + FA_DATA + FA_XCH + 512;
 constexpr int FA_THREADS = 384;            // + warp 10: V producer, warp 11: second K producer
-constexpr int FA_TMEM_COLS = 256;          // S[2] (2 x 64 columns) + accumulator (128 columns)
-constexpr uint32_t FA_ACC_COL = 128;
+// TMEM columns: S[2] (2 x 128 fp32), accumulator (128 fp32), P[2] (2 x 64: 128 keys bf16x2-packed,
+// the A operand of the P V MMA read straight from TMEM)
+constexpr int FA_TMEM_COLS = 512;
+constexpr uint32_t FA_ACC_COL = 256;
+constexpr uint32_t FA_P_COL = 384;
 
 struct FaParams {
   int N, row_lo, L, H, KVH, grp, MT, XT, items, qw;
@@ -115,6 +118,27 @@ __device__ __forceinline__ float ex2p(float x) {
   const float q = fmaf(fmaf(fmaf(0.05753576f, f, 0.24192697f), f, 0.69278964f), f, 1.0f);
   return __int_as_float(__float_as_int(t) * 8388608 + __float_as_int(q));
 }
+// D[tmem] (+)= A[tmem] * B[smem]^T (kind::f16, A read from tensor memory: M lanes x K/2 packed
+// bf16x2 columns)
+__device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 lanes x 16 consecutive 32-bit TMEM columns from registers (thread i -> lane base + i)
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t v[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 // mbar_wait that adds the cycles spent waiting to *acc (debug trace only)
 __device__ __forceinline__ void fa_wait(uint64_t *bar, uint32_t ph, unsigned long long *acc) {
   if (acc) {
@@ -137,10 +161,9 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t *sQ = smem;                                   // [2][32 KB]
-  uint8_t *sK = sQ + FA_QST * FA_Q_BYTES;               // [3][16 KB]
-  uint8_t *sV = sK + FA_KST * FA_KV_BYTES;              // [2][16 KB]
-  uint8_t *sP = sV + FA_VST * FA_KV_BYTES;              // [2][16 KB]
-  float2 *xch = reinterpret_cast<float2 *>(sP + FA_PST * FA_P_BYTES);  // [2 halves][128 rows]
+  uint8_t *sK = sQ + FA_QST * FA_Q_BYTES;               // [2][32 KB]
+  uint8_t *sV = sK + FA_KST * FA_KV_BYTES;              // [2][32 KB]
+  float2 *xch = reinterpret_cast<float2 *>(sV + FA_VST * FA_KV_BYTES);  // [2 halves][128 rows]
   uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(xch) + FA_XCH);
   uint64_t *q_full = bars, *q_empty = bars + 2;
   uint64_t *k_full = bars + 4, *k_empty = bars + 7;
@@ -179,7 +202,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       mbar_init(&p_full[i], 8);
       mbar_init(&p_empty[i], 1);
     }
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < FA_KST; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
     }
@@ -362,12 +385,11 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           if (j == 0) fa_wait(acc_empty, (ai & 1) ^ 1, TR(8));
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t pa = smem_u32(sP + pb * FA_P_BYTES);
             const uint32_t vb = smem_u32(sV + vs * FA_KV_BYTES);
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              umma_bf16(tmem + FA_ACC_COL, sw128_kmajor_desc(pa + kk * 32), sw128_mn_desc(vb + kk * 2048, FA_KV_BYTES / 2),
-                        id_pv, (j | kk) != 0);
+            for (int kk = 0; kk < 8; ++kk)  // 16 keys per MMA: 8 packed TMEM columns of P, 2 KB of V
+              umma_bf16_ts(tmem + FA_ACC_COL, tmem + FA_P_COL + pb * 64 + kk * 8,
+                           sw128_mn_desc(vb + kk * 2048, FA_KV_BYTES / 2), id_pv, (j | kk) != 0);
             umma_commit(&v_empty[vs]);
             umma_commit(&p_empty[pb]);
             if (j == n2 - 1) umma_commit(acc_full);
@@ -414,20 +436,21 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           continue;
         }
         tc_fence_after();
-        float v[32];
-        tmem_ld32(trow + sb * FA_BK + hh * 32, v);
+        float v[64];
+        tmem_ld32(trow + sb * FA_BK + hh * 64, v);
+        tmem_ld32(trow + sb * FA_BK + hh * 64 + 32, v + 32);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[sb]);
-        const int k0 = kt * FA_BK + hh * 32;
-        if (k0 + 32 > p.N) {  // ragged last tile: mask keys >= N
+        const int k0 = kt * FA_BK + hh * 64;
+        if (k0 + 64 > p.N) {  // ragged last tile: mask keys >= N
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
+          for (int j = 0; j < 64; ++j)
             if (k0 + j >= p.N) v[j] = -INFINITY;
         }
         float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
+        for (int j = 0; j < 64; j += 4) {
           mx0 = fmaxf(mx0, v[j]);
           mx1 = fmaxf(mx1, v[j + 1]);
           mx2 = fmaxf(mx2, v[j + 2]);
@@ -439,7 +462,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         const float mnc = mn * c;
         float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
+        for (int j = 0; j < 64; j += 4) {
           a0 += ex2f(fmaf(v[j], c, -mnc));
           a1 += ex2f(fmaf(v[j + 1], c, -mnc));
           a2 += ex2f(fmaf(v[j + 2], c, -mnc));
@@ -459,7 +482,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
                          (h1.x == -INFINITY ? 0.f : h1.y * ex2f((h1.x - M) * c));
       const float Mc = M * c;
       const float inv_l = 1.f / Lsum;
-      // ---- pass P: P = exp2(s - m) into swizzled shared memory for P V
+      // ---- pass P: P = exp2(s - m) into tensor memory for the P V MMA
       const unsigned long long tP = tron ? clock64() : 0;
       float acc[64];
       if (it.passP) {
@@ -478,32 +501,32 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             if (lane == 0) mbar_arrive(&p_full[pb]);
             continue;
           }
+          // P = exp2(s - m) for this half's 64 keys, bf16x2-packed into the P TMEM buffer (32
+          // columns per half); the S buffer is released once both chunks are read
+          fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1, TR(11));
           tc_fence_after();
-          float v[32];
-          tmem_ld32(trow + sb * FA_BK + hh * 32, v);
+#pragma unroll
+          for (int ch = 0; ch < 2; ++ch) {
+            float v[32];
+            tmem_ld32(trow + sb * FA_BK + hh * 64 + ch * 32, v);
+            const int k0 = j * FA_BK + hh * 64 + ch * 32;
+            uint32_t pk[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+              const float e1 = (t & 1) ? ex2p(fmaf(v[2 * t + 1], c, -Mc)) : ex2f(fmaf(v[2 * t + 1], c, -Mc));
+              const float p0 = (k0 + 2 * t < it.nkP) ? ex2f(fmaf(v[2 * t], c, -Mc)) : 0.f;
+              const float p1 = (k0 + 2 * t + 1 < it.nkP) ? e1 : 0.f;
+              pk[t] = pack2(p0, p1);
+            }
+            tmem_st16(trow + FA_P_COL + pb * 64 + hh * 32 + ch * 16, pk);
+          }
+          tmem_st_wait();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&s_empty[sb]);
-          const int k0 = j * FA_BK + hh * 32;
-          uint32_t pk[16];
-#pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            const float e1 = (t & 1) ? ex2p(fmaf(v[2 * t + 1], c, -Mc)) : ex2f(fmaf(v[2 * t + 1], c, -Mc));
-            const float p0 = (k0 + 2 * t < it.nkP) ? ex2f(fmaf(v[2 * t], c, -Mc)) : 0.f;
-            const float p1 = (k0 + 2 * t + 1 < it.nkP) ? e1 : 0.f;
-            pk[t] = pack2(p0, p1);
+          if (lane == 0) {
+            mbar_arrive(&s_empty[sb]);
+            mbar_arrive(&p_full[pb]);
           }
-          fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1, TR(11));
-          uint8_t *prow = sP + pb * FA_P_BYTES + r * 128;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int unit = (hh * 4 + u) ^ (r & 7);
-            *reinterpret_cast<uint4 *>(prow + unit * 16) =
-                make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-          }
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&p_full[pb]);
         }
         fa_wait(acc_full, ai & 1, TR(12));
         ++ai;
