@@ -38,6 +38,8 @@ TENSOR_CODES = {
     "wq": 1, "wk": 2, "wv": 3, "bq": 4, "bk": 5, "bv": 6, "wo": 7,
     "w_gate": 8, "w_up": 9, "w_down": 10, "g_attn": 11, "g_ffn": 12,
     "emb": 20, "g_final": 21, "lm_head": 22, "tokens": 30,
+    # synthetic cache/activation contents for teacher-forced parity at full size
+    "cK": 40, "cV": 41, "cQ": 42, "cC": 43, "cH": 44, "cX": 45, "cX2": 46,
 }
 GLOBAL_LAYER = 65535
 
@@ -151,3 +153,13 @@ def model_weights(cfg, seed: int, dtype=np.float64) -> dict:
     g = global_weights(cfg, seed, dtype)
     g["layers"] = [layer_weights(cfg, seed, l, dtype) for l in range(cfg.n_layers)]
     return g
+
+
+def cache_tensor(seed: int, layer: int, name: str, batch: int, N: int, width: int, std: float,
+                 dtype=np.float32) -> np.ndarray:
+    """Synthetic [batch][N][width] cache/activation contents (IH4, one stream per sequence), for
+    teacher-forced parity at full size: the oracle and the GPU receive the same bf16 values."""
+    out = np.empty((batch, N, width), dtype=dtype)
+    for b in range(batch):
+        out[b] = ih4_normal(seed, stream_id(layer, name) + ((b + 1) << 32), (N, width), std, dtype)
+    return out

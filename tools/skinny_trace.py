@@ -17,7 +17,9 @@ from paper_2603_08026_b200 import dyllm as dy  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--which", default="o")
 ap.add_argument("--rows", type=int, default=410)
+ap.add_argument("--split", type=int, default=0, help="units per weight block (0 = auto)")
 a = ap.parse_args()
+dy.set_option(dy.OPT_SKINNY_SPLIT, a.split)
 shapes = {"qkv": (12288, 4096), "o": (4096, 4096), "gu": (24576, 4096), "down": (4096, 12288)}
 N, K = shapes[a.which]
 ctx = dy.Context(0)
@@ -40,7 +42,7 @@ t0 = t[:, 0].min()
 rel = np.where(t > 0, (t - t0) / 1e3, np.nan)
 names = ["start", "prod_done", "mma_done", "tfull0", "tfull1", "tfull2", "tfull3", "published", "wait0", "wait1",
          "epi_done", "end"]
-print(f"{a.which} M={a.rows}: CTAs traced {valid.sum()}")
+print(f"{a.which} M={a.rows} S={a.split}: CTAs traced {valid.sum()}")
 for i, n in enumerate(names):
     col = rel[:, i]
     if np.all(np.isnan(col)):
