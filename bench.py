@@ -382,6 +382,14 @@ def main():
         totals = {k: float(v.sum()) for k, v in kc.items() if len(v)}
         tot_all = sum(totals.values())
         per_class = {}
+
+        def lm_cost(steps, n):
+            """LM-head bytes / flops per launch: b x (masked rows of the active block at step t)."""
+            cand = b * (run.block - (steps * run.n_u) % run.block)
+            cand = np.tile(cand, nsteps)[:n].astype(np.float64)
+            by, fl = algo_cost("lm_gemm", cfg, run, cand, 0, 0)
+            return np.broadcast_to(by, (n,)).astype(np.float64), np.broadcast_to(fl, (n,)).astype(np.float64)
+
         for k, v in kc.items():
             if not len(v):
                 continue
@@ -391,14 +399,14 @@ def main():
                 Mi = Mo = float(b * N)
                 Lt = np.full(len(v), float(b * N))
                 by, fl = algo_cost(base, cfg, run, Mi, Mo, b * N)
-                if base == "lm_gemm":
-                    by, fl = algo_cost(base, cfg, run, b * run.n_u * run.block, 0, 0)
                 if by is None:
                     continue
                 bys, fls = np.full(len(v), by), np.full(len(v), fl)
-            elif base == "lm_gemm":
-                by, fl = algo_cost(base, cfg, run, float(b * run.block), 0, 0)
-                bys, fls = np.full(len(v), by), np.full(len(v), fl)
+                if base == "lm_gemm":   # logits only for the masked rows of the active block (D13)
+                    bys, fls = lm_cost(np.arange(run.T_full), len(v))
+            elif base == "lm_gemm":   # one launch per denoising step (FullSteps included)
+                steps = np.arange(T) if len(v) >= T * nsteps else np.array(sparse_t)
+                bys, fls = lm_cost(steps, len(v))
             else:
                 Mi, Mo = m_in.ravel(), m_out.ravel()
                 Lt = np.repeat(L_in, cfg.n_layers)

@@ -368,11 +368,14 @@ int gemm_launch(const GemmCall &g, int num_sms, cudaStream_t st) {
     set_error("gemm swiglu: N must be a multiple of 256");
     return DYLLM_E_SHAPE;
   }
-  // Small row counts (<= 512) go to the 2-CTA weight-stationary kernel. With a device-resident
+  // Row counts <= kSkinnyMaxM (16384) go to the 2-CTA weight-stationary kernel. With a device-resident
   // count both kernels are enqueued and each exits unless the count is in its regime.
   GemmCall s = g;
   if (g_skinny_enabled && skinny_eligible(g)) {
-    if (!g.M_ptr && g.M_cap <= kSkinnyMaxM) return gemm_skinny_launch(g, num_sms, st);
+    // host-known large M with a wide N (FullStep gate/up, QKV): the single-CTA 128x256 kernel
+    // measures ~10% faster there (profiles/r1c_gemm_split_sweep.txt); everything else -> skinny
+    const bool wide_full = !g.M_ptr && g.M_cap > 4096 && g.N >= 12288;
+    if (!g.M_ptr && g.M_cap <= kSkinnyMaxM && !wide_full) return gemm_skinny_launch(g, num_sms, st);
     if (g.M_ptr) {
       int rc = gemm_skinny_launch(g, num_sms, st);
       if (rc) return rc;

@@ -1,21 +1,30 @@
-// gemm_skinny.cu — weight-stationary 2-CTA (cta_group::2) tcgen05 GEMM for the small salient row
-// counts of the sparse steps (M <= 512 rows, the weight-streaming
-// regime of §8d.3).
+// gemm_skinny.cu — weight-stationary 2-CTA (cta_group::2) tcgen05 GEMM for the salient row
+// counts of the sparse steps and the FullStep (M <= 16384 rows; the
+// weight-streaming regime of §8d.3 and the tensor-bound range).
 //
 //   D[m][n] = sum_k A[m][k] * W[n][k]     computed as D^T = W A^T:
 //   MMA-M = 256 weight rows of a CTA pair (128 per CTA, its own TMEM lanes),
-//   MMA-N = the activation rows (N <= 256 per instruction; two instructions cover M <= 512, each
-//           CTA of the pair holding half of them, so every activation byte enters one SM per pair).
-// Each weight byte is read by exactly one SM; the accumulator (128 lanes x M columns, <= 512)
-// stays in TMEM for the whole K range of a segment. Work is split stream-K style: the
-// (weight block, k-block) space is cut into equal contiguous ranges, one per co-resident SM pair,
-// so all 148 SMs stream weights even when N/256 is small (O-proj and FFN-down: 16 blocks).
+//   MMA-N = activation rows (N <= 256 per instruction; each CTA of the pair holds half of them,
+//           so every activation byte enters one SM per pair).
+// A tile is (256-row weight block, activation chunk): M <= 512 -> one chunk of all rows (two
+// instructions per k-step above 256 rows, accumulator of M <= 512 TMEM columns); M > 512 ->
+// ceil(M/256) equal chunks of <= 256 rows with a double-buffered accumulator. Per SM and k-block
+// the pair moves 16 KB of weights + R/2 x 128 B of activations for 128 x R x 64 MACs, which is
+// 1.5-2x the arithmetic per byte of a 128 x 256 single-CTA tile: what bounds these GEMMs on
+// B200 is the L2 -> SM operand traffic (tools/tma_probe.cu, profiles/r1c_gemm_split_sweep.txt).
+// Work is split stream-K style: the (tile, k-block) space is cut into equal contiguous ranges,
+// one per co-resident SM pair, so all 148 SMs stream weights even when tiles are few (O-proj and
+// FFN-down at M <= 512: 16 tiles).
 // A block whose K range spans several pairs is reduced through an fp32 workspace in a fixed
-// contributor order (bit-deterministic), each contributor finishing a share of the rows. Roles per CTA (192 threads): warp 0 TMA producer (both
-// CTAs load their halves; the leader's full barrier counts the bytes of both), warp 1 TMEM
-// allocator + (leader only) single-thread tcgen05.mma issuer with multicast commits, warps 2-5
-// epilogue from the CTA's own TMEM lanes (bias / residual / SiLU-gate), transposed store.
-// The kernel exits immediately when the device-side row count is 0 or > 512 (the standard
+// contributor order (bit-deterministic), each contributor finishing a share of the rows; the
+// partials are written and read straight from registers in TMEM-native layout (one 128-byte line
+// per thread and 32-row chunk). Roles per CTA (352 threads): warps 0 (weights) and 10
+// (activations) TMA producers (both CTAs load their halves; the leader's full barrier counts the
+// bytes of both), warp 1 TMEM allocator +
+// (leader only) single-thread tcgen05.mma issuer with multicast commits, warps 2-9 epilogue from
+// the CTA's own TMEM lanes in two halves of four warps taking alternate 32-column chunks (bias /
+// residual / SiLU-gate), transposed through shared memory for coalesced stores.
+// The kernel exits immediately when the device-side row count is 0 or > 16384 (the standard
 // kernel of gemm.cu covers that regime), so both kernels can be enqueued without a host sync.
 #include <cudaTypedefs.h>
 
@@ -28,13 +37,13 @@ constexpr int SK_STAGES = 4;
 constexpr int SK_W_BYTES = 128 * 128;        // 128 weight rows x 64 bf16
 constexpr int SK_A_BYTES = 128 * 128;        // 128 activation rows x 64 bf16 (per MMA half)
 constexpr int SK_STAGE = SK_W_BYTES + 2 * SK_A_BYTES;
-constexpr int SK_XCH = 2 * 32 * 128 * 4;     // epilogue transpose tiles: 2 x [32 rows][128 weight rows] fp32
-constexpr int kSkRing = SK_STAGES * SK_STAGE / (32 * 128 * 4);  // reduction ring buffers in the stage area
-constexpr int SK_SMEM = 1024 + SK_STAGES * SK_STAGE + SK_XCH + 256;
-static_assert(12 * 8 + kSkRing * 8 + 4 <= 256, "barrier area");
+constexpr int SK_XCH = 2 * 32 * 128 * 4;     // epilogue transpose tiles: one [32 rows][128 weight rows] fp32 per half
+constexpr int SK_RING = SK_STAGES * SK_STAGE;  // 192 KB: 4 stages of 48 KB (M in (256, 512]) or 6 of 32 KB
+constexpr int SK_MAX_STAGES = SK_RING / (SK_W_BYTES + SK_A_BYTES);
+constexpr int SK_SMEM = 1024 + SK_RING + SK_XCH + 256;
+constexpr int SK_THREADS = 352;              // W producer, MMA, 8 epilogue warps, A producer
 constexpr int SKINNY_MAX_M = kSkinnyMaxM;
 constexpr int kSkPrefetch = 12;   // k-blocks of weight L2 prefetch ahead of the ring
-constexpr int kSkMaxContrib = 12;  // <= kSkRing: all partial tiles of one chunk fit in the ring  // split-K contributors per weight block (host-checked)
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
@@ -85,29 +94,6 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t *bar) {
           smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-template <int N>
-__device__ __forceinline__ void bulk_wait() {
-  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void bulk_load(void *sdst, const void *gsrc, uint32_t bytes, uint64_t *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(sdst)),
-               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -123,9 +109,9 @@ struct SkinnyParams {
   const bf16 *bias;
   float *ws;   // split-K partials: [2*P slots][512 m][256 weight rows] fp32
   int *ctr;    // per (item, rank) arrival counters, zero between launches
-  int P;       // pairs taking part in the stream-K partition
+  int P_max;   // co-resident pairs of the grid (the partition uses P <= P_max of them)
   unsigned long long *trace;  // optional [grid][16] globaltimer stamps (debug hook)
-  int kpu;     // k-blocks per stream-K unit (K/64 / units per weight block)
+  int S_force; // test hook: split units per tile (0 = automatic)
 };
 
 // Stream-K partition of the (item, k-block) space: pair p owns units [start(p), start(p+1)).
@@ -152,10 +138,18 @@ struct SkSeg {
   int item, kb0, kb1;
 };
 struct SkIter {
-  int64_t u, end;  // unit range [u, end) of the pair
-  int upi, kpu;    // units per weight block, k-blocks per unit
+  int64_t u, end;  // unit range [u, end) of the pair (strided: tile u, u + step, ... < end)
+  int upi, kpu;    // units per tile, k-blocks per unit
+  int64_t step;    // 0: contiguous stream-K range; > 0: whole tiles u, u + step, ...
   __device__ bool next(SkSeg &s) {
     if (u >= end) return false;
+    if (step) {
+      s.item = static_cast<int>(u);
+      s.kb0 = 0;
+      s.kb1 = upi * kpu;
+      u += step;
+      return true;
+    }
     s.item = static_cast<int>(u / upi);
     const int u0 = static_cast<int>(u - static_cast<int64_t>(s.item) * upi);
     const int64_t left = end - u;
@@ -168,7 +162,7 @@ struct SkIter {
 };
 
 template <int EPI>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(SK_THREADS, 1)
     gemm_skinny_kernel(const __grid_constant__ CUtensorMap tmA128, const __grid_constant__ CUtensorMap tmA64,
                        const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CUtensorMap tmA16,
                        const __grid_constant__ CUtensorMap tmW, const SkinnyParams p) {
@@ -179,26 +173,46 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t *stages = smem;
   float *xs = reinterpret_cast<float *>(smem + SK_STAGES * SK_STAGE);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + SK_STAGES * SK_STAGE + SK_XCH);
-  uint64_t *empty = full + SK_STAGES;
-  uint64_t *tfull = empty + SK_STAGES;   // [2]
+  uint64_t *empty = full + SK_MAX_STAGES;
+  uint64_t *tfull = empty + SK_MAX_STAGES;   // [2]
   uint64_t *tempty = tfull + 2;          // [2]
-  uint64_t *rbar = tempty + 2;           // [kSkRing] split-K reduction ring
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rbar + kSkRing);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1;
-  const int items = p.N / 256;
+  // Tiles ("items") = (256-row weight block, activation chunk). M <= 512: one chunk holding all
+  // rows (two MMAs per k-step when M > 256, single-buffered accumulator); M > 512: ceil(M/256)
+  // equal chunks of R <= 256 rows (double-buffered accumulator). Chunks of one weight block are
+  // adjacent in tile order, so the pairs working on them at the same time share it through L2.
+  const int nchunk = M <= 512 ? 1 : (M + 255) / 256;
+  const int R = nchunk == 1 ? M : (((M + nchunk - 1) / nchunk + 31) & ~31);
+  const int items = p.N / 256 * nchunk;
   const int num_kb = p.K / 64;
-  const int kpu = p.kpu, upi = num_kb / kpu;                 // split granularity (host-chosen)
+  // split granularity (stream-K units per tile), from the device-side M: tiles are cut into
+  // S units when there are fewer tiles than pairs (S = pairs / tiles), so all pairs stream
+  int upi = p.S_force > 0 ? p.S_force : max(1, p.P_max / items);
+  upi = min(upi, num_kb);
+  while (num_kb % upi) --upi;
+  const int kpu = num_kb / upi;
   const int64_t Wt = static_cast<int64_t>(items) * upi;      // units of the stream-K partition
+  const int P = static_cast<int>(min(static_cast<int64_t>(p.P_max), Wt));
   // activation rows per MMA, rounded to 32 so that each CTA's half is a multiple of 16 rows
-  const int NA0 = (min(M, 256) + 31) & ~31;
-  const int NA1 = M > 256 ? ((M - 256 + 31) & ~31) : 0;
+  const int NA0 = nchunk == 1 ? ((min(M, 256) + 31) & ~31) : R;
+  const int NA1 = (nchunk == 1 && M > 256) ? ((M - 256 + 31) & ~31) : 0;
   // M <= 256: two 256-column TMEM accumulators (epilogue of segment i overlaps the MMAs of i+1)
   const int nbuf = NA1 ? 1 : 2;
   const uint32_t stage_tx = 2u * (SK_W_BYTES + (NA0 / 2 + NA1 / 2) * 128);
-  SkIter iter0{sk_start(pair, Wt, p.P), sk_start(pair + 1, Wt, p.P), upi, kpu};
+  // ring: a stage holds 16 KB of weights + one (or, for M in (256, 512], two) 16 KB activation
+  // slots; with one slot the same 192 KB hold 6 stages instead of 4
+  const int stage_bytes = NA1 ? SK_STAGE : SK_W_BYTES + SK_A_BYTES;
+  const int nstages = SK_RING / stage_bytes;
+  // Unsplit tiles (upi == 1) are dealt round-robin (pair p: tiles p, p + P, ...), so the pairs
+  // running at the same time hold consecutive tiles (the activation chunks of one weight block:
+  // its HBM read is shared through L2); split tiles use contiguous stream-K ranges.
+  SkIter iter0 = upi == 1 ? SkIter{pair < P ? pair : 0, pair < P ? Wt : 0, upi, kpu, P}
+                          : SkIter{pair < P ? sk_start(pair, Wt, P) : 0, pair < P ? sk_start(pair + 1, Wt, P) : 0,
+                                   upi, kpu, 0};
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA128);
@@ -206,15 +220,14 @@ __global__ void __launch_bounds__(192, 1)
     tma_prefetch_desc(&tmA32);
     tma_prefetch_desc(&tmA16);
     tma_prefetch_desc(&tmW);
-    for (int s = 0; s < SK_STAGES; ++s) {
+    for (int s = 0; s < SK_MAX_STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 2 * 128);
+      mbar_init(&tempty[s], 2 * 8);  // one arrival per epilogue warp of both CTAs
     }
-    for (int s = 0; s < kSkRing; ++s) mbar_init(&rbar[s], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
@@ -224,55 +237,72 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) sk_stamp(p, 0);
 
-  if (warp == 0) {
-    // ===================== TMA producer (both CTAs)
+  if (warp == 0 || warp == 10) {
+    // ===================== TMA producers (both CTAs): warp 0 streams the weight tiles (and the
+    // L2 prefetch stream), warp 10 the activation boxes — two issuing threads, since one thread's
+    // TMA issue rate (a few small ops per microsecond, tools/tma_probe.cu) would otherwise pace
+    // the ring
+    const bool wprod = warp == 0;
     if (lane == 0) {
       int st = 0;
       uint32_t ph = 0;
       SkIter it = iter0;
       SkSeg sg;
-      // weight tiles are read once, from DRAM: an L2 prefetch stream runs kSkPrefetch k-blocks
-      // ahead of the shared-memory ring so the ring's TMA loads hit L2
-      int64_t pf = it.u * kpu;             // k-block space: item * num_kb + kb
-      const int64_t pf_end = it.end * kpu;
-      auto prefetch_to = [&](int64_t upto) {
-        for (; pf < upto && pf < pf_end; ++pf) {
-          const int item = static_cast<int>(pf / num_kb);
-          const int kb = static_cast<int>(pf - static_cast<int64_t>(item) * num_kb);
-          tma_prefetch_l2_2d(&tmW, kb * 64, item * 256 + static_cast<int>(rank) * 128);
+      // weight tiles are read once, from DRAM: an L2 prefetch cursor runs kSkPrefetch k-blocks
+      // ahead of the shared-memory ring over the same segment sequence, so the ring's TMA loads
+      // hit L2 (only the first activation chunk's pair prefetches a weight block)
+      SkIter pit = it;
+      SkSeg ps{0, 0, 0};
+      int pkb = 0;
+      int64_t n_pf = 0, n_ld = 0;
+      auto prefetch_ahead = [&]() {
+        while (n_pf < n_ld + kSkPrefetch) {
+          if (pkb >= ps.kb1) {
+            if (!pit.next(ps)) return;
+            pkb = ps.kb0;
+          }
+          if (ps.item % nchunk == 0)
+            tma_prefetch_l2_2d(&tmW, pkb * 64, ps.item / nchunk * 256 + static_cast<int>(rank) * 128);
+          ++pkb;
+          ++n_pf;
         }
       };
-      prefetch_to(it.u + kSkPrefetch);
+      if (wprod) prefetch_ahead();
       while (it.next(sg)) {
-        const int wrow = sg.item * 256 + static_cast<int>(rank) * 128;
+        const int wrow = sg.item / nchunk * 256 + static_cast<int>(rank) * 128;
+        const int arow = sg.item % nchunk * R;  // first activation row of the tile
         for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
-          prefetch_to(static_cast<int64_t>(sg.item) * num_kb + kb + 1 + kSkPrefetch);
           mbar_wait(&empty[st], ph ^ 1);
-          if (rank == 0) mbar_expect_tx(&full[st], stage_tx);
-          uint8_t *sb = stages + st * SK_STAGE;
-          tma_load_2d_pair(sb, &tmW, &full[st], kb * 64, wrow);
-          // this CTA's half of each activation block, in boxes of 128/64/32/16 rows (only the
-          // rows the MMA reads; 16-row offsets keep the 128B-swizzle atoms aligned)
-          auto load_rows = [&](uint8_t *dst, int r0, int n) {
-            const CUtensorMap *maps[4] = {&tmA128, &tmA64, &tmA32, &tmA16};
-            int off = 0;
-            for (int bi = 0; bi < 4; ++bi) {
-              const int box = 128 >> bi;
-              while (n - off >= box) {
-                tma_load_2d_pair(dst + off * 128, maps[bi], &full[st], kb * 64, r0 + off);
-                off += box;
+          uint8_t *sb = stages + st * stage_bytes;
+          if (wprod) {
+            if (rank == 0) mbar_expect_tx(&full[st], stage_tx);
+            tma_load_2d_pair(sb, &tmW, &full[st], kb * 64, wrow);
+            ++n_ld;
+            prefetch_ahead();
+          } else {
+            // this CTA's half of each activation block, in boxes of 128/64/32/16 rows (only the
+            // rows the MMA reads; 16-row offsets keep the 128B-swizzle atoms aligned)
+            auto load_rows = [&](uint8_t *dst, int r0, int n) {
+              const CUtensorMap *maps[4] = {&tmA128, &tmA64, &tmA32, &tmA16};
+              int off = 0;
+              for (int bi = 0; bi < 4; ++bi) {
+                const int box = 128 >> bi;
+                while (n - off >= box) {
+                  tma_load_2d_pair(dst + off * 128, maps[bi], &full[st], kb * 64, r0 + off);
+                  off += box;
+                }
               }
-            }
-          };
-          load_rows(sb + SK_W_BYTES, static_cast<int>(rank) * (NA0 / 2), NA0 / 2);
-          if (NA1) load_rows(sb + SK_W_BYTES + SK_A_BYTES, 256 + static_cast<int>(rank) * (NA1 / 2), NA1 / 2);
-          if (++st == SK_STAGES) {
+            };
+            load_rows(sb + SK_W_BYTES, arow + static_cast<int>(rank) * (NA0 / 2), NA0 / 2);
+            if (NA1) load_rows(sb + SK_W_BYTES + SK_A_BYTES, 256 + static_cast<int>(rank) * (NA1 / 2), NA1 / 2);
+          }
+          if (++st == nstages) {
             st = 0;
             ph ^= 1;
           }
         }
       }
-      sk_stamp(p, 1);
+      if (wprod) sk_stamp(p, 1);
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA only)
@@ -294,7 +324,7 @@ __global__ void __launch_bounds__(192, 1)
           mbar_wait(&full[st], ph);
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t w0 = smem_u32(stages + st * SK_STAGE);
+            const uint32_t w0 = smem_u32(stages + st * stage_bytes);
             const uint32_t a0 = w0 + SK_W_BYTES;
             const uint32_t first = (kb == sg.kb0) ? 1u : 0u;
 #pragma unroll
@@ -309,7 +339,7 @@ __global__ void __launch_bounds__(192, 1)
             if (kb == sg.kb1 - 1) umma_commit_pair(&tfull[b]);
           }
           __syncwarp();
-          if (++st == SK_STAGES) {
+          if (++st == nstages) {
             st = 0;
             ph ^= 1;
           }
@@ -319,23 +349,30 @@ __global__ void __launch_bounds__(192, 1)
       if (lane == 0) sk_stamp(p, 2);
     }
   } else {
-    // ===================== epilogue warps 2..5 (both CTAs, own TMEM lanes)
+    // ===================== epilogue warps 2..9 (both CTAs, own TMEM lanes): two halves of four
+    // warps (one per TMEM lane quadrant) take alternate 32-column chunks, so two chunks are in
+    // flight per CTA; each warp prefetches its next chunk's TMEM load before storing the current.
     const int quad = warp & 3;
-    const int row = quad * 32 + lane;  // weight row within this CTA's 128
-    const int et = threadIdx.x - 64;   // 0..127
+    const int half = (warp - 2) >> 2;
+    const int row = quad * 32 + lane;        // weight row within this CTA's 128 (= TMEM lane)
+    const int et = threadIdx.x - 64;         // 0..255
+    const int t = et & 127;                  // thread within the half
+    float *x = xs + half * (32 * 128);       // this half's transpose tile [32 m][128 n] fp32
     const uint32_t leader_tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
     const uint32_t leader_tempty1 = mapa_shared(smem_u32(&tempty[1]), 0);
-    // Final epilogue of 32 output rows [m0, m0+32) x this CTA's 128 weight rows, read from a
+    // Final epilogue of 32 output rows [m0, m0+32) x this CTA's 128 weight rows, from a
     // [32 m][128 n] fp32 tile in shared memory. Threads are laid out along the weight (= output
     // column) dimension so that the 8-byte bf16 stores (and residual loads) are coalesced.
     // Register slot i holds the float4 at (row m0 + sl_m(i), weight rows sl_n(i)..+3): SwiGLU
     // slots 0-3 gate, 4-7 up (weight rows [0,64) gate, [64,128) up of the same 64 FFN channels).
     constexpr bool kSw = EPI == EPI_SWIGLU;
-    const int n4 = kSw ? (et & 15) : (et & 31);
-    const int msub = kSw ? (et >> 4) : (et >> 5);
+    const int n4 = kSw ? (t & 15) : (t & 31);
+    const int msub = kSw ? (t >> 4) : (t >> 5);
     auto sl_m = [&](int i) { return kSw ? msub + 8 * (i & 3) : msub + 4 * i; };
     auto sl_n = [&](int i) { return kSw ? (i < 4 ? 4 * n4 : 64 + 4 * n4) : 4 * n4; };
-    auto store = [&](const float4 r[8], int m0, int item) {
+    auto store = [&](const float4 r[8], int m0, int tile) {
+      const int item = tile / nchunk;  // weight block (output columns)
+      m0 += tile % nchunk * R;         // output rows of the tile's activation chunk
       if constexpr (kSw) {
         const int ch = (item * 2 + static_cast<int>(rank)) * 64 + 4 * n4;
 #pragma unroll
@@ -376,22 +413,39 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     };
-    // workspace: slot-major, then rank, then [512 m][128 n] fp32, so one 32-row chunk of one
-    // CTA's partial is a contiguous 16 KB block (one bulk copy each way)
-    auto ws_chunk = [&](int slot, int c) -> float * {
-      return p.ws + ((static_cast<int64_t>(slot) * 2 + rank) * 512 + c * 32) * 128;
+    // transpose one chunk (thread = weight row `row`, v = its 32 output rows m0..m0+31) through
+    // this half's tile and store it. The leading barrier also orders the previous chunk's tile
+    // reads before this chunk's writes.
+    auto transpose_store = [&](const float v[32], int m0, int item) {
+      named_bar_sync(1 + half, 128);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[j * 128 + row] = v[j];
+      named_bar_sync(1 + half, 128);
+      const float4 *x4 = reinterpret_cast<const float4 *>(x);
+      float4 r[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) r[i] = x4[sl_m(i) * 32 + sl_n(i) / 4];
+      store(r, m0, item);
+    };
+    // split-K partials, TMEM-native layout: slot-major, then rank, then [16 chunks][8][128 n]
+    // float4 (element j of a thread's 32 values at [j / 4][n]), so every warp store / load of one
+    // float4 per thread is a contiguous 512-byte line
+    auto ws_line = [&](int slot, int c) -> float4 * {
+      return reinterpret_cast<float4 *>(p.ws) + (((static_cast<int64_t>(slot) * 2 + rank) * 16 + c) * 8) * 128 + row;
     };
     // slot of (pair pp, item): side 0 if the pair's range starts inside the item (its first
     // segment), side 1 otherwise (its last segment)
     auto slot_of = [&](int pp, int item) -> int {
-      return pp * 2 + (sk_start(pp, Wt, p.P) >= static_cast<int64_t>(item) * upi ? 0 : 1);
+      return pp * 2 + (sk_start(pp, Wt, P) >= static_cast<int64_t>(item) * upi ? 0 : 1);
     };
     int deferred[2];
     int ndef = 0;
     int local = 0;
-    int xb = 0;  // transpose tile double buffer index
     SkIter it = iter0;
     SkSeg sg;
+    const int NAt = NA0 + NA1;
+    const int nch = NAt / 32;
+    auto tcol = [&](int c) { return c * 32 < NA0 ? c * 32 : 256 + (c * 32 - NA0); };  // TMEM column = output row
     while (it.next(sg)) {
       const int b = nbuf == 2 ? (local & 1) : 0;
       const uint32_t tph = nbuf == 2 ? ((local >> 1) & 1) : (local & 1);
@@ -401,114 +455,104 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + b * 256;
       const bool whole = sg.kb0 == 0 && sg.kb1 == num_kb;  // the segment spans the whole K range
       const int slot = whole ? 0 : slot_of(pair, sg.item);
-      const int NAt = NA0 + NA1;
-      for (int c0 = 0; c0 < NAt; c0 += 32) {
-        // TMEM columns: [0, NA0) hold rows 0.., [256, 256+NA1) hold rows 256..
-        const int m0 = c0 < NA0 ? c0 : 256 + (c0 - NA0);
-        float *x = xs + xb * (32 * 128);
-        float v[32];
-        tmem_ld32(tb + (c0 < NA0 ? c0 : 256 + (c0 - NA0)), v);
-        if (c0 + 32 >= NAt) {  // accumulator fully read: hand TMEM back to the MMA warp
+      uint32_t ra[32], rb[32];  // current chunk / next chunk (its TMEM load in flight meanwhile)
+      if (half < nch) {
+        tmem_ld32_issue(tb + tcol(half), ra);
+        tmem_ld32_wait(ra);
+      }
+      for (int c = half; c < nch; c += 2) {
+        const bool more = c + 2 < nch;
+        if (more) tmem_ld32_issue(tb + tcol(c + 2), rb);
+        if (!more) {  // this warp's last read of the accumulator: hand TMEM back to the MMA warp
           tc_fence_before();
-          mbar_arrive_cluster(b ? leader_tempty1 : leader_tempty0);
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(b ? leader_tempty1 : leader_tempty0);
         }
-        if (et == 0) bulk_wait_read<1>();  // a bulk store of 2 chunks ago has left x
-        named_bar_sync(1, 128);
+        float v[32];
 #pragma unroll
-        for (int t = 0; t < 32; ++t) x[t * 128 + row] = v[t];
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(ra[j]);
         if (whole) {
-          named_bar_sync(1, 128);
-          const float4 *x4 = reinterpret_cast<const float4 *>(x);
-          float4 r[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) r[i] = x4[sl_m(i) * 32 + sl_n(i) / 4];
-          store(r, m0, sg.item);
+          transpose_store(v, tcol(c), sg.item);
         } else {
-          // split-K partial: publish the 16 KB tile with one bulk store
-          fence_proxy_async();
-          named_bar_sync(1, 128);
-          if (et == 0) {
-            bulk_store(ws_chunk(slot, m0 / 32), x, 32 * 128 * 4);
-            bulk_commit();
-          }
+          float4 *dst = ws_line(slot, c);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) dst[j * 128] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         }
-        xb ^= 1;
+        if (more) {
+          tmem_ld32_wait(rb);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) ra[j] = rb[j];
+        }
+      }
+      if (half >= nch) {  // (nch == 1) the idle half still releases its share of the accumulator
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(b ? leader_tempty1 : leader_tempty0);
       }
       if (!whole) {
-        if (et == 0) {
-          bulk_wait<0>();   // partial is in global memory (L2)
-          fence_proxy_async_global();
-          __threadfence();
-          atomicAdd(p.ctr + sg.item * 2 + static_cast<int>(rank), 1);
-        }
+        __threadfence();
+        named_bar_sync(3, 256);
+        if (et == 0) atomicAdd(p.ctr + sg.item * 2 + static_cast<int>(rank), 1);
         if (ndef < 2) deferred[ndef++] = sg.item;
       }
       ++local;
     }
     if (et == 0) sk_stamp(p, 7);
     // Reductions of the split blocks (after every segment of this pair is published, so no pair
-    // waits while holding unpublished work). Contributor q of nc finishes 32-row chunks
-    // q, q+nc, ...: the nc partial tiles of a chunk are streamed into the idle stage ring with
-    // bulk copies (kRing buffers of 16 KB) and summed in fixed contributor order
-    // (bit-deterministic: the order does not depend on arrival order).
-    constexpr int kRing = SK_STAGES * SK_STAGE / (32 * 128 * 4);
-    float *ring = reinterpret_cast<float *>(stages);
-    int rseq = 0;  // ring buffer sequence number (buffer rseq % kRing, phase (rseq / kRing) & 1)
+    // waits while holding unpublished work). Contributor q of nc finishes chunks q, q+nc, ...
+    // (alternating between the two halves); each thread sums its 128-byte partial lines of the
+    // nc contributors in fixed contributor order (bit-deterministic: the order does not depend on
+    // arrival order), then transposes and stores like an unsplit tile.
     for (int di = 0; di < ndef; ++di) {
       const int item = deferred[di];
       const int64_t ib = static_cast<int64_t>(item) * upi;
-      const int p_first = sk_owner(ib, Wt, p.P);
-      const int nc = sk_owner(ib + upi - 1, Wt, p.P) - p_first + 1;
+      const int p_first = sk_owner(ib, Wt, P);
+      const int nc = sk_owner(ib + upi - 1, Wt, P) - p_first + 1;
       const int q = pair - p_first;
       int *ctr = p.ctr + item * 2 + static_cast<int>(rank);
       if (et == 0) {
         while (ld_acquire(ctr) < nc) {
         }
-        fence_proxy_async_global();  // generic acquire -> async-proxy (bulk copy) reads
       }
-      named_bar_sync(1, 128);
+      named_bar_sync(3, 256);
       if (et == 0 && di < 2) sk_stamp(p, 8 + di);
-      const int nchunks = (M + 31) / 32;
-      const int my = nchunks > q ? (nchunks - q + nc - 1) / nc : 0;  // my chunks
-      const int per = kRing / nc;                                      // chunks in flight
-      if (per == 0) __trap();                                          // host keeps nc <= kRing
-      // issue loads for chunk k of mine into ring sequence rseq + k*nc + qq
-      auto issue = [&](int k) {
+      const int my = nch > q ? (nch - q + nc - 1) / nc : 0;  // chunks this pair finishes
+      for (int k = half; k < my; k += 2) {
         const int c = q + k * nc;
-        for (int qq = 0; qq < nc; ++qq) {
-          const int sq = rseq + k * nc + qq;
-          uint64_t *bar = &rbar[sq % kRing];
-          mbar_expect_tx(bar, 32 * 128 * 4);
-          bulk_load(ring + (sq % kRing) * (32 * 128), ws_chunk(slot_of(p_first + qq, item), c), 32 * 128 * 4, bar);
-        }
-      };
-      if (et == 0) {
-        fence_proxy_async();
-        for (int k = 0; k < my && k < per; ++k) issue(k);
-      }
-      for (int k = 0; k < my; ++k) {
-        float4 r[8];
+        float4 acc[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) r[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int qq = 0; qq < nc; ++qq) {
-          const int sq = rseq + k * nc + qq;
-          mbar_wait(&rbar[sq % kRing], (sq / kRing) & 1);
-          const float4 *t4 = reinterpret_cast<const float4 *>(ring + (sq % kRing) * (32 * 128));
+        for (int j = 0; j < 8; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        // contributors in ascending order, loads of two of them in flight together
+        for (int q0 = 0; q0 < nc; q0 += 2) {
+          const int nq = nc - q0 < 2 ? nc - q0 : 2;
+          float4 tv[2][8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 t = t4[sl_m(i) * 32 + sl_n(i) / 4];
-            r[i].x += t.x; r[i].y += t.y; r[i].z += t.z; r[i].w += t.w;
+          for (int u = 0; u < 2; ++u) {
+            if (u < nq) {
+              const float4 *src = ws_line(slot_of(p_first + q0 + u, item), c);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) tv[u][j] = __ldcg(src + j * 128);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            if (u < nq) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                acc[j].x += tv[u][j].x; acc[j].y += tv[u][j].y; acc[j].z += tv[u][j].z; acc[j].w += tv[u][j].w;
+              }
+            }
           }
         }
-        named_bar_sync(1, 128);  // every thread is done with chunk k's buffers
-        if (et == 0 && k + per < my) {
-          fence_proxy_async();
-          issue(k + per);
+        float vr[32];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          vr[4 * j] = acc[j].x; vr[4 * j + 1] = acc[j].y; vr[4 * j + 2] = acc[j].z; vr[4 * j + 3] = acc[j].w;
         }
-        store(r, (q + k * nc) * 32, item);
+        transpose_store(vr, tcol(c), item);
       }
-      rseq += my * nc;
       // second arrival: the last contributor to pass re-arms the counter for the next launch
+      named_bar_sync(3, 256);
       if (et == 0 && atomicAdd(ctr, 1) == 2 * nc - 1) atomicExch(ctr, 0);
     }
   }
@@ -522,8 +566,6 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
-int skinny_auto_split(int items, int num_kb, int max_pairs);
-
 template <int EPI>
 static int launch_skinny_t(const GemmCall &g, int num_sms, cudaStream_t st) {
   auto kern = gemm_skinny_kernel<EPI>;
@@ -535,7 +577,7 @@ static int launch_skinny_t(const GemmCall &g, int num_sms, cudaStream_t st) {
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(192);
+  cfg.blockDim = dim3(SK_THREADS);
   cfg.dynamicSmemBytes = SK_SMEM;
   cfg.stream = st;
   cfg.attrs = attr;
@@ -554,8 +596,9 @@ static int launch_skinny_t(const GemmCall &g, int num_sms, cudaStream_t st) {
     }
     attr_done = true;
   }
-  if (!g.ws || !g.ctr || g.N / 256 * 2 > kSkinnyCtrCap) {
-    set_error("skinny gemm: missing split-K workspace or too many weight blocks");
+  // split-K counters are used only when tiles < pairs (2 per tile): at most 2 * max_pairs
+  if (!g.ws || !g.ctr || 2 * max_pairs > kSkinnyCtrCap) {
+    set_error("skinny gemm: missing split-K workspace or counters");
     return DYLLM_E_ARG;
   }
   CUtensorMap ta[4], tw;
@@ -565,46 +608,17 @@ static int launch_skinny_t(const GemmCall &g, int num_sms, cudaStream_t st) {
   }
   int rc = make_tmap(&tw, g.W, g.N, g.K, 128);
   if (rc) return rc;
-  const int items = g.N / 256, num_kb = g.K / 64;
-  // split granularity: units per weight block (S); each unit is num_kb / S k-blocks
-  int S = g_skinny_split > 0 ? g_skinny_split : skinny_auto_split(items, num_kb, max_pairs);
-  if (S > num_kb) S = num_kb;
-  while (num_kb % S) --S;
-  const int64_t units = static_cast<int64_t>(items) * S;
-  int pairs = max_pairs;
-  if (pairs > units) pairs = static_cast<int>(units);
-  // every weight block must have <= kSkMaxContrib contributors (its partial tiles share the ring)
-  auto max_contrib = [&](int P) {
-    int mx = 0;
-    for (int i = 0; i < items; ++i) {
-      const int64_t a = static_cast<int64_t>(i) * S, b = a + S - 1;
-      const int nc = static_cast<int>((b * P + P - 1) / units - (a * P + P - 1) / units) + 1;
-      mx = nc > mx ? nc : mx;
-    }
-    return mx;
-  };
-  while (pairs > 1 && max_contrib(pairs) > kSkMaxContrib) --pairs;
-  SkinnyParams p{g.M_ptr, g.M_cap, g.N, g.K, g.D, g.ldd, g.resid, g.ldr, g.resid_rows, g.bias, g.ws, g.ctr, pairs,
-                 g_skinny_trace, num_kb / S};
-  cfg.gridDim = dim3(2 * pairs);
+  // the tile count (hence the split and the number of pairs used) depends on the device-side row
+  // count: the kernel derives them; the grid is every co-resident pair
+  SkinnyParams p{g.M_ptr, g.M_cap, g.N, g.K, g.D, g.ldd, g.resid, g.ldr, g.resid_rows, g.bias, g.ws, g.ctr, max_pairs,
+                 g_skinny_trace, g_skinny_split};
+  cfg.gridDim = dim3(2 * max_pairs);
   DY_CUDA(cudaLaunchKernelEx(&cfg, kern, ta[0], ta[1], ta[2], ta[3], tw, p));
   return DYLLM_OK;
 }
 
 unsigned long long *g_skinny_trace = nullptr;
 int g_skinny_split = 0;
-
-// Default split: units per weight block. One unit per pair when there are fewer weight blocks
-// than SM pairs (S = pairs / blocks: O-proj and FFN-down, 16 blocks -> S = 4), otherwise no split:
-// the fp32 partial round trip through L2 costs more than the imbalance it removes. Measured at
-// the LLaDA-8B shapes for M in {100, 410} against S in {1, 2, 4, 8, K/64} (tools/gemm_bench.py
-// --split; profiles/).
-int skinny_auto_split(int items, int num_kb, int max_pairs) {
-  int S = max_pairs / items;
-  if (S < 1) S = 1;
-  if (S > num_kb) S = num_kb;
-  return S;
-}
 
 bool skinny_eligible(const GemmCall &g) {
   return g.N % 256 == 0 && g.K % 64 == 0 && (g.epi == EPI_BF16 || g.epi == EPI_RESID || g.epi == EPI_SWIGLU);

@@ -58,8 +58,8 @@ int make_tmap(CUtensorMap *m, const void *ptr, int rows, int K, int box_rows);
 int make_tmap3(CUtensorMap *m, const void *ptr, int rows, int K, int box_rows, int box_chunks);
 int gemm_lmhead_ntiles(int N);
 bool skinny_eligible(const GemmCall &g);
-constexpr int kSkinnyMaxM = 512;
-constexpr int kSkinnyCtrCap = 4096;  // 2 counters per 256-row weight block
+constexpr int kSkinnyMaxM = 16384;  // skinny kernel: device row counts 1..16384 (standard kernel above)
+constexpr int kSkinnyCtrCap = 4096;  // 2 counters per skinny tile (weight block x activation chunk)
 inline int64_t skinny_ws_floats(int num_sms) { return static_cast<int64_t>(num_sms) * 512 * 256; }
 extern bool g_skinny_enabled;  // test hook (dyllm_set_option)
 extern unsigned long long *g_skinny_trace;

@@ -423,6 +423,20 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
     for (int sq = warp; sq < batch; sq += kSelWarps) {
       const float *sv = sim_out + static_cast<int64_t>(sq) * N + row_lo;
       const int k = static_cast<int>(floorf(frac * L + 0.5f));
+      // the sequence's similarities, loaded once (all loads in flight together) into registers:
+      // element j of lane l is row j*32 + l (L <= 1024; longer inputs stream from L2 per pass)
+      constexpr int kRegRows = 32;
+      const bool in_regs = L <= 32 * kRegRows;
+      float sreg[kRegRows];
+#pragma unroll
+      for (int j = 0; j < kRegRows; ++j) {
+        const int i = j * 32 + lane;
+        sreg[j] = (in_regs && i < L) ? __ldcg(sv + i) : INFINITY;
+      }
+      auto key_of = [](float f) {
+        const uint32_t u = __float_as_uint(f);
+        return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+      };
       float thr = INFINITY;
       if (k < L) {
         uint32_t prefix = 0, pmask = 0;
@@ -430,10 +444,17 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
         for (int shift = 24; shift >= 0; shift -= 8) {
           for (int i = lane; i < 256; i += 32) hist[warp][i] = 0;
           __syncwarp();
-          for (int i = lane; i < L; i += 32) {
-            const uint32_t u = __float_as_uint(__ldcg(sv + i));
-            const uint32_t key = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-            if ((key & pmask) == prefix) atomicAdd(&hist[warp][(key >> shift) & 255u], 1u);
+          if (in_regs) {
+#pragma unroll
+            for (int j = 0; j < kRegRows; ++j) {
+              const uint32_t key = key_of(sreg[j]);
+              if (j * 32 + lane < L && (key & pmask) == prefix) atomicAdd(&hist[warp][(key >> shift) & 255u], 1u);
+            }
+          } else {
+            for (int i = lane; i < L; i += 32) {
+              const uint32_t key = key_of(__ldcg(sv + i));
+              if ((key & pmask) == prefix) atomicAdd(&hist[warp][(key >> shift) & 255u], 1u);
+            }
           }
           __syncwarp();
           unsigned loc[8], sum = 0;
@@ -473,11 +494,22 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
         const uint32_t u = (prefix & 0x80000000u) ? (prefix & 0x7FFFFFFFu) : ~prefix;
         thr = __uint_as_float(u);
       }
-      for (int w = 0; w < nchunks; ++w) {
-        const int i = w * kSelRowsPerCta + lane;
-        const bool fl = i < L && __ldcg(sv + i) < thr;
-        const unsigned m = __ballot_sync(0xffffffffu, fl);
-        if (lane == 0) masks[sq * nchunks + w] = m;
+      if (in_regs) {
+#pragma unroll
+        for (int w = 0; w < kRegRows; ++w) {
+          if (w < nchunks) {
+            const bool fl = w * 32 + lane < L && sreg[w] < thr;
+            const unsigned m = __ballot_sync(0xffffffffu, fl);
+            if (lane == 0) masks[sq * nchunks + w] = m;
+          }
+        }
+      } else {
+        for (int w = 0; w < nchunks; ++w) {
+          const int i = w * kSelRowsPerCta + lane;
+          const bool fl = i < L && __ldcg(sv + i) < thr;
+          const unsigned m = __ballot_sync(0xffffffffu, fl);
+          if (lane == 0) masks[sq * nchunks + w] = m;
+        }
       }
     }
     __syncthreads();

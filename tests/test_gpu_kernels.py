@@ -52,7 +52,11 @@ def test_gemm_vs_torch(dy, ctx, M_cap, M, N, K):
     (512, 512, 512, 12288),     # maximum skinny M, long K (dozens of split-K contributors per block)
     (512, 300, 4096, 12288),    # FFN-down shape: 16 weight blocks split over all SM pairs
     (512, 100, 24576, 4096),    # gate/up width, M <= 256 (double-buffered TMEM accumulator)
-    (1024, 700, 1024, 256),     # device M > 512: skinny exits, standard kernel computes
+    (1024, 700, 1024, 256),     # M > 512: three activation chunks of <= 256 rows
+    (2048, 1530, 4096, 4096),   # full-input O-proj row count: 6 chunks x 16 weight blocks, ragged last chunk
+    (2048, 2048, 512, 12288),   # maximum skinny M, long K
+    (4096, 2500, 512, 256),     # 10 activation chunks
+    (17000, 16500, 256, 128),   # device M > 16384: skinny exits, standard kernel computes
 ])
 def test_gemm_skinny_vs_torch(dy, ctx, skinny, M_cap, M, N, K):
     prev = dy.set_option(dy.OPT_SKINNY_GEMM, skinny)
@@ -83,17 +87,18 @@ def test_gemm_skinny_vs_torch(dy, ctx, skinny, M_cap, M, N, K):
 
 
 @pytest.mark.parametrize("S", [1, 2, 3, 4, 16, 64])
-@pytest.mark.parametrize("M,N,K", [(410, 4096, 4096), (100, 12288, 4096), (257, 512, 1024)])
+@pytest.mark.parametrize("M,N,K", [(410, 4096, 4096), (100, 12288, 4096), (257, 512, 1024), (1530, 4096, 4096)])
 def test_gemm_skinny_split_granularity(dy, ctx, S, M, N, K):
     """Every split-K granularity gives the same result (fixed-order fp32 reduction)."""
     prev = dy.set_option(dy.OPT_SKINNY_SPLIT, S)
     try:
         g = torch.Generator(device="cuda").manual_seed(S * 7 + M)
-        A = (torch.randn(512, K, device="cuda", generator=g) * 0.5).bfloat16()
+        cap = 2048
+        A = (torch.randn(cap, K, device="cuda", generator=g) * 0.5).bfloat16()
         W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
-        R = torch.randn(512, N, device="cuda", generator=g).bfloat16()
+        R = torch.randn(cap, N, device="cuda", generator=g).bfloat16()
         Md = torch.tensor([M], dtype=torch.int32, device="cuda")
-        D = torch.full((512, N), 7.0, device="cuda").bfloat16()
+        D = torch.full((cap, N), 7.0, device="cuda").bfloat16()
         ctx.gemm_bf16(A, W, D, M_dev=Md, resid=R)
         torch.cuda.synchronize()
         ref = A[:M].float() @ W.float().T + R[:M].float()
