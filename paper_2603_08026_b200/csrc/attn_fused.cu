@@ -339,73 +339,89 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ================================================================ MMA issuer
-    constexpr uint32_t id_qk = idesc_bf16_f32(128, FA_BK);
-    constexpr uint32_t id_pv = idesc_bf16_f32(128, 128) | (1u << 16);  // B (V) MN-major
-    int qi = 0, ks = 0, vs = 0, sc = 0, pc = 0, ai = 0;
-    uint32_t kph = 0, vph = 0;
-    FaItem it;
-    for (int w = next_item(it); w >= 0; w = next_item(it)) {
-      const int qb = qi & 1;
-      fa_wait(&q_full[qb], (qi >> 1) & 1, TR(3));
-      ++qi;
-      const uint32_t qa = smem_u32(sQ + qb * FA_Q_BYTES);
-      auto qk = [&]() {
-        const int sb = sc & 1;
-        fa_wait(&s_empty[sb], ((sc >> 1) & 1) ^ 1, TR(4));
-        fa_wait(&k_full[ks], kph, TR(5));
-        tc_fence_after();
-        const unsigned long long ti = tron ? clock64() : 0;
-        if (lane == 0) {
-          const uint32_t kb = smem_u32(sK + ks * FA_KV_BYTES);
+    // ================================================================ MMA issuer: one thread runs
+    // the whole role (no per-instruction divergence handling), with every smem descriptor formed
+    // once and advanced by constant offsets (the descriptor's address field is addr >> 4)
+    if (lane == 0) {
+      constexpr uint32_t id_qk = idesc_bf16_f32(128, FA_BK);
+      constexpr uint32_t id_pv = idesc_bf16_f32(128, 128) | (1u << 16);  // B (V) MN-major
+      uint64_t kdesc[FA_KST], vdesc[FA_VST], qdesc[FA_QST];
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_bf16(tmem + sb * FA_BK, sw128_kmajor_desc(qa + (kk >> 2) * (FA_Q_BYTES / 2) + (kk & 3) * 32),
-                      sw128_kmajor_desc(kb + (kk >> 2) * (FA_KV_BYTES / 2) + (kk & 3) * 32), id_qk, kk > 0);
+      for (int i = 0; i < FA_KST; ++i) kdesc[i] = sw128_kmajor_desc(smem_u32(sK + i * FA_KV_BYTES));
+#pragma unroll
+      for (int i = 0; i < FA_VST; ++i) vdesc[i] = sw128_mn_desc(smem_u32(sV + i * FA_KV_BYTES), FA_KV_BYTES / 2);
+#pragma unroll
+      for (int i = 0; i < FA_QST; ++i) qdesc[i] = sw128_kmajor_desc(smem_u32(sQ + i * FA_Q_BYTES));
+      // K-major operand: k-step kk (16 elements) at +32 B within a 64-column half, halves 16 KB apart
+      auto koff = [](int kk) -> uint64_t { return static_cast<uint64_t>(((kk >> 2) * (FA_KV_BYTES / 2) + (kk & 3) * 32) >> 4); };
+      int qi = 0, ks = 0, vs = 0, sc = 0, pc = 0, ai = 0, wn1 = 0;
+      uint32_t kph = 0, vph = 0;
+      for (;;) {
+        // work queue (single-thread form of next_item)
+        const int slot = wn1 & 3;
+        fa_wait(&wq_full[slot], (wn1 >> 2) & 1, TR(18));
+        const int4 q = wq[slot];
+        mbar_arrive(&wq_empty[slot]);
+        ++wn1;
+        if (q.x < 0) break;
+        const FaItem it = fa_item(p, q.x, q.y, q.z);
+        const int qb = qi & 1;
+        fa_wait(&q_full[qb], (qi >> 1) & 1, TR(3));
+        ++qi;
+        const uint64_t qd = qdesc[qb];
+        auto qk = [&]() {
+          const int sb = sc & 1;
+          fa_wait(&s_empty[sb], ((sc >> 1) & 1) ^ 1, TR(4));
+          fa_wait(&k_full[ks], kph, TR(5));
+          tc_fence_after();
+          const unsigned long long ti = tron ? clock64() : 0;
+          const uint64_t kd = kdesc[ks];
+          const uint32_t dst = tmem + sb * FA_BK;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) umma_bf16(dst, qd + koff(kk), kd + koff(kk), id_qk, kk > 0);
           umma_commit(&k_empty[ks]);
           umma_commit(&s_full[sb]);
-        }
-        __syncwarp();
-        if (tron) tr[19] += clock64() - ti;
-        if (++ks == FA_KST) {
-          ks = 0;
-          kph ^= 1;
-        }
-        ++sc;
-      };
-      for (int kt = 0; kt < NKT; ++kt) qk();
-      if (it.passP) {
-        const int n2 = (it.nkP + FA_BK - 1) / FA_BK;
-        qk();
-        for (int j = 0; j < n2; ++j) {
-          if (j + 1 < n2) qk();
-          const int pb = pc & 1;
-          fa_wait(&p_full[pb], (pc >> 1) & 1, TR(6));
-          fa_wait(&v_full[vs], vph, TR(7));
-          if (j == 0) fa_wait(acc_empty, (ai & 1) ^ 1, TR(8));
-          tc_fence_after();
-          if (lane == 0) {
-            const uint32_t vb = smem_u32(sV + vs * FA_KV_BYTES);
+          if (tron) tr[19] += clock64() - ti;
+          if (++ks == FA_KST) {
+            ks = 0;
+            kph ^= 1;
+          }
+          ++sc;
+        };
+        for (int kt = 0; kt < NKT; ++kt) qk();
+        if (it.passP) {
+          const int n2 = (it.nkP + FA_BK - 1) / FA_BK;
+          qk();
+          for (int j = 0; j < n2; ++j) {
+            if (j + 1 < n2) qk();
+            const int pb = pc & 1;
+            fa_wait(&p_full[pb], (pc >> 1) & 1, TR(6));
+            fa_wait(&v_full[vs], vph, TR(7));
+            if (j == 0) fa_wait(acc_empty, (ai & 1) ^ 1, TR(8));
+            tc_fence_after();
+            const unsigned long long tpv = tron ? clock64() : 0;
+            const uint64_t vd = vdesc[vs];
+            const uint32_t pa = tmem + FA_P_COL + pb * 64;
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk)  // 16 keys per MMA: 8 packed TMEM columns of P, 2 KB of V
-              umma_bf16_ts(tmem + FA_ACC_COL, tmem + FA_P_COL + pb * 64 + kk * 8,
-                           sw128_mn_desc(vb + kk * 2048, FA_KV_BYTES / 2), id_pv, (j | kk) != 0);
+              umma_bf16_ts(tmem + FA_ACC_COL, pa + kk * 8, vd + static_cast<uint64_t>(kk * 2048 >> 4), id_pv,
+                           (j | kk) != 0);
             umma_commit(&v_empty[vs]);
             umma_commit(&p_empty[pb]);
             if (j == n2 - 1) umma_commit(acc_full);
+            if (tron) tr[17] += clock64() - tpv;
+            if (++vs == FA_VST) {
+              vs = 0;
+              vph ^= 1;
+            }
+            ++pc;
           }
-          __syncwarp();
-          if (++vs == FA_VST) {
-            vs = 0;
-            vph ^= 1;
-          }
-          ++pc;
+          ++ai;
         }
-        ++ai;
+        umma_commit(&q_empty[qb]);
       }
-      if (lane == 0) umma_commit(&q_empty[qb]);
-      __syncwarp();
     }
+    __syncwarp();
   } else {
     // ================================================================ softmax / epilogue warps 2-9
     const int quad = warp & 3;            // TMEM lane quadrant this warp may access
@@ -436,12 +452,14 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           continue;
         }
         tc_fence_after();
+        const unsigned long long tld = tron ? clock64() : 0;
         float v[64];
         tmem_ld32(trow + sb * FA_BK + hh * 64, v);
         tmem_ld32(trow + sb * FA_BK + hh * 64 + 32, v + 32);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[sb]);
+        if (tron) tr[17] += clock64() - tld;
         const int k0 = kt * FA_BK + hh * 64;
         if (k0 + 64 > p.N) {  // ragged last tile: mask keys >= N
 #pragma unroll
@@ -565,11 +583,14 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       p.trace[blockIdx.x * 32 + 13] = clock64() - t_begin;
       for (int i = 14; i < 17; ++i) p.trace[blockIdx.x * 32 + i] = tr[i];
       p.trace[blockIdx.x * 32 + 17] = tr[18];  // softmax next_item wait
+      p.trace[blockIdx.x * 32 + 22] = tr[17];  // softmax pass-S TMEM load time
     }
     if (warp == 1) {
       p.trace[blockIdx.x * 32 + 18] = tr[18];  // MMA next_item wait
       p.trace[blockIdx.x * 32 + 19] = tr[19];  // MMA QK issue time
       p.trace[blockIdx.x * 32 + 20] = clock64() - t_begin;
+      p.trace[blockIdx.x * 32 + 21] = tr[17];  // MMA P.V issue time
+      p.trace[blockIdx.x * 32 + 23] = tr[16];  // MMA fence time before QK issue
     }
   }
 #undef TR

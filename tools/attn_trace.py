@@ -44,7 +44,7 @@ t = tr.view(148, 32).cpu().numpy().astype(np.float64) / 1.9e3  # cycles -> us at
 names = ["prod k_empty", "prod q_empty", "vprod v_empty", "mma q_full", "mma s_empty", "mma k_full", "mma p_full",
          "mma v_full", "mma acc_empty", "smx s_full(S)", "smx s_full(P)", "smx p_empty", "smx acc_full", "total",
          "smx passS (incl wait)", "smx passP (incl wait)", "smx epilogue", "smx next_item", "mma next_item",
-         "mma QK issue", "mma total"]
+         "mma QK issue", "mma total", "mma PV issue", "smx passS tmem ld", "mma QK fence"]
 print(f"mode {a.mode} step {target}: per-CTA wait time (us, median / max over CTAs)")
 for i, n in enumerate(names):
     print(f"  {n:15s} {np.median(t[:, i]):8.1f} {t[:, i].max():8.1f}")
