@@ -379,6 +379,7 @@ int gemm_launch(const GemmCall &g, int num_sms, cudaStream_t st) {
     if (g.M_ptr) {
       int rc = gemm_skinny_launch(g, num_sms, st);
       if (rc) return rc;
+      if (g.M_cap <= kSkinnyMaxM) return DYLLM_OK;  // the device count can never leave the skinny range
       s.m_skip_le = kSkinnyMaxM;
     }
   }

@@ -1,5 +1,7 @@
 // kernels.cu — the HBM-bound kernels of the salient step
 // and the list / unmasking plumbing. All row counts are read from device memory.
+#include <algorithm>
+
 #include "common.cuh"
 #include "internal.h"
 #include "kernels.h"
@@ -37,10 +39,14 @@ __global__ void gather_rmsnorm_kernel(const bf16 *__restrict__ src, const int *_
     uint4 *o = reinterpret_cast<uint4 *>(dst + static_cast<int64_t>(i) * d);
     const uint4 *gv = reinterpret_cast<const uint4 *>(g);
     if (nv <= 32 * VMAX) {
-      uint4 v[VMAX];
+      // row and gain loads issued together (one memory round trip per row)
+      uint4 v[VMAX], gw[VMAX];
 #pragma unroll
       for (int u = 0; u < VMAX; ++u)
         if (lane + u * 32 < nv) v[u] = ld_nc_v4(s + lane + u * 32);
+#pragma unroll
+      for (int u = 0; u < VMAX; ++u)
+        if (lane + u * 32 < nv) gw[u] = gv[lane + u * 32];
       float ss = 0.f;
 #pragma unroll
       for (int u = 0; u < VMAX; ++u)
@@ -57,7 +63,7 @@ __global__ void gather_rmsnorm_kernel(const bf16 *__restrict__ src, const int *_
         if (lane + u * 32 < nv) {
           float f[8], w[8];
           unpack8(v[u], f);
-          unpack8(gv[lane + u * 32], w);
+          unpack8(gw[u], w);
 #pragma unroll
           for (int j = 0; j < 8; ++j) f[j] = f[j] * inv * w[j];
           o[lane + u * 32] = pack8(f);
@@ -137,69 +143,98 @@ __global__ void qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restr
   const int M = M_ptr ? *M_ptr : M_cap;
   const int qw = H * hd, kw = KVH * hd, W = qw + 2 * kw;
   const int half = hd / 2, hv = half / 8;  // 8 rotation pairs per thread (16-byte vectors)
+  const int nqk = (H + KVH) * hv, nvv = kw / 8;
+  const int rounds = (max(nqk, nvv) + blockDim.x - 1) / blockDim.x;  // 1 with the host's block size
   for (int i = blockIdx.x; i < M; i += gridDim.x) {
     const int r = idx ? idx[i] : i;
     const int pos = r % N;
     const bf16 *src = qkv + static_cast<int64_t>(i) * W;
     const float2 *cs = rope_cs + static_cast<int64_t>(pos) * half;
-    // q and k heads: pairs (x[k], x[k + hd/2]) rotated by pos * theta^(-2k/hd) (table, fp64-derived)
-    for (int v = threadIdx.x; v < (H + KVH) * hv; v += blockDim.x) {
-      const int head = v / hv, k0 = (v - head * hv) * 8;
-      const int col = head * hd + k0;  // q cols [0,qw), k cols [qw, qw+kw): heads contiguous
-      float x1[8], x2[8];
-      unpack8(*reinterpret_cast<const uint4 *>(src + col), x1);
-      unpack8(*reinterpret_cast<const uint4 *>(src + col + half), x2);
-      if (bias) {
-        float b1[8], b2[8];
-        unpack8(*reinterpret_cast<const uint4 *>(bias + col), b1);
-        unpack8(*reinterpret_cast<const uint4 *>(bias + col + half), b2);
+    for (int rd = 0; rd < rounds; ++rd) {
+      const int v = rd * blockDim.x + threadIdx.x;
+      const bool has_qk = v < nqk, has_v = v < nvv;
+      // all loads of this thread first (one memory round trip): its q/k rotation pairs + table,
+      // its V slice and the V cache slice it replaces
+      int head = 0, k0 = 0, col = 0;
+      uint4 u1 = make_uint4(0, 0, 0, 0), u2 = u1, ub1 = u1, ub2 = u1, uv = u1, uvb = u1, uvo = u1;
+      float4 c4[4];
+      if (has_qk) {
+        head = v / hv;
+        k0 = (v - head * hv) * 8;
+        col = head * hd + k0;  // q cols [0,qw), k cols [qw, qw+kw): heads contiguous
+        u1 = *reinterpret_cast<const uint4 *>(src + col);
+        u2 = *reinterpret_cast<const uint4 *>(src + col + half);
+        if (bias) {
+          ub1 = *reinterpret_cast<const uint4 *>(bias + col);
+          ub2 = *reinterpret_cast<const uint4 *>(bias + col + half);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c4[j] = reinterpret_cast<const float4 *>(cs + k0)[j];
+      }
+      const int vc0 = v * 8;
+      uint4 *vc = reinterpret_cast<uint4 *>(Vc + static_cast<int64_t>(r) * kw + vc0);
+      if (has_v) {
+        uv = *reinterpret_cast<const uint4 *>(src + qw + kw + vc0);
+        if (bias) uvb = *reinterpret_cast<const uint4 *>(bias + qw + kw + vc0);
+        if (dV) uvo = *vc;
+      }
+      // q and k heads: pairs (x[k], x[k + hd/2]) rotated by pos * theta^(-2k/hd) (table, fp64-derived)
+      if (has_qk) {
+        float x1[8], x2[8];
+        unpack8(u1, x1);
+        unpack8(u2, x2);
+        if (bias) {
+          float b1[8], b2[8];
+          unpack8(ub1, b1);
+          unpack8(ub2, b2);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            x1[j] += b1[j];
+            x2[j] += b2[j];
+          }
+        }
+        const float *cf = reinterpret_cast<const float *>(c4);
+        float y1[8], y2[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          x1[j] += b1[j];
-          x2[j] += b2[j];
+          const float cc = cf[2 * j], sn = cf[2 * j + 1];
+          y1[j] = x1[j] * cc - x2[j] * sn;
+          y2[j] = x2[j] * cc + x1[j] * sn;
+        }
+        bf16 *dst = (col < qw) ? Qc + static_cast<int64_t>(r) * qw + col : Kc + static_cast<int64_t>(r) * kw + (col - qw);
+        const uint4 p1 = pack8(y1), p2 = pack8(y2);
+        *reinterpret_cast<uint4 *>(dst) = p1;
+        *reinterpret_cast<uint4 *>(dst + half) = p2;
+        // compact copies aligned with the packed list (the attention kernel's exact-row queries
+        // and salient keys are then contiguous rows: TMA tiles)
+        bf16 *cx = (col < qw) ? (Qx ? Qx + static_cast<int64_t>(i) * qw + col : nullptr)
+                              : (Kx ? Kx + static_cast<int64_t>(i) * kw + (col - qw) : nullptr);
+        if (cx) {
+          *reinterpret_cast<uint4 *>(cx) = p1;
+          *reinterpret_cast<uint4 *>(cx + half) = p2;
         }
       }
-      float y1[8], y2[8];
+      // v: dV = v_new - V_cache (read before the overwrite), then V_cache <- v_new
+      if (has_v) {
+        float vv[8];
+        unpack8(uv, vv);
+        if (bias) {
+          float bb[8];
+          unpack8(uvb, bb);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float2 c = cs[k0 + j];
-        y1[j] = x1[j] * c.x - x2[j] * c.y;
-        y2[j] = x2[j] * c.x + x1[j] * c.y;
-      }
-      bf16 *dst = (col < qw) ? Qc + static_cast<int64_t>(r) * qw + col : Kc + static_cast<int64_t>(r) * kw + (col - qw);
-      const uint4 p1 = pack8(y1), p2 = pack8(y2);
-      *reinterpret_cast<uint4 *>(dst) = p1;
-      *reinterpret_cast<uint4 *>(dst + half) = p2;
-      // compact copies aligned with the packed list (the attention kernel's exact-row queries
-      // and salient keys are then contiguous rows: TMA tiles)
-      bf16 *cx = (col < qw) ? (Qx ? Qx + static_cast<int64_t>(i) * qw + col : nullptr)
-                            : (Kx ? Kx + static_cast<int64_t>(i) * kw + (col - qw) : nullptr);
-      if (cx) {
-        *reinterpret_cast<uint4 *>(cx) = p1;
-        *reinterpret_cast<uint4 *>(cx + half) = p2;
-      }
-    }
-    // v: dV = v_new - V_cache (read before the overwrite), then V_cache <- v_new
-    for (int c = threadIdx.x * 8; c < kw; c += blockDim.x * 8) {
-      float v[8];
-      unpack8(*reinterpret_cast<const uint4 *>(src + qw + kw + c), v);
-      if (bias) {
-        float bb[8];
-        unpack8(*reinterpret_cast<const uint4 *>(bias + qw + kw + c), bb);
+          for (int j = 0; j < 8; ++j) vv[j] += bb[j];
+        }
+        const uint4 vb = pack8(vv);
+        if (dV) {
+          float vn[8], vo[8], dd[8];
+          unpack8(vb, vn);
+          unpack8(uvo, vo);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] += bb[j];
+          for (int j = 0; j < 8; ++j) dd[j] = vn[j] - vo[j];
+          *reinterpret_cast<uint4 *>(dV + static_cast<int64_t>(i) * kw + vc0) = pack8(dd);
+        }
+        *vc = vb;
       }
-      const uint4 vb = pack8(v);
-      uint4 *vc = reinterpret_cast<uint4 *>(Vc + static_cast<int64_t>(r) * kw + c);
-      if (dV) {
-        float vn[8], vo[8], dd[8];
-        unpack8(vb, vn);
-        unpack8(*vc, vo);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) dd[j] = vn[j] - vo[j];
-        *reinterpret_cast<uint4 *>(dV + static_cast<int64_t>(i) * kw + c) = pack8(dd);
-      }
-      *vc = vb;
     }
   }
 }
@@ -730,7 +765,10 @@ __global__ void fill_const_kernel(bf16 *__restrict__ dst, int64_t n, float v) {
 }
 
 // ============================================================================ launch wrappers
-static inline int grid_for(int64_t work, int per_block, int cap = 148 * 16) {
+// Row kernels read their row count from device memory, so the grid is sized for the capacity;
+// it is capped at two CTAs per SM (grid-stride loops) so that a small device count does not pay
+// for launching and retiring thousands of empty CTAs.
+static inline int grid_for(int64_t work, int per_block, int cap = 148 * 2) {
   int64_t g = (work + per_block - 1) / per_block;
   if (g < 1) g = 1;
   return static_cast<int>(g < cap ? g : cap);
@@ -742,7 +780,7 @@ void launch_embed_rows(const int *tokens, const int *rows, const int *M_ptr, int
 }
 void launch_gather_rmsnorm(const bf16 *src, const int *idx, const int *M_ptr, int M_cap, const bf16 *g, float eps,
                            bf16 *dst, int d, cudaStream_t st) {
-  gather_rmsnorm_kernel<<<grid_for(M_cap, 8), 256, 0, st>>>(src, idx, M_ptr, M_cap, g, eps, dst, d);
+  gather_rmsnorm_kernel<<<grid_for(M_cap, 4, 148 * 4), 128, 0, st>>>(src, idx, M_ptr, M_cap, g, eps, dst, d);
 }
 void launch_gather_rows(const bf16 *src, const int *idx, const int *M_ptr, int M_cap, bf16 *dst, int width,
                         cudaStream_t st) {
@@ -754,13 +792,15 @@ void launch_scatter_rows(const bf16 *src, const int *idx, const int *M_ptr, int 
 }
 void launch_rmsnorm_rows(const bf16 *src, const int *M_ptr, int M_cap, const bf16 *g, float eps, bf16 *dst, int d,
                          cudaStream_t st) {
-  gather_rmsnorm_kernel<<<grid_for(M_cap, 8), 256, 0, st>>>(src, nullptr, M_ptr, M_cap, g, eps, dst, d);
+  gather_rmsnorm_kernel<<<grid_for(M_cap, 4, 148 * 4), 128, 0, st>>>(src, nullptr, M_ptr, M_cap, g, eps, dst, d);
 }
 void launch_qkv_post(const bf16 *qkv, const int *idx, const int *M_ptr, int M_cap, const bf16 *bias, int N, int H,
                      int KVH, int hd, const float2 *rope_cs, bf16 *Qc, bf16 *Kc, bf16 *Vc, bf16 *dV, bf16 *Qx,
                      bf16 *Kx, cudaStream_t st) {
-  const int g = M_cap < 148 * 8 ? M_cap : 148 * 8;
-  qkv_post_kernel<<<g > 0 ? g : 1, 256, 0, st>>>(qkv, idx, M_ptr, M_cap, bias, N, H, KVH, hd, rope_cs, Qc, Kc, Vc,
+  const int g = M_cap < 148 * 4 ? M_cap : 148 * 4;  // one row per CTA per pass; capped like grid_for
+  const int work = std::max((H + KVH) * (hd / 16), KVH * hd / 8);  // vectors per row of each part
+  const int threads = std::min(1024, std::max(32, (work + 31) / 32 * 32));
+  qkv_post_kernel<<<g > 0 ? g : 1, threads, 0, st>>>(qkv, idx, M_ptr, M_cap, bias, N, H, KVH, hd, rope_cs, Qc, Kc, Vc,
                                                  dV, Qx, Kx);
 }
 void launch_rope_table(float2 *cs, int N, int hd, double theta, cudaStream_t st) {
