@@ -647,6 +647,7 @@ static int launch_split(const AttnArgs &a, cudaStream_t st) {
 
 bool g_attn_fused_enabled = true;
 unsigned long long *g_attn_trace = nullptr;
+unsigned long long *g_attn_events = nullptr;
 
 bool attention_writes_delta(int hd) { return hd == 128 && g_attn_fused_enabled; }
 

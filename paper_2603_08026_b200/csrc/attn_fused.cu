@@ -30,11 +30,20 @@ constexpr int FA_BK = 128;                 // keys per tile (MMA N = 128: the Q 
                                            // instruction is amortised over 128 keys)
 constexpr int FA_Q_BYTES = 128 * 256;      // 128 rows x 128 bf16: two 64-column halves of 16 KB
 constexpr int FA_KV_BYTES = 128 * 256;     // 128 keys x 128 bf16: two 64-column halves of 16 KB
-constexpr int FA_QST = 2, FA_KST = 2, FA_VST = 2;
-constexpr int FA_DATA = FA_QST * FA_Q_BYTES + FA_KST * FA_KV_BYTES + FA_VST * FA_KV_BYTES;
-constexpr int FA_XCH = 2 * 128 * 8;        // (m, l) per half per row
+constexpr int FA_QST = 2;
+constexpr int FA_KVST = 4;                 // unified K / V / dV tile ring, filled in MMA consumption order
+constexpr int FA_DATA = FA_QST * FA_Q_BYTES + FA_KVST * FA_KV_BYTES;
+// softmax warps: FA_NG column groups x 4 TMEM lane quadrants; each warp owns 32 rows x FA_CW keys
+// of a score tile (and FA_CW head dims of the output)
+constexpr int FA_NG = 4;
+constexpr int FA_CW = FA_BK / FA_NG;
+constexpr int FA_NSW = 4 * FA_NG;           // softmax warps 2 .. 1 + FA_NSW
+constexpr int FA_WV = 2 + FA_NSW;           // V / dV producer warp
+constexpr int FA_WK2 = 3 + FA_NSW;          // second K producer warp
+constexpr int FA_THREADS = 32 * (4 + FA_NSW);
+constexpr int FA_XCH = FA_NG * 128 * 8;     // (m, l) per column group per row
 constexpr int FA_SMEM = 1024 + FA_DATA + FA_XCH + 512;
-constexpr int FA_THREADS = 384;            // + warp 10: V producer, warp 11: second K producer
+static_assert(FA_CW % 32 == 0, "column groups are whole 32-column TMEM loads");
 // TMEM columns: S[2] (2 x 128 fp32), accumulator (128 fp32), P[2] (2 x 64: 128 keys bf16x2-packed,
 // the A operand of the P V MMA read straight from TMEM)
 constexpr int FA_TMEM_COLS = 512;
@@ -51,6 +60,7 @@ struct FaParams {
   bf16 *C_out;
   unsigned long long *trace;  // optional [grid][32] wait-cycle counters (debug hook)
   int *work_ctr;              // [2] dynamic scheduler: next item, finished CTAs (zero between launches)
+  unsigned long long *events; // optional event log of CTAs 0-1 (debug hook): [cta][role][8192]
 };
 
 struct FaItem {
@@ -153,6 +163,19 @@ __device__ __forceinline__ void fa_named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// debug event log: one 8192-entry region per (CTA < 2, role); entry = code << 56 | clock64
+constexpr int FA_EV_N = 8192;
+struct FaEv {
+  unsigned long long *buf = nullptr;
+  int n = 0;
+  __device__ __forceinline__ void operator()(int code) {
+    if (buf && n < FA_EV_N) buf[n++] = (static_cast<unsigned long long>(code) << 56) | (clock64() & ((1ull << 56) - 1));
+  }
+  __device__ __forceinline__ void finish() {
+    if (buf && n < FA_EV_N) buf[n] = 0;  // terminator (later launches overwrite the same region)
+  }
+};
+
 __global__ void __launch_bounds__(FA_THREADS, 1)
     attn_fused_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQx,
                       const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
@@ -161,13 +184,11 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t *sQ = smem;                                   // [2][32 KB]
-  uint8_t *sK = sQ + FA_QST * FA_Q_BYTES;               // [2][32 KB]
-  uint8_t *sV = sK + FA_KST * FA_KV_BYTES;              // [2][32 KB]
-  float2 *xch = reinterpret_cast<float2 *>(sV + FA_VST * FA_KV_BYTES);  // [2 halves][128 rows]
+  uint8_t *sKV = sQ + FA_QST * FA_Q_BYTES;              // [4][32 KB] K, V or dV tiles
+  float2 *xch = reinterpret_cast<float2 *>(sKV + FA_KVST * FA_KV_BYTES);  // [column group][128 rows]
   uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(xch) + FA_XCH);
   uint64_t *q_full = bars, *q_empty = bars + 2;
-  uint64_t *k_full = bars + 4, *k_empty = bars + 7;
-  uint64_t *v_full = bars + 10, *v_empty = bars + 12;
+  uint64_t *kv_full = bars + 4, *kv_empty = bars + 8;   // [FA_KVST]
   uint64_t *s_full = bars + 14, *s_empty = bars + 16;
   uint64_t *p_full = bars + 18, *p_empty = bars + 20;
   uint64_t *acc_full = bars + 22, *acc_empty = bars + 23;
@@ -184,6 +205,12 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   const bool tron = p.trace != nullptr && lane == 0;
 #define TR(k) (tron ? &tr[k] : nullptr)
   const unsigned long long t_begin = clock64();
+  // event roles: 0 MMA, 1 softmax warp 2, 2 producer warp 0, 3 V producer
+  FaEv ev;
+  {
+    const int role = warp == 1 ? 0 : warp == 2 ? 1 : warp == 0 ? 2 : warp == FA_WV ? 3 : -1;
+    if (p.events && blockIdx.x < 2 && lane == 0 && role >= 0) ev.buf = p.events + (blockIdx.x * 4 + role) * FA_EV_N;
+  }
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
@@ -195,22 +222,20 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
-      mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 8);
-      mbar_init(&p_full[i], 8);
+      mbar_init(&s_empty[i], FA_NSW);
+      mbar_init(&p_full[i], FA_NSW);
       mbar_init(&p_empty[i], 1);
     }
-    for (int i = 0; i < FA_KST; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
+    for (int i = 0; i < FA_KVST; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
     }
     mbar_init(acc_full, 1);
-    mbar_init(acc_empty, 8);
+    mbar_init(acc_empty, FA_NSW);
     for (int i = 0; i < 4; ++i) {
       mbar_init(&wq_full[i], 1);
-      mbar_init(&wq_empty[i], 11);  // MMA warp, V producer, second K producer, 8 softmax warps
+      mbar_init(&wq_empty[i], 3 + FA_NSW);  // MMA warp, V producer, second K producer, softmax warps
     }
     fence_barrier_init();
   }
@@ -235,22 +260,25 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     return q.x;
   };
 
-  if (warp == 0 || warp == 11) {
-    // ================================================================ TMA producers: warp 0 claims
-    // items (work queue) and loads Q; warps 0 and 11 load alternate K tiles (global tile counter
-    // parity), doubling the TMA issue rate of the K stream
-    const int kpar = warp == 0 ? 0 : 1;
-    int kg = 0;  // global K tile counter (ring slot kg % FA_KST, phase (kg / FA_KST) & 1)
-    auto load_k = [&](const CUtensorMap *m, int row, int kvh) {
-      if ((kg & 1) == kpar && lane == 0) {
-        const int ks = kg % FA_KST;
-        fa_wait(&k_empty[ks], ((kg / FA_KST) & 1) ^ 1, TR(0));
-        mbar_expect_tx(&k_full[ks], FA_KV_BYTES);
-        tma_load_3d(sK + ks * FA_KV_BYTES, m, &k_full[ks], 0, row, kvh * 2);
+  if (warp == 0 || warp == FA_WK2 || warp == FA_WV) {
+    // ================================================================ TMA producers. Warp 0 claims
+    // items (work queue) and loads Q. All three producer warps walk the same tile sequence — the
+    // order in which the MMA warp consumes K / V / dV tiles — and each issues every third tile
+    // into the 4-slot ring (ring index g: slot g % 4), tripling the TMA issue rate of one thread
+    const int pid = warp == 0 ? 0 : warp == FA_WK2 ? 1 : 2;
+    int g = 0;  // ring index of the next tile in consumption order
+    auto load_kv = [&](const CUtensorMap *m, int row, int kvh) {
+      if (g % 3 == pid && lane == 0) {
+        const int ks = g % FA_KVST;
+        ev(60);
+        fa_wait(&kv_empty[ks], ((g / FA_KVST) & 1) ^ 1, TR(0));
+        ev(61);
+        mbar_expect_tx(&kv_full[ks], FA_KV_BYTES);
+        tma_load_3d(sKV + ks * FA_KV_BYTES, m, &kv_full[ks], 0, row, kvh * 2);
       }
-      ++kg;
+      ++g;
     };
-    // warp 0 claims one item ahead: the queue already holds item i+1 while item i's K tiles are
+    // warp 0 claims one item ahead: the queue already holds item i+1 while item i's tiles are
     // issued, and Q of item i+1 is loaded early in item i, so item boundaries cost no claim
     // latency and no exposed Q load
     int wnext = -1, onext = 0, enext = 0;
@@ -306,35 +334,22 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         if (w < 0) break;
       }
       const int seq0 = it.s * p.N;
+      // pass S: the N keys
       for (int kt = 0; kt < NKT; ++kt) {
-        load_k(&tmK, seq0 + kt * FA_BK, it.kvh);
+        load_kv(&tmK, seq0 + kt * FA_BK, it.kvh);
         if (kt == 0 && warp == 0 && lane == 0 && wnext >= 0) load_q(fa_item(p, wnext, onext, enext), qi + 1);
       }
       ++qi;
+      // pass P, in the MMA warp's order: K'(0), then K'(j+1), V'(j) for each j (K' = keys of the P
+      // tiles, V' = their values: all keys + V for exact rows, salient keys + dV otherwise)
       if (it.passP) {
         const int n2 = (it.nkP + FA_BK - 1) / FA_BK;
-        for (int j = 0; j < n2; ++j)
-          load_k(it.type2 ? &tmK : &tmKx, (it.type2 ? seq0 : it.off) + j * FA_BK, it.kvh);
-      }
-    }
-  } else if (warp == 10) {
-    // ================================================================ V / dV producer
-    {
-      int vs = 0;
-      uint32_t vph = 0;
-      FaItem it;
-      for (int w = next_item(it); w >= 0; w = next_item(it)) {
-        if (!it.passP || lane != 0) continue;
-        const int n2 = (it.nkP + FA_BK - 1) / FA_BK;
+        const CUtensorMap *mk = it.type2 ? &tmK : &tmKx, *mv = it.type2 ? &tmV : &tmDV;
+        const int r0 = it.type2 ? seq0 : it.off;
+        load_kv(mk, r0, it.kvh);
         for (int j = 0; j < n2; ++j) {
-          fa_wait(&v_empty[vs], vph ^ 1, TR(2));
-          mbar_expect_tx(&v_full[vs], FA_KV_BYTES);
-          tma_load_3d(sV + vs * FA_KV_BYTES, it.type2 ? &tmV : &tmDV, &v_full[vs], 0,
-                      (it.type2 ? it.s * p.N : it.off) + j * FA_BK, it.kvh * 2);
-          if (++vs == FA_VST) {
-            vs = 0;
-            vph ^= 1;
-          }
+          if (j + 1 < n2) load_kv(mk, r0 + (j + 1) * FA_BK, it.kvh);
+          load_kv(mv, r0 + j * FA_BK, it.kvh);
         }
       }
     }
@@ -345,17 +360,17 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     if (lane == 0) {
       constexpr uint32_t id_qk = idesc_bf16_f32(128, FA_BK);
       constexpr uint32_t id_pv = idesc_bf16_f32(128, 128) | (1u << 16);  // B (V) MN-major
-      uint64_t kdesc[FA_KST], vdesc[FA_VST], qdesc[FA_QST];
+      uint64_t kdesc[FA_KVST], vdesc[FA_KVST], qdesc[FA_QST];
 #pragma unroll
-      for (int i = 0; i < FA_KST; ++i) kdesc[i] = sw128_kmajor_desc(smem_u32(sK + i * FA_KV_BYTES));
-#pragma unroll
-      for (int i = 0; i < FA_VST; ++i) vdesc[i] = sw128_mn_desc(smem_u32(sV + i * FA_KV_BYTES), FA_KV_BYTES / 2);
+      for (int i = 0; i < FA_KVST; ++i) {
+        kdesc[i] = sw128_kmajor_desc(smem_u32(sKV + i * FA_KV_BYTES));
+        vdesc[i] = sw128_mn_desc(smem_u32(sKV + i * FA_KV_BYTES), FA_KV_BYTES / 2);
+      }
 #pragma unroll
       for (int i = 0; i < FA_QST; ++i) qdesc[i] = sw128_kmajor_desc(smem_u32(sQ + i * FA_Q_BYTES));
       // K-major operand: k-step kk (16 elements) at +32 B within a 64-column half, halves 16 KB apart
       auto koff = [](int kk) -> uint64_t { return static_cast<uint64_t>(((kk >> 2) * (FA_KV_BYTES / 2) + (kk & 3) * 32) >> 4); };
-      int qi = 0, ks = 0, vs = 0, sc = 0, pc = 0, ai = 0, wn1 = 0;
-      uint32_t kph = 0, vph = 0;
+      int qi = 0, g = 0, sc = 0, pc = 0, ai = 0, wn1 = 0;  // g: K/V ring index
       for (;;) {
         // work queue (single-thread form of next_item)
         const int slot = wn1 & 3;
@@ -365,27 +380,30 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         ++wn1;
         if (q.x < 0) break;
         const FaItem it = fa_item(p, q.x, q.y, q.z);
+        ev(it.type2 ? 2 : 1);
         const int qb = qi & 1;
         fa_wait(&q_full[qb], (qi >> 1) & 1, TR(3));
         ++qi;
         const uint64_t qd = qdesc[qb];
         auto qk = [&]() {
           const int sb = sc & 1;
+          ev(10);
           fa_wait(&s_empty[sb], ((sc >> 1) & 1) ^ 1, TR(4));
-          fa_wait(&k_full[ks], kph, TR(5));
+          ev(11);
+          const int ks = g % FA_KVST;
+          fa_wait(&kv_full[ks], (g / FA_KVST) & 1, TR(5));
+          ev(12);
           tc_fence_after();
           const unsigned long long ti = tron ? clock64() : 0;
           const uint64_t kd = kdesc[ks];
           const uint32_t dst = tmem + sb * FA_BK;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) umma_bf16(dst, qd + koff(kk), kd + koff(kk), id_qk, kk > 0);
-          umma_commit(&k_empty[ks]);
+          umma_commit(&kv_empty[ks]);
           umma_commit(&s_full[sb]);
+          ev(13);
           if (tron) tr[19] += clock64() - ti;
-          if (++ks == FA_KST) {
-            ks = 0;
-            kph ^= 1;
-          }
+          ++g;
           ++sc;
         };
         for (int kt = 0; kt < NKT; ++kt) qk();
@@ -395,9 +413,13 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           for (int j = 0; j < n2; ++j) {
             if (j + 1 < n2) qk();
             const int pb = pc & 1;
+            ev(20);
             fa_wait(&p_full[pb], (pc >> 1) & 1, TR(6));
-            fa_wait(&v_full[vs], vph, TR(7));
+            ev(21);
+            const int vs = g % FA_KVST;
+            fa_wait(&kv_full[vs], (g / FA_KVST) & 1, TR(7));
             if (j == 0) fa_wait(acc_empty, (ai & 1) ^ 1, TR(8));
+            ev(22);
             tc_fence_after();
             const unsigned long long tpv = tron ? clock64() : 0;
             const uint64_t vd = vdesc[vs];
@@ -406,14 +428,12 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             for (int kk = 0; kk < 8; ++kk)  // 16 keys per MMA: 8 packed TMEM columns of P, 2 KB of V
               umma_bf16_ts(tmem + FA_ACC_COL, pa + kk * 8, vd + static_cast<uint64_t>(kk * 2048 >> 4), id_pv,
                            (j | kk) != 0);
-            umma_commit(&v_empty[vs]);
+            umma_commit(&kv_empty[vs]);
             umma_commit(&p_empty[pb]);
             if (j == n2 - 1) umma_commit(acc_full);
+            ev(23);
             if (tron) tr[17] += clock64() - tpv;
-            if (++vs == FA_VST) {
-              vs = 0;
-              vph ^= 1;
-            }
+            ++g;
             ++pc;
           }
           ++ai;
@@ -423,12 +443,13 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     }
     __syncwarp();
   } else {
-    // ================================================================ softmax / epilogue warps 2-9
+    // ================================================================ softmax / epilogue warps
     const int quad = warp & 3;            // TMEM lane quadrant this warp may access
-    const int hh = (warp - 2) >> 2;       // which 32 of the 64 columns of a score tile
+    const int hh = (warp - 2) >> 2;       // which FA_CW columns of a score tile (and head dims)
     const int r = quad * 32 + lane;       // row of the tile
     const uint32_t trow = tmem + (static_cast<uint32_t>(quad * 32) << 16);
     const float c = p.c;
+    constexpr int NCH = FA_CW / 32;       // 32-column TMEM loads per warp and tile
     int sc = 0, pc = 0, ai = 0;
     FaItem it;
     for (int w = next_item(it); w >= 0; w = next_item(it)) {
@@ -439,12 +460,15 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       // type 1 writes approximate rows only: fetch the row kind early (its latency hides under pass S)
       const int64_t orow = it.type2 ? (rvalid ? p.ex_rows[it.q_row + r] : 0) : static_cast<int64_t>(it.q_row) + r;
       const bool write_row = rvalid && (it.type2 || (it.passP && !p.rowflag[orow]));
-      // ---- pass S: running (m, l) of this half of the row
+      ev(it.type2 ? 2 : 1);
+      // ---- pass S: running (m, l) of this column group of the row
       const unsigned long long tS = tron ? clock64() : 0;
       float m = -INFINITY, l = 0.f;
       for (int kt = 0; kt < NKT; ++kt) {
         const int sb = sc & 1;
+        ev(30);
         fa_wait(&s_full[sb], (sc >> 1) & 1, TR(9));
+        ev(31);
         ++sc;
         if (!wact) {
           __syncwarp();
@@ -453,22 +477,23 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         }
         tc_fence_after();
         const unsigned long long tld = tron ? clock64() : 0;
-        float v[64];
-        tmem_ld32(trow + sb * FA_BK + hh * 64, v);
-        tmem_ld32(trow + sb * FA_BK + hh * 64 + 32, v + 32);
+        float v[FA_CW];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) tmem_ld32(trow + sb * FA_BK + hh * FA_CW + ch * 32, v + ch * 32);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[sb]);
+        ev(32);
         if (tron) tr[17] += clock64() - tld;
-        const int k0 = kt * FA_BK + hh * 64;
-        if (k0 + 64 > p.N) {  // ragged last tile: mask keys >= N
+        const int k0 = kt * FA_BK + hh * FA_CW;
+        if (k0 + FA_CW > p.N) {  // ragged last tile: mask keys >= N
 #pragma unroll
-          for (int j = 0; j < 64; ++j)
+          for (int j = 0; j < FA_CW; ++j)
             if (k0 + j >= p.N) v[j] = -INFINITY;
         }
         float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
-        for (int j = 0; j < 64; j += 4) {
+        for (int j = 0; j < FA_CW; j += 4) {
           mx0 = fmaxf(mx0, v[j]);
           mx1 = fmaxf(mx1, v[j + 1]);
           mx2 = fmaxf(mx2, v[j + 2]);
@@ -476,11 +501,11 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         }
         const float mt = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
         const float mn = fmaxf(m, mt);
-        if (mn == -INFINITY) continue;  // every key of this half-tile masked
+        if (mn == -INFINITY) continue;  // every key of this column group masked
         const float mnc = mn * c;
         float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
-        for (int j = 0; j < 64; j += 4) {
+        for (int j = 0; j < FA_CW; j += 4) {
           a0 += ex2f(fmaf(v[j], c, -mnc));
           a1 += ex2f(fmaf(v[j + 1], c, -mnc));
           a2 += ex2f(fmaf(v[j + 2], c, -mnc));
@@ -488,26 +513,34 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         }
         l = l * ex2f((m - mn) * c) + ((a0 + a1) + (a2 + a3));
         m = mn;
+        ev(33);
       }
       if (tron) tr[14] += clock64() - tS;
-      // ---- combine the two halves of each row (fixed order: half 0 then half 1)
+      // ---- combine the column groups of each row (fixed order: group 0, 1, ...)
       xch[hh * 128 + r] = make_float2(m, l);
-      fa_named_sync(1 + quad, 64);
-      const float2 h0 = xch[r], h1 = xch[128 + r];
-      fa_named_sync(1 + quad, 64);
-      const float M = fmaxf(h0.x, h1.x);
-      const float Lsum = (h0.x == -INFINITY ? 0.f : h0.y * ex2f((h0.x - M) * c)) +
-                         (h1.x == -INFINITY ? 0.f : h1.y * ex2f((h1.x - M) * c));
+      fa_named_sync(1 + quad, 32 * FA_NG);
+      float2 hg[FA_NG];
+#pragma unroll
+      for (int g = 0; g < FA_NG; ++g) hg[g] = xch[g * 128 + r];
+      fa_named_sync(1 + quad, 32 * FA_NG);
+      float M = -INFINITY;
+#pragma unroll
+      for (int g = 0; g < FA_NG; ++g) M = fmaxf(M, hg[g].x);
+      float Lsum = 0.f;
+#pragma unroll
+      for (int g = 0; g < FA_NG; ++g) Lsum += hg[g].x == -INFINITY ? 0.f : hg[g].y * ex2f((hg[g].x - M) * c);
       const float Mc = M * c;
       const float inv_l = 1.f / Lsum;
       // ---- pass P: P = exp2(s - m) into tensor memory for the P V MMA
       const unsigned long long tP = tron ? clock64() : 0;
-      float acc[64];
+      float acc[FA_CW];
       if (it.passP) {
         const int n2 = (it.nkP + FA_BK - 1) / FA_BK;
         for (int j = 0; j < n2; ++j) {
           const int sb = sc & 1;
+          ev(40);
           fa_wait(&s_full[sb], (sc >> 1) & 1, TR(10));
+          ev(41);
           ++sc;
           const int pb = pc & 1;
           ++pc;
@@ -519,15 +552,15 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             if (lane == 0) mbar_arrive(&p_full[pb]);
             continue;
           }
-          // P = exp2(s - m) for this half's 64 keys, bf16x2-packed into the P TMEM buffer (32
-          // columns per half); the S buffer is released once both chunks are read
+          // P = exp2(s - m) for this group's FA_CW keys, bf16x2-packed into the P TMEM buffer
+          // (FA_CW / 2 columns per group); the S buffer is released once all chunks are read
           fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1, TR(11));
           tc_fence_after();
 #pragma unroll
-          for (int ch = 0; ch < 2; ++ch) {
+          for (int ch = 0; ch < NCH; ++ch) {
             float v[32];
-            tmem_ld32(trow + sb * FA_BK + hh * 64 + ch * 32, v);
-            const int k0 = j * FA_BK + hh * 64 + ch * 32;
+            tmem_ld32(trow + sb * FA_BK + hh * FA_CW + ch * 32, v);
+            const int k0 = j * FA_BK + hh * FA_CW + ch * 32;
             uint32_t pk[16];
 #pragma unroll
             for (int t = 0; t < 16; ++t) {
@@ -536,7 +569,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
               const float p1 = (k0 + 2 * t + 1 < it.nkP) ? e1 : 0.f;
               pk[t] = pack2(p0, p1);
             }
-            tmem_st16(trow + FA_P_COL + pb * 64 + hh * 32 + ch * 16, pk);
+            tmem_st16(trow + FA_P_COL + pb * 64 + hh * (FA_CW / 2) + ch * 16, pk);
           }
           tmem_st_wait();
           tc_fence_before();
@@ -545,13 +578,16 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             mbar_arrive(&s_empty[sb]);
             mbar_arrive(&p_full[pb]);
           }
+          ev(42);
         }
+        ev(50);
         fa_wait(acc_full, ai & 1, TR(12));
+        ev(51);
         ++ai;
         if (wact) {
           tc_fence_after();
-          tmem_ld32(trow + FA_ACC_COL + hh * 64, acc);
-          tmem_ld32(trow + FA_ACC_COL + hh * 64 + 32, acc + 32);
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) tmem_ld32(trow + FA_ACC_COL + hh * FA_CW + ch * 32, acc + ch * 32);
           tc_fence_before();
         }
         __syncwarp();
@@ -559,25 +595,26 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       }
       if (tron) tr[15] += clock64() - tP;
       const unsigned long long tE = tron ? clock64() : 0;
-      // ---- epilogue: this thread's row, head columns [hh*64, hh*64 + 64). Exact rows (type 2):
-      // C = O / l. Approximate rows (type 1): the delta dC / l only; the similarity kernel, which
-      // reads C_cache anyway, forms C_new = C_cache + dC (no C_cache read here).
+      // ---- epilogue: this thread's row, head columns [hh*FA_CW, (hh+1)*FA_CW). Exact rows
+      // (type 2): C = O / l. Approximate rows (type 1): the delta dC / l only; the similarity
+      // kernel, which reads C_cache anyway, forms C_new = C_cache + dC (no C_cache read here).
       if (write_row) {
-        uint4 *dst = reinterpret_cast<uint4 *>(p.C_out + orow * p.qw + it.h * 128 + hh * 64);
+        uint4 *dst = reinterpret_cast<uint4 *>(p.C_out + orow * p.qw + it.h * 128 + hh * FA_CW);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < FA_CW / 8; ++u) {
           float o[8];
 #pragma unroll
           for (int t = 0; t < 8; ++t) o[t] = acc[u * 8 + t] * inv_l;
           dst[u] = pack8(o);
         }
       }
+      ev(52);
       if (tron) tr[16] += clock64() - tE;
     }
   }
-  if (tron && (warp <= 2 || warp == 10)) {
-    const int lo = warp == 0 ? 0 : warp == 10 ? 2 : warp == 1 ? 3 : 9;
-    const int hi = warp == 0 ? 2 : warp == 10 ? 3 : warp == 1 ? 9 : 13;
+  if (tron && (warp <= 2 || warp == FA_WV)) {
+    const int lo = warp == 0 ? 0 : warp == FA_WV ? 2 : warp == 1 ? 3 : 9;
+    const int hi = warp == 0 ? 2 : warp == FA_WV ? 3 : warp == 1 ? 9 : 13;
     for (int i = lo; i < hi; ++i) p.trace[blockIdx.x * 32 + i] = tr[i];
     if (warp == 2) {
       p.trace[blockIdx.x * 32 + 13] = clock64() - t_begin;
@@ -594,6 +631,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     }
   }
 #undef TR
+  ev.finish();
   __syncthreads();
   if (threadIdx.x == 0) {
     // the last CTA to finish re-arms the scheduler for the next launch (stream-ordered)
@@ -644,6 +682,7 @@ int attention_fused_launch(const AttnArgs &a, cudaStream_t st) {
   p.C_cache = a.C_cache;
   p.C_out = a.C_out;
   p.trace = g_attn_trace;
+  p.events = g_attn_events;
   p.work_ctr = a.work_ctr;
   if (!p.work_ctr) {
     set_error("fused attention: missing scheduler counters");

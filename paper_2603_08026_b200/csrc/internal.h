@@ -95,5 +95,6 @@ int attention_fused_launch(const AttnArgs &a, cudaStream_t st);  // attn_fused.c
 bool attention_writes_delta(int hd);
 extern bool g_attn_fused_enabled;  // test hook (dyllm_set_option)
 extern unsigned long long *g_attn_trace;  // debug hook (dyllm_debug_trace_buffer, which = 1)
+extern unsigned long long *g_attn_events;  // debug hook (dyllm_debug_trace_buffer, which = 2)
 
 }  // namespace dy

@@ -1,0 +1,108 @@
+"""Event timeline of the fused attention kernel (debug hook, dyllm_debug_trace_buffer which = 2):
+per-role event logs of CTAs 0-1 for the last layer of one denoising step of the bench workload.
+
+    python tools/attn_events.py --mode ro|fi|full [--items 3]
+
+Codes: MMA 1/2 item (type 1/2), 10 QK begin, 11 S buffer free, 12 K tile ready, 13 QK issued,
+20 PV begin, 21 P ready, 22 V/acc ready, 23 PV issued. Softmax (warp 2) 1/2 item, 30 S wait,
+31 S ready, 32 S read (buffer released), 33 S tile done, 40 P-pass S wait, 41 ready, 42 P stored,
+50 acc wait, 51 acc ready, 52 epilogue done. Producer 60 K slot wait, 61 K issued. V 70, 71.
+"""
+import argparse
+import collections
+import os
+import sys
+from dataclasses import replace
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2603_08026_b200 import dyllm as dy  # noqa: E402
+from synth import configs, gen  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--mode", default="ro")
+ap.add_argument("--frac", type=float, default=0.10)
+ap.add_argument("--items", type=int, default=3)
+ap.add_argument("--ghz", type=float, default=1.9)
+a = ap.parse_args()
+cfg, run = configs.preset("llada8b")
+run = replace(run, select_mode=1)
+ctx = dy.Context(0)
+w = dy.Weights.random(ctx, cfg, seed=0)
+eng = dy.Engine(ctx, w, run)
+eng.tokens[:, : run.L_P].copy_(torch.tensor(gen.prompt_tokens(0, run.batch, run.L_P, cfg.mask_id), dtype=torch.int32))
+eng.tokens[:, run.L_P:].fill_(cfg.mask_id)
+taus = np.full(cfg.n_layers, a.frac, np.float32)
+if a.mode == "full":
+    target = 0
+else:
+    t0 = run.T_full + 8
+    target = next(s for s in range(t0, run.T_total) if (s % run.full_period == 0) == (a.mode == "fi"))
+for t in range(target):
+    eng.cache.denoise_step(t, taus, eng.tokens, eng.dec_pos, eng.dec_tok)
+N_EV = 8192
+buf = torch.zeros(2 * 4 * N_EV, dtype=torch.int64, device="cuda")
+torch.cuda.synchronize()
+dy.lib().dyllm_debug_trace_buffer(2, buf.data_ptr())
+eng.cache.denoise_step(target, taus, eng.tokens, eng.dec_pos, eng.dec_tok)
+torch.cuda.synchronize()
+dy.lib().dyllm_debug_trace_buffer(2, None)
+raw = buf.view(2, 4, N_EV).cpu().numpy().astype(np.uint64)
+cyc = 1e-3 / a.ghz  # us per cycle
+
+
+def decode(arr):
+    z = np.flatnonzero(arr == 0)
+    arr = arr[: z[0]] if len(z) else arr
+    return [(int(x >> np.uint64(56)), int(x & np.uint64((1 << 56) - 1))) for x in arr]
+
+
+roles = ["MMA", "softmax(w2)", "producer(w0)", "V producer"]
+pairs = {0: [(10, 11, "S buf free wait"), (11, 12, "K tile wait"), (12, 13, "QK issue"), (20, 21, "P wait"),
+             (21, 22, "V/acc wait"), (22, 23, "PV issue")],
+         1: [(30, 31, "S wait (pass S)"), (31, 32, "S read"), (32, 33, "S math"), (40, 41, "S wait (pass P)"),
+             (41, 42, "P math+store"), (50, 51, "acc wait"), (51, 52, "epilogue")],
+         2: [(60, 61, "K slot wait")], 3: [(70, 71, "V slot wait")]}
+print(f"mode {a.mode} step {target}, last layer's launch, CTA 0 (us at {a.ghz} GHz)")
+for role in range(4):
+    ev = decode(raw[0, role])
+    if not ev:
+        continue
+    t0 = ev[0][1]
+    span = (ev[-1][1] - t0) * cyc
+    print(f"== {roles[role]}: {len(ev)} events over {span:.1f} us")
+    sums = collections.defaultdict(float)
+    cnt = collections.defaultdict(int)
+    last = {}
+    for code, t in ev:
+        for (c0, c1, name) in pairs.get(role, []):
+            if code == c1 and c0 in last:
+                sums[name] += (t - last[c0]) * cyc
+                cnt[name] += 1
+        last[code] = t
+    for (c0, c1, name) in pairs.get(role, []):
+        if cnt[name]:
+            print(f"   {name:18s} total {sums[name]:8.1f} us  n={cnt[name]:5d}  mean {sums[name] / cnt[name] * 1e3:7.0f} ns")
+    if role in (0, 1):
+        # per-item durations
+        starts = [(t, code) for code, t in ev if code in (1, 2)]
+        durs = [((starts[i + 1][0] - starts[i][0]) * cyc, starts[i][1]) for i in range(len(starts) - 1)]
+        for kind in (1, 2):
+            d = [x for x, k in durs if k == kind]
+            if d:
+                print(f"   items type {kind}: n={len(d)} mean {np.mean(d):.2f} us  min {np.min(d):.2f}  max {np.max(d):.2f}")
+# detailed timeline of the first items (MMA and softmax interleaved)
+mm = decode(raw[0, 0])
+sm = decode(raw[0, 1])
+t0 = min(mm[0][1], sm[0][1])
+merged = sorted([(t, "M", c) for c, t in mm] + [(t, "S", c) for c, t in sm])
+n_items = 0
+print("== timeline (first items): time_us role code")
+for t, r, c in merged:
+    if r == "M" and c in (1, 2):
+        n_items += 1
+        if n_items > a.items:
+            break
+    print(f"   {(t - t0) * cyc:9.3f} {r} {c}")
