@@ -17,6 +17,8 @@ SOURCES = ["dyllm.cu", "gemm.cu", "gemm_skinny.cu", "attn.cu", "attn_fused.cu", 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v"]
+# extra nvcc flags for debug builds, e.g. DYLLM_NVCC_FLAGS=-DDYLLM_ATTN_EVENTS=1 (use --force)
+FLAGS += os.environ.get("DYLLM_NVCC_FLAGS", "").split()
 
 
 def _newer(target, deps):

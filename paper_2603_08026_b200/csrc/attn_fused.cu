@@ -10,9 +10,10 @@
 //                dC = P dV (Alg. 4 lines 3-4, dV compact, aligned with idx_in);
 //       output : approximate rows (not in idx_in): the delta dC / l (C_new = C_cache + dC is
 //                formed by the similarity kernel, which reads C_cache anyway — no second read).
-//   type 2 — up to 128 exact rows (idx_in, compact new queries Qx) of s:
-//       pass S : m, l over all N keys;   pass P : P = exp2(s - m), O = P V over all N keys;
-//       output : C = O / l scattered to the exact rows.
+//   type 2 — up to 128 exact rows (idx_in, compact new queries Qx) of s, one pass over the N keys
+//       (online softmax): P = exp2(s - ref) with a per-row reference ref = the first tile's row
+//       max, raised (and the accumulator rescaled in TMEM) only when a later tile's max exceeds it
+//       by more than 2^8; O = P V, l = sum P; output C = O / l scattered to the exact rows.
 // Roles (384 threads, 1 CTA per SM): warp 0 claims items and loads Q (double-buffered), warps 0 and
 // 11 load alternate 128-key K tiles (2-deep ring), warp 10 loads V / dV tiles (2-deep ring) — one
 // 32 KB 3D TMA op per tile, spread over three issuing warps, since TMA issue throughput is per
@@ -35,7 +36,7 @@ constexpr int FA_KVST = 4;                 // unified K / V / dV tile ring, fill
 constexpr int FA_DATA = FA_QST * FA_Q_BYTES + FA_KVST * FA_KV_BYTES;
 // softmax warps: FA_NG column groups x 4 TMEM lane quadrants; each warp owns 32 rows x FA_CW keys
 // of a score tile (and FA_CW head dims of the output)
-constexpr int FA_NG = 4;
+constexpr int FA_NG = 2;
 constexpr int FA_CW = FA_BK / FA_NG;
 constexpr int FA_NSW = 4 * FA_NG;           // softmax warps 2 .. 1 + FA_NSW
 constexpr int FA_WV = 2 + FA_NSW;           // V / dV producer warp
@@ -58,7 +59,6 @@ struct FaParams {
   const uint8_t *rowflag;   // [b*N]: 1 = exact row (type-1 tiles leave it to type 2)
   const bf16 *C_cache;
   bf16 *C_out;
-  unsigned long long *trace;  // optional [grid][32] wait-cycle counters (debug hook)
   int *work_ctr;              // [2] dynamic scheduler: next item, finished CTAs (zero between launches)
   unsigned long long *events; // optional event log of CTAs 0-1 (debug hook): [cta][role][8192]
 };
@@ -148,24 +148,32 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t v[16]) 
       "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
       : "memory");
 }
-__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-// mbar_wait that adds the cycles spent waiting to *acc (debug trace only)
-__device__ __forceinline__ void fa_wait(uint64_t *bar, uint32_t ph, unsigned long long *acc) {
-  if (acc) {
-    const unsigned long long t0 = clock64();
-    mbar_wait(bar, ph);
-    *acc += clock64() - t0;
-  } else {
-    mbar_wait(bar, ph);
-  }
+// 32 lanes x 32 consecutive 32-bit TMEM columns from registers
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t v[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
 }
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void fa_wait(uint64_t *bar, uint32_t ph) { mbar_wait(bar, ph); }
 __device__ __forceinline__ void fa_named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// debug event log: one 8192-entry region per (CTA < 2, role); entry = code << 56 | clock64
+// debug event log (compiled in with -DDYLLM_ATTN_EVENTS=1, tools/attn_events.py): one 8192-entry
+// region per (CTA < 2, role); entry = code << 56 | clock64
+#ifndef DYLLM_ATTN_EVENTS
+#define DYLLM_ATTN_EVENTS 0
+#endif
 constexpr int FA_EV_N = 8192;
 struct FaEv {
+#if DYLLM_ATTN_EVENTS
   unsigned long long *buf = nullptr;
   int n = 0;
   __device__ __forceinline__ void operator()(int code) {
@@ -174,6 +182,12 @@ struct FaEv {
   __device__ __forceinline__ void finish() {
     if (buf && n < FA_EV_N) buf[n] = 0;  // terminator (later launches overwrite the same region)
   }
+  __device__ __forceinline__ void attach(unsigned long long *b) { buf = b; }
+#else
+  __device__ __forceinline__ void operator()(int) {}
+  __device__ __forceinline__ void finish() {}
+  __device__ __forceinline__ void attach(unsigned long long *) {}
+#endif
 };
 
 __global__ void __launch_bounds__(FA_THREADS, 1)
@@ -195,21 +209,15 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   uint64_t *wq_full = bars + 24, *wq_empty = bars + 28;   // [4] work queue (producer -> other roles)
   int4 *wq = reinterpret_cast<int4 *>(bars + 32);          // [4] (item, off, e, -) ; item -1 = done
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wq + 4);
+  int *flg = reinterpret_cast<int *>(bars + 48);           // [2 parities][4 quads][FA_NG] rescale votes
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int NKT = (p.N + FA_BK - 1) / FA_BK;
-  // debug trace: per-role wait cycles (slots 0-2 producers, 3-8 MMA, 9-12 softmax warp 2), 13 total
-  unsigned long long tr[20];
-#pragma unroll
-  for (int i = 0; i < 20; ++i) tr[i] = 0;
-  const bool tron = p.trace != nullptr && lane == 0;
-#define TR(k) (tron ? &tr[k] : nullptr)
-  const unsigned long long t_begin = clock64();
   // event roles: 0 MMA, 1 softmax warp 2, 2 producer warp 0, 3 V producer
   FaEv ev;
   {
     const int role = warp == 1 ? 0 : warp == 2 ? 1 : warp == 0 ? 2 : warp == FA_WV ? 3 : -1;
-    if (p.events && blockIdx.x < 2 && lane == 0 && role >= 0) ev.buf = p.events + (blockIdx.x * 4 + role) * FA_EV_N;
+    if (p.events && blockIdx.x < 2 && lane == 0 && role >= 0) ev.attach(p.events + (blockIdx.x * 4 + role) * FA_EV_N);
   }
 
   if (warp == 0 && lane == 0) {
@@ -251,7 +259,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   int wn = 0;  // queue position of this role
   auto next_item = [&](FaItem &it) -> int {
     const int slot = wn & 3;
-    fa_wait(&wq_full[slot], (wn >> 2) & 1, TR(18));
+    fa_wait(&wq_full[slot], (wn >> 2) & 1);
     const int4 q = wq[slot];
     __syncwarp();
     if (lane == 0) mbar_arrive(&wq_empty[slot]);
@@ -271,7 +279,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       if (g % 3 == pid && lane == 0) {
         const int ks = g % FA_KVST;
         ev(60);
-        fa_wait(&kv_empty[ks], ((g / FA_KVST) & 1) ^ 1, TR(0));
+        fa_wait(&kv_empty[ks], ((g / FA_KVST) & 1) ^ 1);
         ev(61);
         mbar_expect_tx(&kv_full[ks], FA_KV_BYTES);
         tma_load_3d(sKV + ks * FA_KV_BYTES, m, &kv_full[ks], 0, row, kvh * 2);
@@ -306,7 +314,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     };
     auto load_q = [&](const FaItem &it, int qi) {
       const int qb = qi & 1;
-      fa_wait(&q_empty[qb], ((qi >> 1) & 1) ^ 1, TR(1));
+      fa_wait(&q_empty[qb], ((qi >> 1) & 1) ^ 1);
       mbar_expect_tx(&q_full[qb], FA_Q_BYTES);
       tma_load_3d(sQ + qb * FA_Q_BYTES, it.type2 ? &tmQx : &tmQ, &q_full[qb], 0, it.q_row, it.h * 2);
     };
@@ -334,12 +342,17 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         if (w < 0) break;
       }
       const int seq0 = it.s * p.N;
-      // pass S: the N keys
-      for (int kt = 0; kt < NKT; ++kt) {
-        load_kv(&tmK, seq0 + kt * FA_BK, it.kvh);
-        if (kt == 0 && warp == 0 && lane == 0 && wnext >= 0) load_q(fa_item(p, wnext, onext, enext), qi + 1);
+      // Q of the next item is loaded right after this item's first tile is queued
+      auto after_first = [&]() {
+        if (warp == 0 && lane == 0 && wnext >= 0) load_q(fa_item(p, wnext, onext, enext), qi + 1);
+      };
+      // pass S (type 1): the N keys
+      if (!it.type2) {
+        for (int kt = 0; kt < NKT; ++kt) {
+          load_kv(&tmK, seq0 + kt * FA_BK, it.kvh);
+          if (kt == 0) after_first();
+        }
       }
-      ++qi;
       // pass P, in the MMA warp's order: K'(0), then K'(j+1), V'(j) for each j (K' = keys of the P
       // tiles, V' = their values: all keys + V for exact rows, salient keys + dV otherwise)
       if (it.passP) {
@@ -347,11 +360,13 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         const CUtensorMap *mk = it.type2 ? &tmK : &tmKx, *mv = it.type2 ? &tmV : &tmDV;
         const int r0 = it.type2 ? seq0 : it.off;
         load_kv(mk, r0, it.kvh);
+        if (it.type2) after_first();
         for (int j = 0; j < n2; ++j) {
           if (j + 1 < n2) load_kv(mk, r0 + (j + 1) * FA_BK, it.kvh);
           load_kv(mv, r0 + j * FA_BK, it.kvh);
         }
       }
+      ++qi;
     }
   } else if (warp == 1) {
     // ================================================================ MMA issuer: one thread runs
@@ -360,21 +375,18 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     if (lane == 0) {
       constexpr uint32_t id_qk = idesc_bf16_f32(128, FA_BK);
       constexpr uint32_t id_pv = idesc_bf16_f32(128, 128) | (1u << 16);  // B (V) MN-major
-      uint64_t kdesc[FA_KVST], vdesc[FA_KVST], qdesc[FA_QST];
-#pragma unroll
-      for (int i = 0; i < FA_KVST; ++i) {
-        kdesc[i] = sw128_kmajor_desc(smem_u32(sKV + i * FA_KV_BYTES));
-        vdesc[i] = sw128_mn_desc(smem_u32(sKV + i * FA_KV_BYTES), FA_KV_BYTES / 2);
-      }
-#pragma unroll
-      for (int i = 0; i < FA_QST; ++i) qdesc[i] = sw128_kmajor_desc(smem_u32(sQ + i * FA_Q_BYTES));
+      // descriptors of slot 0; slot i is + i * (32 KB >> 4) in the address field
+      const uint64_t kdesc0 = sw128_kmajor_desc(smem_u32(sKV));
+      const uint64_t vdesc0 = sw128_mn_desc(smem_u32(sKV), FA_KV_BYTES / 2);
+      const uint64_t qdesc0 = sw128_kmajor_desc(smem_u32(sQ));
+      constexpr uint64_t kSlot = FA_KV_BYTES >> 4;
       // K-major operand: k-step kk (16 elements) at +32 B within a 64-column half, halves 16 KB apart
       auto koff = [](int kk) -> uint64_t { return static_cast<uint64_t>(((kk >> 2) * (FA_KV_BYTES / 2) + (kk & 3) * 32) >> 4); };
       int qi = 0, g = 0, sc = 0, pc = 0, ai = 0, wn1 = 0;  // g: K/V ring index
       for (;;) {
         // work queue (single-thread form of next_item)
         const int slot = wn1 & 3;
-        fa_wait(&wq_full[slot], (wn1 >> 2) & 1, TR(18));
+        fa_wait(&wq_full[slot], (wn1 >> 2) & 1);
         const int4 q = wq[slot];
         mbar_arrive(&wq_empty[slot]);
         ++wn1;
@@ -382,31 +394,30 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         const FaItem it = fa_item(p, q.x, q.y, q.z);
         ev(it.type2 ? 2 : 1);
         const int qb = qi & 1;
-        fa_wait(&q_full[qb], (qi >> 1) & 1, TR(3));
+        fa_wait(&q_full[qb], (qi >> 1) & 1);
         ++qi;
-        const uint64_t qd = qdesc[qb];
+        const uint64_t qd = qdesc0 + qb * kSlot;
         auto qk = [&]() {
           const int sb = sc & 1;
           ev(10);
-          fa_wait(&s_empty[sb], ((sc >> 1) & 1) ^ 1, TR(4));
+          fa_wait(&s_empty[sb], ((sc >> 1) & 1) ^ 1);
           ev(11);
           const int ks = g % FA_KVST;
-          fa_wait(&kv_full[ks], (g / FA_KVST) & 1, TR(5));
+          fa_wait(&kv_full[ks], (g / FA_KVST) & 1);
           ev(12);
           tc_fence_after();
-          const unsigned long long ti = tron ? clock64() : 0;
-          const uint64_t kd = kdesc[ks];
+          const uint64_t kd = kdesc0 + ks * kSlot;
           const uint32_t dst = tmem + sb * FA_BK;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) umma_bf16(dst, qd + koff(kk), kd + koff(kk), id_qk, kk > 0);
           umma_commit(&kv_empty[ks]);
           umma_commit(&s_full[sb]);
           ev(13);
-          if (tron) tr[19] += clock64() - ti;
           ++g;
           ++sc;
         };
-        for (int kt = 0; kt < NKT; ++kt) qk();
+        if (!it.type2)
+          for (int kt = 0; kt < NKT; ++kt) qk();
         if (it.passP) {
           const int n2 = (it.nkP + FA_BK - 1) / FA_BK;
           qk();
@@ -414,15 +425,14 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             if (j + 1 < n2) qk();
             const int pb = pc & 1;
             ev(20);
-            fa_wait(&p_full[pb], (pc >> 1) & 1, TR(6));
+            fa_wait(&p_full[pb], (pc >> 1) & 1);
             ev(21);
             const int vs = g % FA_KVST;
-            fa_wait(&kv_full[vs], (g / FA_KVST) & 1, TR(7));
-            if (j == 0) fa_wait(acc_empty, (ai & 1) ^ 1, TR(8));
+            fa_wait(&kv_full[vs], (g / FA_KVST) & 1);
+            if (j == 0) fa_wait(acc_empty, (ai & 1) ^ 1);
             ev(22);
             tc_fence_after();
-            const unsigned long long tpv = tron ? clock64() : 0;
-            const uint64_t vd = vdesc[vs];
+            const uint64_t vd = vdesc0 + vs * kSlot;
             const uint32_t pa = tmem + FA_P_COL + pb * 64;
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk)  // 16 keys per MMA: 8 packed TMEM columns of P, 2 KB of V
@@ -432,7 +442,6 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             umma_commit(&p_empty[pb]);
             if (j == n2 - 1) umma_commit(acc_full);
             ev(23);
-            if (tron) tr[17] += clock64() - tpv;
             ++g;
             ++pc;
           }
@@ -461,13 +470,136 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       const int64_t orow = it.type2 ? (rvalid ? p.ex_rows[it.q_row + r] : 0) : static_cast<int64_t>(it.q_row) + r;
       const bool write_row = rvalid && (it.type2 || (it.passP && !p.rowflag[orow]));
       ev(it.type2 ? 2 : 1);
+      float acc[FA_CW];
+      float oscale;
+      if (it.type2) {
+        // ---- exact rows: one pass over the N keys (online softmax, lazy rescale)
+        float ref = -INFINITY, l = 0.f;
+        for (int j = 0; j < NKT; ++j) {
+          const int sb = sc & 1;
+          ev(40);
+          fa_wait(&s_full[sb], (sc >> 1) & 1);
+          ev(41);
+          ++sc;
+          const int pb = pc & 1;
+          ++pc;
+          if (!wact) {  // the whole quad is past the item's rows: keep the barrier protocol only
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[sb]);
+            fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[pb]);
+            continue;
+          }
+          tc_fence_after();
+          float v[FA_CW];
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) tmem_ld32(trow + sb * FA_BK + hh * FA_CW + ch * 32, v + ch * 32);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_empty[sb]);
+          const int k0 = j * FA_BK + hh * FA_CW;
+          if (k0 + FA_CW > p.N) {
+#pragma unroll
+            for (int t = 0; t < FA_CW; ++t)
+              if (k0 + t >= p.N) v[t] = -INFINITY;
+          }
+          float tmax = -INFINITY;
+#pragma unroll
+          for (int t = 0; t < FA_CW; ++t) tmax = fmaxf(tmax, v[t]);
+          if (j == 0) {
+            // the row reference: max over the first tile (all column groups; key 0 is valid)
+            xch[hh * 128 + r].x = tmax;
+            fa_named_sync(1 + quad, 32 * FA_NG);
+#pragma unroll
+            for (int g2 = 0; g2 < FA_NG; ++g2) ref = fmaxf(ref, xch[g2 * 128 + r].x);
+          } else {
+            // raise the reference only when some row of the quad grew by more than 2^8 (P stays
+            // <= 256, exact in bf16/fp32 range): one vote per tile, a rescale is rare
+            const unsigned need = __ballot_sync(0xffffffffu, (tmax - ref) * c > 8.f);
+            int *fv = flg + (j & 1) * 16 + quad * 4;
+            if (lane == 0) fv[hh] = need != 0u;
+            fa_named_sync(1 + quad, 32 * FA_NG);
+            int any = 0;
+#pragma unroll
+            for (int g2 = 0; g2 < FA_NG; ++g2) any |= fv[g2];
+            if (any) {
+              xch[hh * 128 + r].x = tmax;
+              fa_named_sync(1 + quad, 32 * FA_NG);
+              float nref = ref;
+#pragma unroll
+              for (int g2 = 0; g2 < FA_NG; ++g2) nref = fmaxf(nref, xch[g2 * 128 + r].x);
+              fa_named_sync(1 + quad, 32 * FA_NG);
+              const float f = ex2f((ref - nref) * c);
+              l *= f;
+              // the accumulator holds P V of tiles < j: wait for the last of those MMAs, scale
+              fa_wait(&p_empty[(pc - 2) & 1], ((pc - 2) >> 1) & 1);
+              tc_fence_after();
+#pragma unroll 1
+              for (int ch = 0; ch < NCH; ++ch) {
+                uint32_t a32[32];
+                tmem_ld32_issue(trow + FA_ACC_COL + hh * FA_CW + ch * 32, a32);
+                tmem_ld32_wait(a32);
+#pragma unroll
+                for (int t = 0; t < 32; ++t) a32[t] = __float_as_uint(__uint_as_float(a32[t]) * f);
+                tmem_st32(trow + FA_ACC_COL + hh * FA_CW + ch * 32, a32);
+              }
+              tmem_st_wait();
+              ref = nref;
+            }
+          }
+          const float rc = ref * c;
+          // P = exp2((s - ref) c), bf16x2-packed into the P buffer; l sums the fp32 values
+          fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1);
+          tc_fence_after();
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+              const float x0 = v[ch * 32 + 2 * t], x1 = v[ch * 32 + 2 * t + 1];
+              const float p0 = ex2f(fmaf(x0, c, -rc));
+              const float p1 = (t & 1) ? ex2p(fmaf(x1, c, -rc)) : ex2f(fmaf(x1, c, -rc));
+              l += p0 + p1;
+              pk[t] = pack2(p0, p1);
+            }
+            tmem_st16(trow + FA_P_COL + pb * 64 + hh * (FA_CW / 2) + ch * 16, pk);
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[pb]);
+          ev(42);
+        }
+        ev(50);
+        fa_wait(acc_full, ai & 1);
+        ev(51);
+        ++ai;
+        if (wact) {
+          tc_fence_after();
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) tmem_ld32(trow + FA_ACC_COL + hh * FA_CW + ch * 32, acc + ch * 32);
+          tc_fence_before();
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty);
+        // row normaliser: the column groups' sums share the reference (fixed order 0, 1, ...)
+        float L = 0.f;
+        if (wact) {
+          xch[hh * 128 + r].y = l;
+          fa_named_sync(1 + quad, 32 * FA_NG);
+#pragma unroll
+          for (int g2 = 0; g2 < FA_NG; ++g2) L += xch[g2 * 128 + r].y;
+          fa_named_sync(1 + quad, 32 * FA_NG);
+        }
+        oscale = 1.f / L;
+      } else {
       // ---- pass S: running (m, l) of this column group of the row
-      const unsigned long long tS = tron ? clock64() : 0;
       float m = -INFINITY, l = 0.f;
       for (int kt = 0; kt < NKT; ++kt) {
         const int sb = sc & 1;
         ev(30);
-        fa_wait(&s_full[sb], (sc >> 1) & 1, TR(9));
+        fa_wait(&s_full[sb], (sc >> 1) & 1);
         ev(31);
         ++sc;
         if (!wact) {
@@ -476,7 +608,6 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           continue;
         }
         tc_fence_after();
-        const unsigned long long tld = tron ? clock64() : 0;
         float v[FA_CW];
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) tmem_ld32(trow + sb * FA_BK + hh * FA_CW + ch * 32, v + ch * 32);
@@ -484,7 +615,6 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[sb]);
         ev(32);
-        if (tron) tr[17] += clock64() - tld;
         const int k0 = kt * FA_BK + hh * FA_CW;
         if (k0 + FA_CW > p.N) {  // ragged last tile: mask keys >= N
 #pragma unroll
@@ -515,7 +645,6 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         m = mn;
         ev(33);
       }
-      if (tron) tr[14] += clock64() - tS;
       // ---- combine the column groups of each row (fixed order: group 0, 1, ...)
       xch[hh * 128 + r] = make_float2(m, l);
       fa_named_sync(1 + quad, 32 * FA_NG);
@@ -532,14 +661,13 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       const float Mc = M * c;
       const float inv_l = 1.f / Lsum;
       // ---- pass P: P = exp2(s - m) into tensor memory for the P V MMA
-      const unsigned long long tP = tron ? clock64() : 0;
-      float acc[FA_CW];
+      oscale = inv_l;
       if (it.passP) {
         const int n2 = (it.nkP + FA_BK - 1) / FA_BK;
         for (int j = 0; j < n2; ++j) {
           const int sb = sc & 1;
           ev(40);
-          fa_wait(&s_full[sb], (sc >> 1) & 1, TR(10));
+          fa_wait(&s_full[sb], (sc >> 1) & 1);
           ev(41);
           ++sc;
           const int pb = pc & 1;
@@ -547,14 +675,14 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           if (!wact) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_empty[sb]);
-            fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1, TR(11));
+            fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1);
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_full[pb]);
             continue;
           }
           // P = exp2(s - m) for this group's FA_CW keys, bf16x2-packed into the P TMEM buffer
           // (FA_CW / 2 columns per group); the S buffer is released once all chunks are read
-          fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1, TR(11));
+          fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1);
           tc_fence_after();
 #pragma unroll
           for (int ch = 0; ch < NCH; ++ch) {
@@ -581,7 +709,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           ev(42);
         }
         ev(50);
-        fa_wait(acc_full, ai & 1, TR(12));
+        fa_wait(acc_full, ai & 1);
         ev(51);
         ++ai;
         if (wact) {
@@ -593,8 +721,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty);
       }
-      if (tron) tr[15] += clock64() - tP;
-      const unsigned long long tE = tron ? clock64() : 0;
+      }  // type 1
       // ---- epilogue: this thread's row, head columns [hh*FA_CW, (hh+1)*FA_CW). Exact rows
       // (type 2): C = O / l. Approximate rows (type 1): the delta dC / l only; the similarity
       // kernel, which reads C_cache anyway, forms C_new = C_cache + dC (no C_cache read here).
@@ -604,33 +731,13 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         for (int u = 0; u < FA_CW / 8; ++u) {
           float o[8];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) o[t] = acc[u * 8 + t] * inv_l;
+          for (int t = 0; t < 8; ++t) o[t] = acc[u * 8 + t] * oscale;
           dst[u] = pack8(o);
         }
       }
       ev(52);
-      if (tron) tr[16] += clock64() - tE;
     }
   }
-  if (tron && (warp <= 2 || warp == FA_WV)) {
-    const int lo = warp == 0 ? 0 : warp == FA_WV ? 2 : warp == 1 ? 3 : 9;
-    const int hi = warp == 0 ? 2 : warp == FA_WV ? 3 : warp == 1 ? 9 : 13;
-    for (int i = lo; i < hi; ++i) p.trace[blockIdx.x * 32 + i] = tr[i];
-    if (warp == 2) {
-      p.trace[blockIdx.x * 32 + 13] = clock64() - t_begin;
-      for (int i = 14; i < 17; ++i) p.trace[blockIdx.x * 32 + i] = tr[i];
-      p.trace[blockIdx.x * 32 + 17] = tr[18];  // softmax next_item wait
-      p.trace[blockIdx.x * 32 + 22] = tr[17];  // softmax pass-S TMEM load time
-    }
-    if (warp == 1) {
-      p.trace[blockIdx.x * 32 + 18] = tr[18];  // MMA next_item wait
-      p.trace[blockIdx.x * 32 + 19] = tr[19];  // MMA QK issue time
-      p.trace[blockIdx.x * 32 + 20] = clock64() - t_begin;
-      p.trace[blockIdx.x * 32 + 21] = tr[17];  // MMA P.V issue time
-      p.trace[blockIdx.x * 32 + 23] = tr[16];  // MMA fence time before QK issue
-    }
-  }
-#undef TR
   ev.finish();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -681,7 +788,6 @@ int attention_fused_launch(const AttnArgs &a, cudaStream_t st) {
   p.rowflag = a.rowflag;
   p.C_cache = a.C_cache;
   p.C_out = a.C_out;
-  p.trace = g_attn_trace;
   p.events = g_attn_events;
   p.work_ctr = a.work_ctr;
   if (!p.work_ctr) {

@@ -384,13 +384,19 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
       constexpr int U = 4;  // 2*U independent 16-byte loads in flight per lane
       for (int c0 = lane; c0 < nv; c0 += 32 * U) {
         uint4 ua[U], ub[U];
+        // both rows are loaded unconditionally (no dependence on the row-kind loads above); an
+        // approximate row of a sequence without salient keys then takes C_cache
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int c = c0 + u * 32;
           if (c < nv) {
             ub[u] = b[c];
-            ua[u] = (take_new || add) ? ld_nc_v4(a + c) : ub[u];
+            ua[u] = ld_nc_v4(a + c);
           }
+        }
+        if (!take_new && !add) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) ua[u] = ub[u];
         }
         if (add) {
 #pragma unroll
@@ -480,10 +486,20 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
           for (int i = lane; i < 256; i += 32) hist[warp][i] = 0;
           __syncwarp();
           if (in_regs) {
+            // similarities cluster in a few top-byte bins: lanes with equal digits are merged
+            // (match.any) so each bin takes one shared-memory atomic per instruction instead of
+            // up to 32 serialised ones
 #pragma unroll
             for (int j = 0; j < kRegRows; ++j) {
+              if (j * 32 >= L) break;
               const uint32_t key = key_of(sreg[j]);
-              if (j * 32 + lane < L && (key & pmask) == prefix) atomicAdd(&hist[warp][(key >> shift) & 255u], 1u);
+              const bool in = j * 32 + lane < L && (key & pmask) == prefix;
+              const unsigned act = __ballot_sync(0xffffffffu, in);
+              if (in) {
+                const uint32_t dig = (key >> shift) & 255u;
+                const unsigned same = __match_any_sync(act, dig);
+                if (lane == __ffs(same) - 1) atomicAdd(&hist[warp][dig], static_cast<unsigned>(__popc(same)));
+              }
             }
           } else {
             for (int i = lane; i < L; i += 32) {

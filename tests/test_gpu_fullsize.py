@@ -38,23 +38,34 @@ CHECK_SEQS = (0, 7, 15)
 STD = {"cK": 1.25, "cQ": 1.5, "cV": 1.25, "cC": 0.1, "cH": 1.0, "cX": 1.0}
 
 
-@pytest.fixture(scope="module")
-def big():
+def _make(name):
     from paper_2603_08026_b200 import dyllm as dy
-    cfg, run = configs.preset("llada8b")
+    cfg, run = configs.preset(name)
     cfg = replace(cfg, n_layers=1, vocab=1024, mask_id=1023)    # layer_step never reads the vocab
     run = replace(run, select_mode=1)
     b, N, d = run.batch, run.N, cfg.d_model
     ctx = dy.Context(0)
     w = dy.Weights.random(ctx, cfg, seed=SEED)                  # on-device IH4 (same streams)
     W = gen.layer_weights(cfg, SEED, 0)                         # oracle copy, fp64
-    host = {k: gen.cache_tensor(SEED, 0, k, b, N, d, s) for k, s in STD.items()}
+    qw, kw = cfg.q_width, cfg.kv_width
+    width = {"cK": kw, "cV": kw, "cQ": qw, "cC": qw, "cH": d, "cX": d}
+    host = {k: gen.cache_tensor(SEED, 0, k, b, N, width[k], s) for k, s in STD.items()}
     # cached contexts with row norms spread over 2^0 .. 2^-4 (exact in bf16), so that the
     # similarity of approximate rows (~ cos of C_cache vs C_cache + dC) spreads over (0, 1]
     # instead of piling up within the 1e-3 exclusion band around tau
     k = np.random.default_rng(SEED).integers(0, 5, size=(b, N, 1))
     host["cC"] *= np.ldexp(np.float32(1.0), -k).astype(np.float32)
     return dy, ctx, cfg, run, w, W, host
+
+
+@pytest.fixture(scope="module")
+def big():
+    return _make("llada8b")
+
+
+@pytest.fixture(scope="module")
+def big_dream():
+    return _make("dream7b")
 
 
 def _upload(dy, ctx, cache, host):
@@ -69,7 +80,17 @@ def _upload(dy, ctx, cache, host):
 
 
 @pytest.mark.parametrize("mode,frac_in", [("ro", 0.06), ("ro", 0.10), ("fi", 0.06)])
-def test_layer_step_full_size_sampled(big, mode, frac_in, frac=0.10):
+def test_layer_step_full_size_sampled(big, mode, frac_in):
+    _check_full_size(big, mode, frac_in)
+
+
+@pytest.mark.parametrize("mode,frac_in", [("ro", 0.06), ("fi", 0.06)])
+def test_layer_step_full_size_sampled_dream(big_dream, mode, frac_in):
+    """Dream-7B layer shape (GQA 28 q / 4 kv heads, QKV bias, FFN 18944), L_P 160 + L_R 512."""
+    _check_full_size(big_dream, mode, frac_in)
+
+
+def _check_full_size(big, mode, frac_in, frac=0.10):
     dy, ctx, cfg, run, w, W, host = big
     b, N = run.batch, run.N
     row_lo = 0 if mode == "fi" else run.L_P

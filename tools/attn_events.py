@@ -1,6 +1,7 @@
 """Event timeline of the fused attention kernel (debug hook, dyllm_debug_trace_buffer which = 2):
 per-role event logs of CTAs 0-1 for the last layer of one denoising step of the bench workload.
 
+    DYLLM_NVCC_FLAGS=-DDYLLM_ATTN_EVENTS=1 python -m paper_2603_08026_b200.build --force
     python tools/attn_events.py --mode ro|fi|full [--items 3]
 
 Codes: MMA 1/2 item (type 1/2), 10 QK begin, 11 S buffer free, 12 K tile ready, 13 QK issued,
