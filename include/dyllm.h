@@ -209,7 +209,9 @@ uint64_t dyllm_launch_count(void);
  * up to fp32 summation order. */
 /* DYLLM_OPT_ATTN_FUSED (default 1): head_dim 128 uses the fused tcgen05 attention kernel
  * (attn_fused.cu); 0 = the two-kernel path (tcgen05 row statistics + mma.sync P.V). */
-enum { DYLLM_OPT_SKINNY_GEMM = 1, DYLLM_OPT_SKINNY_SPLIT = 2, DYLLM_OPT_ATTN_FUSED = 3 };
+/* DYLLM_OPT_SKINNY_ONE_CHUNK (default -1 = automatic): largest device row count the skinny kernel
+ * keeps in a single activation chunk (above it: chunks of <= 256 rows). */
+enum { DYLLM_OPT_SKINNY_GEMM = 1, DYLLM_OPT_SKINNY_SPLIT = 2, DYLLM_OPT_ATTN_FUSED = 3, DYLLM_OPT_SKINNY_ONE_CHUNK = 4 };
 int dyllm_set_option(int option, int value);
 
 /* Debug hook: when d_buf != NULL, kernels of family `which` (0 = skinny GEMM) write %globaltimer

@@ -33,12 +33,18 @@
 
 namespace dy {
 
-constexpr int SK_STAGES = 4;
-constexpr int SK_W_BYTES = 128 * 128;        // 128 weight rows x 64 bf16
-constexpr int SK_A_BYTES = 128 * 128;        // 128 activation rows x 64 bf16 (per MMA half)
+// A k-block is 128 columns: every operand box is one 3-D TMA op {64 columns, rows, 2 chunks}
+// (32 KB for 128 rows), laid out [chunk][rows][64] in shared memory — twice the bytes per TMA
+// op of 2-D 64-column boxes, which is what the per-SM L2 -> SM ingest rate depends on
+// (tools/tma_probe.cu: 16 KB ops ~44-53 GB/s/SM, 32 KB ops ~71-82 GB/s/SM from L2).
+constexpr int SK_KB = 128;                   // k-block width (elements)
+
+constexpr int SK_STAGES = 2;
+constexpr int SK_W_BYTES = 128 * 256;        // 128 weight rows x 128 bf16
+constexpr int SK_A_BYTES = 128 * 256;        // <= 128 activation rows x 128 bf16 (per MMA half)
 constexpr int SK_STAGE = SK_W_BYTES + 2 * SK_A_BYTES;
 constexpr int SK_XCH = 2 * 32 * 128 * 4;     // epilogue transpose tiles: one [32 rows][128 weight rows] fp32 per half
-constexpr int SK_RING = SK_STAGES * SK_STAGE;  // 192 KB: 4 stages of 48 KB (M in (256, 512]) or 6 of 32 KB
+constexpr int SK_RING = SK_STAGES * SK_STAGE;  // 192 KB: 2 stages of 96 KB (M in (256, 512]) or 3 of 64 KB
 constexpr int SK_MAX_STAGES = SK_RING / (SK_W_BYTES + SK_A_BYTES);
 constexpr int SK_SMEM = 1024 + SK_RING + SK_XCH + 256;
 constexpr int SK_THREADS = 352;              // W producer, MMA, 8 epilogue warps, A producer
@@ -112,6 +118,8 @@ struct SkinnyParams {
   int P_max;   // co-resident pairs of the grid (the partition uses P <= P_max of them)
   unsigned long long *trace;  // optional [grid][16] globaltimer stamps (debug hook)
   int S_force; // test hook: split units per tile (0 = automatic)
+  int one_chunk_max;  // largest M kept in ONE activation chunk (two MMAs per k-step above 256
+                      // rows, single-buffered accumulator); above: chunks of <= 256 rows
 };
 
 // Stream-K partition of the (item, k-block) space: pair p owns units [start(p), start(p+1)).
@@ -161,11 +169,32 @@ struct SkIter {
   }
 };
 
+// tensor maps: weights (box 128 rows) and activations (box 16 * (i + 1) rows, i = 0..7: one op
+// loads exactly a CTA's half of the activation rows of an MMA, whatever the device-side M)
+struct SkMaps {
+  CUtensorMap w;
+  CUtensorMap a[8];
+};
+
+__device__ __forceinline__ void tma_load_3d_pair(void *smem_dst, const void *tmap, uint64_t *bar, int c0, int c1,
+                                                 int c2) {
+  const uint32_t leader_bar = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_l2_3d(const void *tmap, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+
 template <int EPI>
 __global__ void __launch_bounds__(SK_THREADS, 1)
-    gemm_skinny_kernel(const __grid_constant__ CUtensorMap tmA128, const __grid_constant__ CUtensorMap tmA64,
-                       const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CUtensorMap tmA16,
-                       const __grid_constant__ CUtensorMap tmW, const SkinnyParams p) {
+    gemm_skinny_kernel(const __grid_constant__ SkMaps maps, const SkinnyParams p) {
   const int M = p.M_ptr ? min(*p.M_ptr, p.M_cap) : p.M_cap;
   if (M <= 0 || M > SKINNY_MAX_M) return;  // uniform across the grid
   extern __shared__ uint8_t smem_raw[];
@@ -185,10 +214,17 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   // rows (two MMAs per k-step when M > 256, single-buffered accumulator); M > 512: ceil(M/256)
   // equal chunks of R <= 256 rows (double-buffered accumulator). Chunks of one weight block are
   // adjacent in tile order, so the pairs working on them at the same time share it through L2.
-  const int nchunk = M <= 512 ? 1 : (M + 255) / 256;
+  // M in (256, 512]: one chunk (two MMAs per k-step, single-buffered accumulator, 2-stage ring)
+  // only when that fills the pairs in one round and two chunks would need two rounds
+  // (P/2 <= weight blocks < P: the QKV projection); otherwise chunks of <= 256 rows pipeline
+  // better (double-buffered accumulator, 3-stage ring). Measured: tools/gemm_bench.py --one-chunk.
+  const int nwb = p.N / 256;
+  const bool one = p.one_chunk_max >= 0 ? M <= p.one_chunk_max
+                                        : (M <= 256 || (M <= 512 && 2 * nwb >= p.P_max && nwb < p.P_max));
+  const int nchunk = one ? 1 : (M + 255) / 256;
   const int R = nchunk == 1 ? M : (((M + nchunk - 1) / nchunk + 31) & ~31);
   const int items = p.N / 256 * nchunk;
-  const int num_kb = p.K / 64;
+  const int num_kb = p.K / SK_KB;
   // split granularity (stream-K units per tile), from the device-side M: tiles are cut into
   // S units when there are fewer tiles than pairs (S = pairs / tiles), so all pairs stream
   int upi = p.S_force > 0 ? p.S_force : max(1, p.P_max / items);
@@ -202,9 +238,9 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   const int NA1 = (nchunk == 1 && M > 256) ? ((M - 256 + 31) & ~31) : 0;
   // M <= 256: two 256-column TMEM accumulators (epilogue of segment i overlaps the MMAs of i+1)
   const int nbuf = NA1 ? 1 : 2;
-  const uint32_t stage_tx = 2u * (SK_W_BYTES + (NA0 / 2 + NA1 / 2) * 128);
-  // ring: a stage holds 16 KB of weights + one (or, for M in (256, 512], two) 16 KB activation
-  // slots; with one slot the same 192 KB hold 6 stages instead of 4
+  const uint32_t stage_tx = 2u * (SK_W_BYTES + (NA0 / 2 + NA1 / 2) * 256);
+  // ring: a stage holds 32 KB of weights + one (or, for M in (256, 512], two) 32 KB activation
+  // slots; with one slot the same 192 KB hold 3 stages instead of 2
   const int stage_bytes = NA1 ? SK_STAGE : SK_W_BYTES + SK_A_BYTES;
   const int nstages = SK_RING / stage_bytes;
   // Unsplit tiles (upi == 1) are dealt round-robin (pair p: tiles p, p + P, ...), so the pairs
@@ -215,11 +251,9 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
                                    upi, kpu, 0};
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA128);
-    tma_prefetch_desc(&tmA64);
-    tma_prefetch_desc(&tmA32);
-    tma_prefetch_desc(&tmA16);
-    tma_prefetch_desc(&tmW);
+    tma_prefetch_desc(&maps.w);
+    tma_prefetch_desc(&maps.a[NA0 / 32 - 1]);
+    if (NA1) tma_prefetch_desc(&maps.a[NA1 / 32 - 1]);
     for (int s = 0; s < SK_MAX_STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -262,7 +296,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             pkb = ps.kb0;
           }
           if (ps.item % nchunk == 0)
-            tma_prefetch_l2_2d(&tmW, pkb * 64, ps.item / nchunk * 256 + static_cast<int>(rank) * 128);
+            tma_prefetch_l2_3d(&maps.w, 0, ps.item / nchunk * 256 + static_cast<int>(rank) * 128, pkb * 2);
           ++pkb;
           ++n_pf;
         }
@@ -276,25 +310,16 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           uint8_t *sb = stages + st * stage_bytes;
           if (wprod) {
             if (rank == 0) mbar_expect_tx(&full[st], stage_tx);
-            tma_load_2d_pair(sb, &tmW, &full[st], kb * 64, wrow);
+            tma_load_3d_pair(sb, &maps.w, &full[st], 0, wrow, kb * 2);
             ++n_ld;
             prefetch_ahead();
           } else {
-            // this CTA's half of each activation block, in boxes of 128/64/32/16 rows (only the
-            // rows the MMA reads; 16-row offsets keep the 128B-swizzle atoms aligned)
-            auto load_rows = [&](uint8_t *dst, int r0, int n) {
-              const CUtensorMap *maps[4] = {&tmA128, &tmA64, &tmA32, &tmA16};
-              int off = 0;
-              for (int bi = 0; bi < 4; ++bi) {
-                const int box = 128 >> bi;
-                while (n - off >= box) {
-                  tma_load_2d_pair(dst + off * 128, maps[bi], &full[st], kb * 64, r0 + off);
-                  off += box;
-                }
-              }
-            };
-            load_rows(sb + SK_W_BYTES, arow + static_cast<int>(rank) * (NA0 / 2), NA0 / 2);
-            if (NA1) load_rows(sb + SK_W_BYTES + SK_A_BYTES, 256 + static_cast<int>(rank) * (NA1 / 2), NA1 / 2);
+            // this CTA's half of the activation rows of each MMA: one op of exactly that many rows
+            tma_load_3d_pair(sb + SK_W_BYTES, &maps.a[NA0 / 32 - 1], &full[st], 0,
+                             arow + static_cast<int>(rank) * (NA0 / 2), kb * 2);
+            if (NA1)
+              tma_load_3d_pair(sb + SK_W_BYTES + SK_A_BYTES, &maps.a[NA1 / 32 - 1], &full[st], 0,
+                               256 + static_cast<int>(rank) * (NA1 / 2), kb * 2);
           }
           if (++st == nstages) {
             st = 0;
@@ -327,13 +352,16 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             const uint32_t w0 = smem_u32(stages + st * stage_bytes);
             const uint32_t a0 = w0 + SK_W_BYTES;
             const uint32_t first = (kb == sg.kb0) ? 1u : 0u;
+            // k-step kk: 64-column chunk kk / 4 (chunk stride = box rows x 128 B), +32 B per 16
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint32_t accum = (first && k == 0) ? 0u : 1u;
-              umma_bf16_pair(acc, sw128_kmajor_desc(w0 + k * 32), sw128_kmajor_desc(a0 + k * 32), id0, accum);
+            for (int kk = 0; kk < 8; ++kk) {
+              const uint32_t accum = (first && kk == 0) ? 0u : 1u;
+              const uint32_t ko = (kk & 3) * 32, ch = kk >> 2;
+              umma_bf16_pair(acc, sw128_kmajor_desc(w0 + ch * (128 * 128) + ko),
+                             sw128_kmajor_desc(a0 + ch * (NA0 / 2 * 128) + ko), id0, accum);
               if (NA1)
-                umma_bf16_pair(acc + 256, sw128_kmajor_desc(w0 + k * 32),
-                               sw128_kmajor_desc(a0 + SK_A_BYTES + k * 32), id1, accum);
+                umma_bf16_pair(acc + 256, sw128_kmajor_desc(w0 + ch * (128 * 128) + ko),
+                               sw128_kmajor_desc(a0 + SK_A_BYTES + ch * (NA1 / 2 * 128) + ko), id1, accum);
             }
             umma_commit_pair(&empty[st]);
             if (kb == sg.kb1 - 1) umma_commit_pair(&tfull[b]);
@@ -601,27 +629,31 @@ static int launch_skinny_t(const GemmCall &g, int num_sms, cudaStream_t st) {
     set_error("skinny gemm: missing split-K workspace or counters");
     return DYLLM_E_ARG;
   }
-  CUtensorMap ta[4], tw;
-  for (int bi = 0; bi < 4; ++bi) {
-    int rc = make_tmap(&ta[bi], g.A, g.M_cap, g.K, 128 >> bi);
+  SkMaps maps;
+  for (int i = 0; i < 8; ++i) {
+    // boxes taller than the (16-rounded) capacity are never selected: clamp them to stay encodable
+    const int cap16 = (g.M_cap + 15) / 16 * 16;
+    const int box = 16 * (i + 1) < cap16 ? 16 * (i + 1) : cap16;
+    int rc = make_tmap3(&maps.a[i], g.A, g.M_cap, g.K, box, 2);
     if (rc) return rc;
   }
-  int rc = make_tmap(&tw, g.W, g.N, g.K, 128);
+  int rc = make_tmap3(&maps.w, g.W, g.N, g.K, 128, 2);
   if (rc) return rc;
   // the tile count (hence the split and the number of pairs used) depends on the device-side row
   // count: the kernel derives them; the grid is every co-resident pair
   SkinnyParams p{g.M_ptr, g.M_cap, g.N, g.K, g.D, g.ldd, g.resid, g.ldr, g.resid_rows, g.bias, g.ws, g.ctr, max_pairs,
-                 g_skinny_trace, g_skinny_split};
+                 g_skinny_trace, g_skinny_split, g_skinny_one_chunk};
   cfg.gridDim = dim3(2 * max_pairs);
-  DY_CUDA(cudaLaunchKernelEx(&cfg, kern, ta[0], ta[1], ta[2], ta[3], tw, p));
+  DY_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, p));
   return DYLLM_OK;
 }
 
 unsigned long long *g_skinny_trace = nullptr;
 int g_skinny_split = 0;
+int g_skinny_one_chunk = -1;  // -1: automatic
 
 bool skinny_eligible(const GemmCall &g) {
-  return g.N % 256 == 0 && g.K % 64 == 0 && (g.epi == EPI_BF16 || g.epi == EPI_RESID || g.epi == EPI_SWIGLU);
+  return g.N % 256 == 0 && g.K % SK_KB == 0 && (g.epi == EPI_BF16 || g.epi == EPI_RESID || g.epi == EPI_SWIGLU);
 }
 
 int gemm_skinny_launch(const GemmCall &g, int num_sms, cudaStream_t st) {

@@ -63,7 +63,8 @@ constexpr int kSkinnyCtrCap = 4096;  // 2 counters per skinny tile (weight block
 inline int64_t skinny_ws_floats(int num_sms) { return static_cast<int64_t>(num_sms) * 512 * 256; }
 extern bool g_skinny_enabled;  // test hook (dyllm_set_option)
 extern unsigned long long *g_skinny_trace;
-extern int g_skinny_split;  // test hook: units per weight block (0 = auto)  // debug hook (dyllm_debug_trace_buffer)
+extern int g_skinny_split;
+extern int g_skinny_one_chunk;  // test hook: largest M in one activation chunk (dyllm_set_option)  // test hook: units per weight block (0 = auto)  // debug hook (dyllm_debug_trace_buffer)
 int gemm_skinny_launch(const GemmCall &g, int num_sms, cudaStream_t st);  // gemm_skinny.cu
 
 // ------------------------------------------------------------------ kernels (kernels.cu)

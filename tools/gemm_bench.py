@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--skinny", type=int, default=1)
     ap.add_argument("--split", default="0", help="comma list of skinny split granularities (0 = auto)")
     ap.add_argument("--which", default="qkv,o,gu,down")
+    ap.add_argument("--one-chunk", type=int, default=-1, help="largest M in one activation chunk (-1 auto)")
     a = ap.parse_args()
     cfg, _ = configs.preset(a.config)
     d, F = cfg.d_model, cfg.d_ff
@@ -35,6 +36,7 @@ def main():
     shapes = {"qkv": (qw + 2 * kw, d), "o": (d, qw), "gu": (2 * F, d), "down": (d, F)}
     ctx = dy.Context(0)
     dy.set_option(dy.OPT_SKINNY_GEMM, a.skinny)
+    dy.set_option(dy.OPT_SKINNY_ONE_CHUNK, a.one_chunk)
     cap = 2048
     for name, (N, K) in shapes.items():
         if name not in a.which.split(","):
