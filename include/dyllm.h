@@ -211,7 +211,10 @@ uint64_t dyllm_launch_count(void);
  * (attn_fused.cu); 0 = the two-kernel path (tcgen05 row statistics + mma.sync P.V). */
 /* DYLLM_OPT_SKINNY_ONE_CHUNK (default -1 = automatic): largest device row count the skinny kernel
  * keeps in a single activation chunk (above it: chunks of <= 256 rows). */
-enum { DYLLM_OPT_SKINNY_GEMM = 1, DYLLM_OPT_SKINNY_SPLIT = 2, DYLLM_OPT_ATTN_FUSED = 3, DYLLM_OPT_SKINNY_ONE_CHUNK = 4 };
+/* DYLLM_OPT_PDL (default 1): launch every kernel with programmatic dependent launch (a kernel's
+ * setup overlaps its predecessor; each kernel waits for its predecessor before touching memory). */
+enum { DYLLM_OPT_SKINNY_GEMM = 1, DYLLM_OPT_SKINNY_SPLIT = 2, DYLLM_OPT_ATTN_FUSED = 3, DYLLM_OPT_SKINNY_ONE_CHUNK = 4,
+       DYLLM_OPT_PDL = 5 };
 int dyllm_set_option(int option, int value);
 
 /* Debug hook: when d_buf != NULL, kernels of family `which` (0 = skinny GEMM) write %globaltimer

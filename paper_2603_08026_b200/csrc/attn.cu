@@ -128,6 +128,7 @@ __device__ __forceinline__ void pv_tile(float O[HD / 8][4], const float P[8][4],
 
 template <int HD>
 __global__ void __launch_bounds__(128) attn_kernel(const AttnArgs a) {
+  pdl_wait();
   constexpr int LD = AttnSmem<HD>::LD;
   extern __shared__ __align__(16) uint8_t attn_smem[];
   bf16 *sQ = reinterpret_cast<bf16 *>(attn_smem);
@@ -320,6 +321,7 @@ template <int HD>
 __global__ void __launch_bounds__(192, 1)
     attn_stats_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                       const StatsParams p) {
+  pdl_wait();
   constexpr int KB = HD / 64;
   constexpr int Q_KB_BYTES = 128 * 128;     // 128 rows x 64 bf16
   constexpr int K_BYTES = ST_BN * 128;      // 256 keys x 64 bf16
@@ -469,6 +471,7 @@ __global__ void __launch_bounds__(192, 1)
 //   approx CTAs : rows input \ idx_in, keys = idx_in, O = P dV, C = C_cache + O   (Alg. 4 lines 3-4)
 template <int HD>
 __global__ void __launch_bounds__(128) attn_pv_kernel(const AttnArgs a) {
+  pdl_wait();
   constexpr int LD = AttnSmem<HD>::LD;
   extern __shared__ __align__(16) uint8_t attn_smem[];
   bf16 *sQ = reinterpret_cast<bf16 *>(attn_smem);
@@ -601,7 +604,7 @@ static int launch_fused(const AttnArgs &a, cudaStream_t st) {
   const int T = (a.max_rows_per_seq + BQ - 1) / BQ;
   if (T <= 0) return DYLLM_OK;
   dim3 grid(2 * T, a.H, a.batch);
-  attn_kernel<HD><<<grid, 128, smem, st>>>(a);
+  DY_CUDA(launch_k(attn_kernel<HD>, dim3(grid), dim3(128), smem, st, 1, a));
   DY_CUDA(cudaGetLastError());
   return DYLLM_OK;
 }
@@ -635,12 +638,12 @@ static int launch_split(const AttnArgs &a, cudaStream_t st) {
   p.sl2 = a.scale * 1.4426950408889634f;
   p.stats = a.stats;
   const int grid = p.items < a.num_sms ? p.items : a.num_sms;
-  attn_stats_kernel<HD><<<grid, 192, smem_stats, st>>>(tq, tk, p);
+  DY_CUDA(launch_k(attn_stats_kernel<HD>, dim3(grid), dim3(192), smem_stats, st, 1, tq, tk, p));
   DY_CUDA(cudaGetLastError());
   // 2) P.V for exact rows (all keys) and approximate rows (salient keys)
   const int T = (a.max_rows_per_seq + BQ - 1) / BQ;
   dim3 g2(2 * T, a.H, a.batch);
-  attn_pv_kernel<HD><<<g2, 128, AttnSmem<HD>::BYTES, st>>>(a);
+  DY_CUDA(launch_k(attn_pv_kernel<HD>, dim3(g2), dim3(128), AttnSmem<HD>::BYTES, st, 1, a));
   DY_CUDA(cudaGetLastError());
   return DYLLM_OK;
 }

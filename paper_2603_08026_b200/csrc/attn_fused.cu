@@ -252,6 +252,8 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();  // grid <= #SMs at one CTA per SM: resident, the next kernel may launch
   // Dynamic scheduling: the producer thread claims items with an atomic counter (items of one
   // (sequence, kv head) stay adjacent in claim order, so concurrently running CTAs share K/V in L2,
   // and heavy exact-row items no longer pile up on fixed CTAs) and passes them to the other roles
@@ -796,7 +798,7 @@ int attention_fused_launch(const AttnArgs &a, cudaStream_t st) {
   }
   if (p.items <= 0) return DYLLM_OK;
   const int grid = p.items < a.num_sms ? p.items : a.num_sms;
-  attn_fused_kernel<<<grid, FA_THREADS, FA_SMEM, st>>>(tq, tqx, tk, tv, tkx, tdv, p);
+  DY_CUDA(launch_k(attn_fused_kernel, dim3(grid), dim3(FA_THREADS), FA_SMEM, st, 1, tq, tqx, tk, tv, tkx, tdv, p));
   DY_CUDA(cudaGetLastError());
   return DYLLM_OK;
 }

@@ -60,6 +60,14 @@ __device__ __forceinline__ int warp_sum_i(int v) {
   return v;
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// Every kernel is launched with programmatic stream serialisation (launch_k): it may start while the
+// previous kernel of the stream is still running, so it waits (griddepcontrol.wait: for the
+// previous grid's completion and memory) before its first global memory access. Kernels whose
+// whole grid is resident (the persistent GEMM / attention kernels) release their successor early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ------------------------------------------------------------------ PTX: smem / mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -789,6 +789,11 @@ int dyllm_set_option(int option, int value) {
     g_skinny_one_chunk = value < 0 ? 0 : value;
     return prev;
   }
+  if (option == DYLLM_OPT_PDL) {
+    const int prev = g_pdl_enabled ? 1 : 0;
+    g_pdl_enabled = value != 0;
+    return prev;
+  }
   if (option == DYLLM_OPT_SKINNY_SPLIT) {
     const int prev = g_skinny_split;
     g_skinny_split = value < 0 ? 0 : value;

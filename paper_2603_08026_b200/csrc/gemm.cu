@@ -81,13 +81,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
 
-  const int M = p.M_ptr ? min(*p.M_ptr, p.M_cap) : p.M_cap;
-  const int num_m = (M + BM - 1) / BM;
-  const int num_n = (p.N + BN - 1) / BN;
-  const int total = (M <= p.m_skip_le) ? 0 : num_m * num_n;  // small M: the skinny kernel runs
-  const int num_kb = p.K / BK;
-  if (total == 0) return;  // uniform: the skinny kernel owns this row count (or M == 0)
-
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -106,6 +99,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // setup above overlaps the previous kernel; the whole grid is resident (grid <= #SMs, one CTA
+  // per SM), so the next kernel may be released now
+  pdl_wait();
+  pdl_trigger();
+
+  const int M = p.M_ptr ? min(*p.M_ptr, p.M_cap) : p.M_cap;
+  const int num_m = (M + BM - 1) / BM;
+  const int num_n = (p.N + BN - 1) / BN;
+  const int total = (M <= p.m_skip_le) ? 0 : num_m * num_n;  // small M: the skinny kernel runs
+  const int num_kb = p.K / BK;
 
   if (warp == 0) {
     // ===================== TMA producer
@@ -351,7 +354,7 @@ static int launch_t(const GemmCall &g, int num_sms, cudaStream_t st) {
   GemmParams p{g.M_ptr, g.M_cap, g.N, g.K, g.D, g.ldd, g.resid, g.ldr, g.resid_rows, g.bias, g.partials, g.m_skip_le};
   const int max_tiles = ((g.M_cap + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   const int grid = max_tiles < num_sms ? max_tiles : num_sms;
-  kern<<<grid, kGemmThreads, C::SMEM_BYTES, st>>>(ta, tb, p);
+  DY_CUDA(launch_k(kern, dim3(grid), dim3(kGemmThreads), C::SMEM_BYTES, st, 1, ta, tb, p));
   DY_CUDA(cudaGetLastError());
   return DYLLM_OK;
 }
@@ -396,5 +399,6 @@ int gemm_launch(const GemmCall &g, int num_sms, cudaStream_t st) {
 }
 
 bool g_skinny_enabled = true;
+bool g_pdl_enabled = true;
 
 }  // namespace dy

@@ -195,8 +195,6 @@ __device__ __forceinline__ void tma_prefetch_l2_3d(const void *tmap, int c0, int
 template <int EPI>
 __global__ void __launch_bounds__(SK_THREADS, 1)
     gemm_skinny_kernel(const __grid_constant__ SkMaps maps, const SkinnyParams p) {
-  const int M = p.M_ptr ? min(*p.M_ptr, p.M_cap) : p.M_cap;
-  if (M <= 0 || M > SKINNY_MAX_M) return;  // uniform across the grid
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t *stages = smem;
@@ -210,6 +208,36 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1;
+  // setup (independent of the device row count) overlaps the previous kernel of the stream
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&maps.w);
+    for (int s = 0; s < SK_MAX_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 2 * 8);  // one arrival per epilogue warp of both CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();  // the grid is co-resident (occupancy-sized): the next kernel may launch
+  const int M = p.M_ptr ? min(*p.M_ptr, p.M_cap) : p.M_cap;
+  if (M <= 0 || M > SKINNY_MAX_M) {  // uniform across the grid: nothing to do
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 1) {
+      tc_fence_after();
+      tmem_dealloc_pair(tmem_base, 512);
+    }
+    return;
+  }
   // Tiles ("items") = (256-row weight block, activation chunk). M <= 512: one chunk holding all
   // rows (two MMAs per k-step when M > 256, single-buffered accumulator); M > 512: ceil(M/256)
   // equal chunks of R <= 256 rows (double-buffered accumulator). Chunks of one weight block are
@@ -250,25 +278,10 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
                           : SkIter{pair < P ? sk_start(pair, Wt, P) : 0, pair < P ? sk_start(pair + 1, Wt, P) : 0,
                                    upi, kpu, 0};
 
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&maps.w);
+  if (warp == 10 && lane == 0) {
     tma_prefetch_desc(&maps.a[NA0 / 32 - 1]);
     if (NA1) tma_prefetch_desc(&maps.a[NA1 / 32 - 1]);
-    for (int s = 0; s < SK_MAX_STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 2 * 8);  // one arrival per epilogue warp of both CTAs
-    }
-    fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
-  tc_fence_before();
-  cluster_sync_all();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) sk_stamp(p, 0);
 
   if (warp == 0 || warp == 10) {
@@ -643,8 +656,7 @@ static int launch_skinny_t(const GemmCall &g, int num_sms, cudaStream_t st) {
   // count: the kernel derives them; the grid is every co-resident pair
   SkinnyParams p{g.M_ptr, g.M_cap, g.N, g.K, g.D, g.ldd, g.resid, g.ldr, g.resid_rows, g.bias, g.ws, g.ctr, max_pairs,
                  g_skinny_trace, g_skinny_split, g_skinny_one_chunk};
-  cfg.gridDim = dim3(2 * max_pairs);
-  DY_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, p));
+  DY_CUDA(launch_k(kern, dim3(2 * max_pairs), dim3(SK_THREADS), SK_SMEM, st, 2, maps, p));
   return DYLLM_OK;
 }
 

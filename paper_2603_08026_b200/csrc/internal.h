@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/dyllm.h"
@@ -25,6 +26,41 @@ void set_error(const std::string &msg);
       return DYLLM_E_CUDA;                                                                         \
     }                                                                                              \
   } while (0)
+
+// ------------------------------------------------------------------ launches
+extern bool g_pdl_enabled;  // programmatic dependent launch for every kernel (dyllm_set_option)
+// kern<<<grid, block, smem, st>>>(args...) with programmatic stream serialisation (+ an optional
+// cluster shape): the kernel may begin while its predecessor drains; it calls pdl_wait() first.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster_x,
+                     Args &&...args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  if (g_pdl_enabled) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster_x > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = cluster_x;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// launch from a void helper: a failing runtime call also sets the runtime's last error, which every
+// ABI entry point checks (sticky) and every step checks at its end (cudaGetLastError)
+#define DY_CUDA_LAUNCH(expr) static_cast<void>(expr)
 
 // ------------------------------------------------------------------ GEMM (gemm.cu)
 enum Epi { EPI_BF16 = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_LMHEAD = 3 };

@@ -13,6 +13,7 @@ namespace dy {
 __global__ void embed_rows_kernel(const int *__restrict__ tokens, const int *__restrict__ rows,
                                   const int *__restrict__ M_ptr, int M_cap, const bf16 *__restrict__ emb,
                                   bf16 *__restrict__ H0, int d) {
+  pdl_wait();
   const int M = M_ptr ? *M_ptr : M_cap;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
   for (int i = warp; i < M; i += gridDim.x * blockDim.x / 32) {
@@ -29,6 +30,7 @@ __global__ void embed_rows_kernel(const int *__restrict__ tokens, const int *__r
 __global__ void gather_rmsnorm_kernel(const bf16 *__restrict__ src, const int *__restrict__ idx,
                                       const int *__restrict__ M_ptr, int M_cap, const bf16 *__restrict__ g,
                                       float eps, bf16 *__restrict__ dst, int d) {
+  pdl_wait();
   const int M = M_ptr ? *M_ptr : M_cap;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
   const int nv = d / 8;
@@ -107,6 +109,7 @@ __device__ __forceinline__ void copy_row(uint4 *__restrict__ o, const uint4 *__r
 // plain row gather dst[i] = src[idx[i]] (a6 A-operand: C[idx_out])
 __global__ void gather_rows_kernel(const bf16 *__restrict__ src, const int *__restrict__ idx,
                                    const int *__restrict__ M_ptr, int M_cap, bf16 *__restrict__ dst, int width) {
+  pdl_wait();
   const int M = M_ptr ? *M_ptr : M_cap;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
   const int nv = width / 8;
@@ -121,6 +124,7 @@ __global__ void gather_rows_kernel(const bf16 *__restrict__ src, const int *__re
 // dst[idx[i]] = src[i]  (H_l[idx_out] <- FFN rows); other rows untouched (zero-copy reuse)
 __global__ void scatter_rows_kernel(const bf16 *__restrict__ src, const int *__restrict__ idx,
                                     const int *__restrict__ M_ptr, int M_cap, bf16 *__restrict__ dst, int width) {
+  pdl_wait();
   const int M = M_ptr ? *M_ptr : M_cap;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
   const int nv = width / 8;
@@ -140,6 +144,7 @@ __global__ void qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restr
                                 int H, int KVH, int hd, const float2 *__restrict__ rope_cs, bf16 *__restrict__ Qc,
                                 bf16 *__restrict__ Kc, bf16 *__restrict__ Vc, bf16 *__restrict__ dV,
                                 bf16 *__restrict__ Qx, bf16 *__restrict__ Kx) {
+  pdl_wait();
   const int M = M_ptr ? *M_ptr : M_cap;
   const int qw = H * hd, kw = KVH * hd, W = qw + 2 * kw;
   const int half = hd / 2, hv = half / 8;  // 8 rotation pairs per thread (16-byte vectors)
@@ -241,6 +246,7 @@ __global__ void qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restr
 
 // RoPE table cs[pos][k] = (cos, sin)(pos * theta^(-2k/hd)), computed in fp64 once per cache.
 __global__ void rope_table_kernel(float2 *__restrict__ cs, int N, int hd, double theta) {
+  pdl_wait();
   const int half = hd / 2;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < N * half; e += gridDim.x * blockDim.x) {
     const int pos = e / half, k = e - pos * half;
@@ -257,6 +263,7 @@ __global__ void rope_table_kernel(float2 *__restrict__ cs, int N, int hd, double
 __global__ void approx_rows_kernel(const int *__restrict__ idx_in, const int *__restrict__ off_in, int N,
                                    int row_lo, int *__restrict__ ap_rows, int *__restrict__ ap_off, int batch,
                                    uint8_t *__restrict__ rowflag) {
+  pdl_wait();
   extern __shared__ uint8_t flag[];
   __shared__ int warp_cnt[32];
   const int s = blockIdx.x;
@@ -298,6 +305,7 @@ __global__ void approx_rows_kernel(const int *__restrict__ idx_in, const int *__
 __global__ void build_list_kernel(int mode, const int *__restrict__ carried, const int *__restrict__ carried_off,
                                   const int *__restrict__ dec_pos, int n_u, int policy, int batch, int N,
                                   int row_lo, int resp_lo, int *__restrict__ out, int *__restrict__ out_off) {
+  pdl_wait();
   extern __shared__ uint8_t flag[];
   __shared__ int warp_cnt[32];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
@@ -356,6 +364,7 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
     int cmp, float frac, int *__restrict__ idx_out, int *__restrict__ off_out, float *__restrict__ sim_out,
     unsigned *__restrict__ masks, unsigned *__restrict__ ticket, int *__restrict__ counts_out,
     const uint8_t *__restrict__ rowflag, const int *__restrict__ dl_off) {
+  pdl_wait();
   __shared__ unsigned row_flag[kSelRowsPerCta];
   __shared__ bool is_last;
   const int s = blockIdx.y;
@@ -613,6 +622,7 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
 // Candidate rows = masked positions of the active semi-AR block of each sequence (D13).
 __global__ void lm_candidates_kernel(const int *__restrict__ tokens, int batch, int L_P, int L_R, int block,
                                      int mask_id, int *__restrict__ rows, int *__restrict__ off) {
+  pdl_wait();
   // single CTA, one warp per sequence for the search; counts then prefix
   __shared__ int cnt[1024];
   __shared__ int blk_of[1024];
@@ -668,6 +678,7 @@ __global__ void lm_select_commit_kernel(const float4 *__restrict__ partials, int
                                         int *__restrict__ tokens, int *__restrict__ dec_pos,
                                         int *__restrict__ dec_tok, const bf16 *__restrict__ emb,
                                         bf16 *__restrict__ H0, int d) {
+  pdl_wait();
   __shared__ float conf[256];
   __shared__ int tok[256];
   __shared__ int chosen[64];
@@ -760,6 +771,7 @@ __device__ __forceinline__ bf16 ih4_value(uint64_t key, uint64_t i, float scale)
 // source row (r / (2*il)) * il + r % il  (gate/up interleave of the SwiGLU GEMM, blocks of il).
 __global__ void ih4_fill_kernel(bf16 *__restrict__ dst, int64_t rows, int cols, uint64_t keyA, uint64_t keyB,
                                 int il, float scale) {
+  pdl_wait();
   const int64_t n = rows * cols;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -775,6 +787,7 @@ __global__ void ih4_fill_kernel(bf16 *__restrict__ dst, int64_t rows, int cols, 
   }
 }
 __global__ void fill_const_kernel(bf16 *__restrict__ dst, int64_t n, float v) {
+  pdl_wait();
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x)
     dst[e] = __float2bfloat16_rn(v);
@@ -792,23 +805,23 @@ static inline int grid_for(int64_t work, int per_block, int cap = 148 * 2) {
 
 void launch_embed_rows(const int *tokens, const int *rows, const int *M_ptr, int M_cap, const bf16 *emb, bf16 *H0,
                        int d, cudaStream_t st) {
-  embed_rows_kernel<<<grid_for(M_cap, 8), 256, 0, st>>>(tokens, rows, M_ptr, M_cap, emb, H0, d);
+  DY_CUDA_LAUNCH(launch_k(embed_rows_kernel, dim3(grid_for(M_cap, 8)), dim3(256), 0, st, 1, tokens, rows, M_ptr, M_cap, emb, H0, d));
 }
 void launch_gather_rmsnorm(const bf16 *src, const int *idx, const int *M_ptr, int M_cap, const bf16 *g, float eps,
                            bf16 *dst, int d, cudaStream_t st) {
-  gather_rmsnorm_kernel<<<grid_for(M_cap, 4, 148 * 4), 128, 0, st>>>(src, idx, M_ptr, M_cap, g, eps, dst, d);
+  DY_CUDA_LAUNCH(launch_k(gather_rmsnorm_kernel, dim3(grid_for(M_cap, 4, 148 * 4)), dim3(128), 0, st, 1, src, idx, M_ptr, M_cap, g, eps, dst, d));
 }
 void launch_gather_rows(const bf16 *src, const int *idx, const int *M_ptr, int M_cap, bf16 *dst, int width,
                         cudaStream_t st) {
-  gather_rows_kernel<<<grid_for(M_cap, 8), 256, 0, st>>>(src, idx, M_ptr, M_cap, dst, width);
+  DY_CUDA_LAUNCH(launch_k(gather_rows_kernel, dim3(grid_for(M_cap, 8)), dim3(256), 0, st, 1, src, idx, M_ptr, M_cap, dst, width));
 }
 void launch_scatter_rows(const bf16 *src, const int *idx, const int *M_ptr, int M_cap, bf16 *dst, int width,
                          cudaStream_t st) {
-  scatter_rows_kernel<<<grid_for(M_cap, 8), 256, 0, st>>>(src, idx, M_ptr, M_cap, dst, width);
+  DY_CUDA_LAUNCH(launch_k(scatter_rows_kernel, dim3(grid_for(M_cap, 8)), dim3(256), 0, st, 1, src, idx, M_ptr, M_cap, dst, width));
 }
 void launch_rmsnorm_rows(const bf16 *src, const int *M_ptr, int M_cap, const bf16 *g, float eps, bf16 *dst, int d,
                          cudaStream_t st) {
-  gather_rmsnorm_kernel<<<grid_for(M_cap, 4, 148 * 4), 128, 0, st>>>(src, nullptr, M_ptr, M_cap, g, eps, dst, d);
+  DY_CUDA_LAUNCH(launch_k(gather_rmsnorm_kernel, dim3(grid_for(M_cap, 4, 148 * 4)), dim3(128), 0, st, 1, src, nullptr, M_ptr, M_cap, g, eps, dst, d));
 }
 void launch_qkv_post(const bf16 *qkv, const int *idx, const int *M_ptr, int M_cap, const bf16 *bias, int N, int H,
                      int KVH, int hd, const float2 *rope_cs, bf16 *Qc, bf16 *Kc, bf16 *Vc, bf16 *dV, bf16 *Qx,
@@ -816,45 +829,45 @@ void launch_qkv_post(const bf16 *qkv, const int *idx, const int *M_ptr, int M_ca
   const int g = M_cap < 148 * 4 ? M_cap : 148 * 4;  // one row per CTA per pass; capped like grid_for
   const int work = std::max((H + KVH) * (hd / 16), KVH * hd / 8);  // vectors per row of each part
   const int threads = std::min(1024, std::max(32, (work + 31) / 32 * 32));
-  qkv_post_kernel<<<g > 0 ? g : 1, threads, 0, st>>>(qkv, idx, M_ptr, M_cap, bias, N, H, KVH, hd, rope_cs, Qc, Kc, Vc,
-                                                 dV, Qx, Kx);
+  DY_CUDA_LAUNCH(launch_k(qkv_post_kernel, dim3(g > 0 ? g : 1), dim3(threads), 0, st, 1, qkv, idx, M_ptr, M_cap, bias, N, H, KVH, hd, rope_cs, Qc, Kc, Vc,
+                                                 dV, Qx, Kx));
 }
 void launch_rope_table(float2 *cs, int N, int hd, double theta, cudaStream_t st) {
-  rope_table_kernel<<<148, 256, 0, st>>>(cs, N, hd, theta);
+  DY_CUDA_LAUNCH(launch_k(rope_table_kernel, dim3(148), dim3(256), 0, st, 1, cs, N, hd, theta));
 }
 void launch_approx_rows(const int *idx_in, const int *off_in, int batch, int N, int row_lo, int *ap_rows,
                         int *ap_off, uint8_t *rowflag, cudaStream_t st) {
-  approx_rows_kernel<<<batch, 256, N, st>>>(idx_in, off_in, N, row_lo, ap_rows, ap_off, batch, rowflag);
+  DY_CUDA_LAUNCH(launch_k(approx_rows_kernel, dim3(batch), dim3(256), N, st, 1, idx_in, off_in, N, row_lo, ap_rows, ap_off, batch, rowflag));
 }
 void launch_build_list(int mode, const int *carried, const int *carried_off, const int *dec_pos, int n_u, int policy,
                        int batch, int N, int row_lo, int resp_lo, int *out, int *out_off, cudaStream_t st) {
-  build_list_kernel<<<1, 1024, N, st>>>(mode, carried, carried_off, dec_pos, n_u, policy, batch, N, row_lo, resp_lo,
-                                        out, out_off);
+  DY_CUDA_LAUNCH(launch_k(build_list_kernel, dim3(1), dim3(1024), N, st, 1, mode, carried, carried_off, dec_pos, n_u, policy, batch, N, row_lo, resp_lo,
+                                        out, out_off));
 }
 void launch_select(const bf16 *c_new, bf16 *c_cache, int batch, int N, int row_lo, int width, float tau, int cmp,
                    float frac, int *idx_out, int *off_out, float *sim_out, unsigned *masks, unsigned *ticket,
                    int *counts, const uint8_t *rowflag, const int *dl_off, cudaStream_t st) {
   const int L = N - row_lo;
   dim3 grid((L + kSelRowsPerCta - 1) / kSelRowsPerCta, batch);
-  select_salient_kernel<<<grid, kSelThreads, 0, st>>>(c_new, c_cache, N, row_lo, width, tau, cmp, frac, idx_out, off_out,
-                                              sim_out, masks, ticket, counts, rowflag, dl_off);
+  DY_CUDA_LAUNCH(launch_k(select_salient_kernel, dim3(grid), dim3(kSelThreads), 0, st, 1, c_new, c_cache, N, row_lo, width, tau, cmp, frac, idx_out, off_out,
+                                              sim_out, masks, ticket, counts, rowflag, dl_off));
 }
 void launch_lm_candidates(const int *tokens, int batch, int L_P, int L_R, int block, int mask_id, int *rows, int *off,
                           cudaStream_t st) {
-  lm_candidates_kernel<<<1, 1024, 0, st>>>(tokens, batch, L_P, L_R, block, mask_id, rows, off);
+  DY_CUDA_LAUNCH(launch_k(lm_candidates_kernel, dim3(1), dim3(1024), 0, st, 1, tokens, batch, L_P, L_R, block, mask_id, rows, off));
 }
 void launch_lm_select_commit(const float4 *partials, int n_tiles, const int *rows, const int *off, int batch, int n_u,
                              int *tokens, int *dec_pos, int *dec_tok, const bf16 *emb, bf16 *H0, int d,
                              cudaStream_t st) {
-  lm_select_commit_kernel<<<batch, 256, 0, st>>>(partials, n_tiles, rows, off, n_u, tokens, dec_pos, dec_tok, emb, H0,
-                                                 d);
+  DY_CUDA_LAUNCH(launch_k(lm_select_commit_kernel, dim3(batch), dim3(256), 0, st, 1, partials, n_tiles, rows, off, n_u, tokens, dec_pos, dec_tok, emb, H0,
+                                                 d));
 }
 void launch_ih4_fill(bf16 *dst, int64_t rows, int cols, uint64_t keyA, uint64_t keyB, int il, float scale,
                      cudaStream_t st) {
-  ih4_fill_kernel<<<148 * 8, 256, 0, st>>>(dst, rows, cols, keyA, keyB, il, scale);
+  DY_CUDA_LAUNCH(launch_k(ih4_fill_kernel, dim3(148 * 8), dim3(256), 0, st, 1, dst, rows, cols, keyA, keyB, il, scale));
 }
 void launch_fill_const(bf16 *dst, int64_t n, float v, cudaStream_t st) {
-  fill_const_kernel<<<148 * 4, 256, 0, st>>>(dst, n, v);
+  DY_CUDA_LAUNCH(launch_k(fill_const_kernel, dim3(148 * 4), dim3(256), 0, st, 1, dst, n, v));
 }
 
 }  // namespace dy

@@ -99,7 +99,7 @@ def lib():
     return _lib
 
 
-OPT_SKINNY_GEMM, OPT_SKINNY_SPLIT, OPT_ATTN_FUSED, OPT_SKINNY_ONE_CHUNK = 1, 2, 3, 4
+OPT_SKINNY_GEMM, OPT_SKINNY_SPLIT, OPT_ATTN_FUSED, OPT_SKINNY_ONE_CHUNK, OPT_PDL = 1, 2, 3, 4, 5
 
 
 def set_option(option: int, value: int) -> int:
