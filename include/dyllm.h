@@ -159,12 +159,21 @@ int dyllm_unmask(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int32_t
                  int32_t *d_dec_tok);
 
 /* Device pointer to one cache tensor of one layer (layer in [0,n_layers); which = DYLLM_K..H;
- * for DYLLM_H, layer in [0, n_layers] where H_0 = embeddings). Synchronous, no copy. */
+ * for DYLLM_H, layer in [0, n_layers] where H_0 = embeddings). Synchronous, no copy. Handing out
+ * K or Q invalidates the layer's incremental attention statistics (see dyllm_cache_refresh_stats). */
 int dyllm_cache_tensor(const dyllm_cache *c, int layer, int which, void **d_ptr, int64_t *n_elems);
 /* Copy a cache tensor to (export=1) or from (export=0) `ptr`; `ptr_on_device` = 1 if ptr is
  * device memory. Asynchronous on the ctx stream. Test / teacher-forcing hook. */
 int dyllm_cache_copy(dyllm_ctx *ctx, dyllm_cache *c, int layer, int which, void *ptr,
                      int ptr_on_device, int export_);
+/* Recompute, densely, the per-(row, head) softmax statistics (row max, sum of exps) of one layer
+ * from its current Q and K caches. The head_dim-128 attention keeps them to update response rows
+ * incrementally (only the salient keys changed, so the normaliser is updated by their
+ * old and new terms instead of a pass over all N keys); they are written by every FullStep and
+ * denoising step and invalidated whenever dyllm_cache_tensor hands out K or Q of the layer (the
+ * next step then runs that layer densely). Test hook after writing caches from outside.
+ * Asynchronous. Returns DYLLM_OK without work for other head dims. */
+int dyllm_cache_refresh_stats(dyllm_ctx *ctx, dyllm_cache *c, int layer);
 /* Set the carried salient list (idx_sal between steps) — test hook; NULL resets to None. */
 int dyllm_cache_set_carried(dyllm_ctx *ctx, dyllm_cache *c, const int32_t *d_idx, const int32_t *d_off);
 
@@ -213,8 +222,10 @@ uint64_t dyllm_launch_count(void);
  * keeps in a single activation chunk (above it: chunks of <= 256 rows). */
 /* DYLLM_OPT_PDL (default 1): launch every kernel with programmatic dependent launch (a kernel's
  * setup overlaps its predecessor; each kernel waits for its predecessor before touching memory). */
+/* DYLLM_OPT_ATTN_INC (default 1): incremental softmax statistics for response tiles (see
+ * dyllm_cache_refresh_stats); 0 = every tile computes its normaliser over all N keys. */
 enum { DYLLM_OPT_SKINNY_GEMM = 1, DYLLM_OPT_SKINNY_SPLIT = 2, DYLLM_OPT_ATTN_FUSED = 3, DYLLM_OPT_SKINNY_ONE_CHUNK = 4,
-       DYLLM_OPT_PDL = 5 };
+       DYLLM_OPT_PDL = 5, DYLLM_OPT_ATTN_INC = 6 };
 int dyllm_set_option(int option, int value);
 
 /* Debug hook: when d_buf != NULL, kernels of family `which` (0 = skinny GEMM) write %globaltimer

@@ -61,11 +61,18 @@ struct FaParams {
   bf16 *C_out;
   int *work_ctr;              // [2] dynamic scheduler: next item, finished CTAs (zero between launches)
   unsigned long long *events; // optional event log of CTAs 0-1 (debug hook): [cta][role][8192]
+  float2 *stats;              // [b*N][H] softmax statistics per (row, head): (m c, l = sum 2^(s c - m c))
+  int inc;                    // statistics of the response rows are current: incremental tiles allowed
+  int resp_lo;                // first response position (L_P)
+  int mode;                   // 0 denoising step, 1 fixup list (dense), 2 statistics refresh (no output)
+  int *fix;                   // [0] count, [1 ..] ids of incremental tiles whose update cancelled
+  int fix_cap;
 };
 
 struct FaItem {
   int s, h, kvh, nrows, q_row, off, nkP, xc;
   bool type2, passP;
+  bool inc;  // type 3: incremental statistics (response tile, <= 128 salient keys, current stats)
 };
 
 // Item decode from its index and the exact-row range (off, e) of its sequence (the producer reads
@@ -86,8 +93,12 @@ __device__ __forceinline__ FaItem fa_item(const FaParams &p, int w, int off, int
     it.xc = 0;
     it.q_row = it.s * p.N + p.row_lo + t * 128;
     it.nrows = min(128, p.L - t * 128);
-    it.passP = e > 0;
+    it.passP = e > 0 && p.mode != 2;
     it.nkP = e;
+    it.inc = p.inc && p.mode == 0 && e > 0 && e <= FA_BK && p.row_lo + t * 128 >= p.resp_lo;
+    // no salient key in the sequence: the keys did not change, so neither did the statistics
+    // (when current) nor the contexts: nothing to do
+    if (e == 0 && p.inc && p.mode == 0) it.nrows = 0;
   } else {
     it.type2 = true;
     it.xc = t - p.MT;
@@ -95,6 +106,7 @@ __device__ __forceinline__ FaItem fa_item(const FaParams &p, int w, int off, int
     it.nrows = min(128, e - it.xc * 128);
     it.passP = true;
     it.nkP = p.N;
+    it.inc = false;
   }
   return it;
 }
@@ -194,6 +206,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     attn_fused_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQx,
                       const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                       const __grid_constant__ CUtensorMap tmKx, const __grid_constant__ CUtensorMap tmDV,
+                      const __grid_constant__ CUtensorMap tmKxo,
                       const FaParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -217,7 +230,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   FaEv ev;
   {
     const int role = warp == 1 ? 0 : warp == 2 ? 1 : warp == 0 ? 2 : warp == FA_WV ? 3 : -1;
-    if (p.events && blockIdx.x < 2 && lane == 0 && role >= 0) ev.attach(p.events + (blockIdx.x * 4 + role) * FA_EV_N);
+    if (p.events && p.mode == 0 && blockIdx.x < 2 && lane == 0 && role >= 0) ev.attach(p.events + (blockIdx.x * 4 + role) * FA_EV_N);
   }
 
   if (warp == 0 && lane == 0) {
@@ -296,7 +309,11 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       int w, off = 0, e = 0;
       for (;;) {
         w = atomicAdd(&p.work_ctr[0], 1);
-        if (w >= p.items) {
+        if (p.mode == 1) {  // fixup launch: the listed tiles, processed densely
+          const int nfix = min(p.fix[0], p.fix_cap);
+          w = w < nfix ? p.fix[1 + w] : -1;
+          if (w < 0) break;
+        } else if (w >= p.items) {
           w = -1;
           break;
         }
@@ -348,6 +365,14 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       auto after_first = [&]() {
         if (warp == 0 && lane == 0 && wnext >= 0) load_q(fa_item(p, wnext, onext, enext), qi + 1);
       };
+      if (it.inc) {  // type 3: new salient keys, their old keys, dV
+        load_kv(&tmKx, it.off, it.kvh);
+        after_first();
+        load_kv(&tmKxo, it.off, it.kvh);
+        load_kv(&tmDV, it.off, it.kvh);
+        ++qi;
+        continue;
+      }
       // pass S (type 1): the N keys
       if (!it.type2) {
         for (int kt = 0; kt < NKT; ++kt) {
@@ -355,16 +380,17 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           if (kt == 0) after_first();
         }
       }
-      // pass P, in the MMA warp's order: K'(0), then K'(j+1), V'(j) for each j (K' = keys of the P
-      // tiles, V' = their values: all keys + V for exact rows, salient keys + dV otherwise)
+      // pass P, in the MMA warp's order: K'(0), K'(1), then K'(j+2), V'(j) for each j (K' = keys of
+      // the P tiles, V' = their values: all keys + V for exact rows, salient keys + dV otherwise)
       if (it.passP) {
         const int n2 = (it.nkP + FA_BK - 1) / FA_BK;
         const CUtensorMap *mk = it.type2 ? &tmK : &tmKx, *mv = it.type2 ? &tmV : &tmDV;
         const int r0 = it.type2 ? seq0 : it.off;
         load_kv(mk, r0, it.kvh);
         if (it.type2) after_first();
+        if (n2 > 1) load_kv(mk, r0 + FA_BK, it.kvh);
         for (int j = 0; j < n2; ++j) {
-          if (j + 1 < n2) load_kv(mk, r0 + (j + 1) * FA_BK, it.kvh);
+          if (j + 2 < n2) load_kv(mk, r0 + (j + 2) * FA_BK, it.kvh);
           load_kv(mv, r0 + j * FA_BK, it.kvh);
         }
       }
@@ -394,7 +420,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         ++wn1;
         if (q.x < 0) break;
         const FaItem it = fa_item(p, q.x, q.y, q.z);
-        ev(it.type2 ? 2 : 1);
+        ev(it.inc ? 3 : it.type2 ? 2 : 1);
         const int qb = qi & 1;
         fa_wait(&q_full[qb], (qi >> 1) & 1);
         ++qi;
@@ -418,34 +444,48 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           ++g;
           ++sc;
         };
+        auto pv = [&](int j, int n2) {
+          const int pb = pc & 1;
+          ev(20);
+          fa_wait(&p_full[pb], (pc >> 1) & 1);
+          ev(21);
+          const int vs = g % FA_KVST;
+          fa_wait(&kv_full[vs], (g / FA_KVST) & 1);
+          if (j == 0) fa_wait(acc_empty, (ai & 1) ^ 1);
+          ev(22);
+          tc_fence_after();
+          const uint64_t vd = vdesc0 + vs * kSlot;
+          const uint32_t pa = tmem + FA_P_COL + pb * 64;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)  // 16 keys per MMA: 8 packed TMEM columns of P, 2 KB of V
+            umma_bf16_ts(tmem + FA_ACC_COL, pa + kk * 8, vd + static_cast<uint64_t>(kk * 2048 >> 4), id_pv,
+                         (j | kk) != 0);
+          umma_commit(&kv_empty[vs]);
+          umma_commit(&p_empty[pb]);
+          if (j == n2 - 1) umma_commit(acc_full);
+          ev(23);
+          ++g;
+          ++pc;
+        };
+        if (it.inc) {  // type 3: S_new, S_old, then P dV
+          qk();
+          qk();
+          pv(0, 1);
+          ++ai;
+          umma_commit(&q_empty[qb]);
+          continue;
+        }
         if (!it.type2)
           for (int kt = 0; kt < NKT; ++kt) qk();
         if (it.passP) {
+          // two score tiles ahead of P V: the score tile j + 2 reuses the S buffer the softmax
+          // read tile j out of, so it is issued while the softmax still computes P(j)
           const int n2 = (it.nkP + FA_BK - 1) / FA_BK;
           qk();
+          if (n2 > 1) qk();
           for (int j = 0; j < n2; ++j) {
-            if (j + 1 < n2) qk();
-            const int pb = pc & 1;
-            ev(20);
-            fa_wait(&p_full[pb], (pc >> 1) & 1);
-            ev(21);
-            const int vs = g % FA_KVST;
-            fa_wait(&kv_full[vs], (g / FA_KVST) & 1);
-            if (j == 0) fa_wait(acc_empty, (ai & 1) ^ 1);
-            ev(22);
-            tc_fence_after();
-            const uint64_t vd = vdesc0 + vs * kSlot;
-            const uint32_t pa = tmem + FA_P_COL + pb * 64;
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk)  // 16 keys per MMA: 8 packed TMEM columns of P, 2 KB of V
-              umma_bf16_ts(tmem + FA_ACC_COL, pa + kk * 8, vd + static_cast<uint64_t>(kk * 2048 >> 4), id_pv,
-                           (j | kk) != 0);
-            umma_commit(&kv_empty[vs]);
-            umma_commit(&p_empty[pb]);
-            if (j == n2 - 1) umma_commit(acc_full);
-            ev(23);
-            ++g;
-            ++pc;
+            if (j + 2 < n2) qk();
+            pv(j, n2);
           }
           ++ai;
         }
@@ -471,10 +511,129 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       // type 1 writes approximate rows only: fetch the row kind early (its latency hides under pass S)
       const int64_t orow = it.type2 ? (rvalid ? p.ex_rows[it.q_row + r] : 0) : static_cast<int64_t>(it.q_row) + r;
       const bool write_row = rvalid && (it.type2 || (it.passP && !p.rowflag[orow]));
-      ev(it.type2 ? 2 : 1);
+      ev(it.inc ? 3 : it.type2 ? 2 : 1);
       float acc[FA_CW];
       float oscale;
-      if (it.type2) {
+      // statistics entry of this row (exact rows' entries belong to the type-2 items)
+      const bool own_stats = p.stats != nullptr && rvalid && hh == 0 && (it.type2 || p.mode == 2 || !p.rowflag[orow]);
+      const int64_t srow = orow * p.H + it.h;
+      if (it.inc) {
+        // ---- type 3, incremental statistics (exact up to rounding): only the salient
+        // keys changed since this row's statistics (m_old, l_old) were computed, so
+        //   l_new = l_old 2^(m_old - m) - sum_j 2^(s_old_j c - m) + sum_j 2^(s_new_j c - m),
+        // with m = max(m_old, max_j s_new_j c); P = 2^(s_new c - m) feeds P dV as in pass P. All
+        // exps on MUFU (no polynomial: the removed and added terms must carry no systematic error).
+        // A row whose l_new cancels below 2^-14 of l_old (the changed keys held nearly all its
+        // attention) sends its tile to the dense fixup launch.
+        const float2 so = rvalid ? p.stats[srow] : make_float2(0.f, 1.f);
+        float part = 0.f, mref = 0.f;
+        {
+          const int sb = sc & 1;
+          fa_wait(&s_full[sb], (sc >> 1) & 1);
+          ++sc;
+          const int pb = pc & 1;
+          ++pc;
+          if (!wact) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[sb]);
+            fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[pb]);
+          } else {
+            tc_fence_after();
+            float v[FA_CW];
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch) tmem_ld32(trow + sb * FA_BK + hh * FA_CW + ch * 32, v + ch * 32);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[sb]);
+            float tmax = -INFINITY;
+#pragma unroll
+            for (int t = 0; t < FA_CW; ++t) {
+              if (hh * FA_CW + t >= it.nkP) v[t] = -INFINITY;
+              tmax = fmaxf(tmax, v[t]);
+            }
+            xch[hh * 128 + r].x = tmax;
+            fa_named_sync(1 + quad, 32 * FA_NG);
+            float mn = -INFINITY;
+#pragma unroll
+            for (int g2 = 0; g2 < FA_NG; ++g2) mn = fmaxf(mn, xch[g2 * 128 + r].x);
+            fa_named_sync(1 + quad, 32 * FA_NG);
+            mref = fmaxf(so.x, mn * c);
+            fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1);
+            tc_fence_after();
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch) {
+              uint32_t pk[16];
+#pragma unroll
+              for (int t = 0; t < 16; ++t) {
+                const float p0 = ex2f(fmaf(v[ch * 32 + 2 * t], c, -mref));
+                const float p1 = ex2f(fmaf(v[ch * 32 + 2 * t + 1], c, -mref));
+                part += p0 + p1;
+                pk[t] = pack2(p0, p1);
+              }
+              tmem_st16(trow + FA_P_COL + pb * 64 + hh * (FA_CW / 2) + ch * 16, pk);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[pb]);
+          }
+        }
+        {  // the same keys before this step's overwrite
+          const int sb = sc & 1;
+          fa_wait(&s_full[sb], (sc >> 1) & 1);
+          ++sc;
+          if (!wact) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[sb]);
+          } else {
+            tc_fence_after();
+            float v[FA_CW];
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch) tmem_ld32(trow + sb * FA_BK + hh * FA_CW + ch * 32, v + ch * 32);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[sb]);
+            float sub = 0.f;
+#pragma unroll
+            for (int t = 0; t < FA_CW; ++t)
+              sub += hh * FA_CW + t < it.nkP ? ex2f(fmaf(v[t], c, -mref)) : 0.f;
+            part -= sub;
+          }
+        }
+        float Lnew = 1.f;
+        bool bad = false;
+        if (wact) {
+          xch[hh * 128 + r].y = part;
+          fa_named_sync(1 + quad, 32 * FA_NG);
+          float tot = 0.f;
+#pragma unroll
+          for (int g2 = 0; g2 < FA_NG; ++g2) tot += xch[g2 * 128 + r].y;
+          fa_named_sync(1 + quad, 32 * FA_NG);
+          const float base = so.y * ex2f(so.x - mref);
+          Lnew = base + tot;
+          bad = !(so.y > 0.f) || !(Lnew > base * 0x1p-14f) || !(Lnew < INFINITY);
+          if (own_stats && !bad) p.stats[srow] = make_float2(mref, Lnew);
+        }
+        // a tile with a cancelled row is recomputed densely by the fixup launch (duplicates of a
+        // tile id are harmless: the dense recomputation is deterministic)
+        if (__ballot_sync(0xffffffffu, rvalid && bad) != 0u && lane == 0) {
+          const int pos = atomicAdd(&p.fix[0], 1);
+          if (pos < p.fix_cap) p.fix[1 + pos] = w;
+        }
+        fa_wait(acc_full, ai & 1);
+        ++ai;
+        if (wact) {
+          tc_fence_after();
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) tmem_ld32(trow + FA_ACC_COL + hh * FA_CW + ch * 32, acc + ch * 32);
+          tc_fence_before();
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty);
+        oscale = 1.f / Lnew;
+      } else if (it.type2) {
         // ---- exact rows: one pass over the N keys (online softmax, lazy rescale)
         float ref = -INFINITY, l = 0.f;
         for (int j = 0; j < NKT; ++j) {
@@ -593,6 +752,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
 #pragma unroll
           for (int g2 = 0; g2 < FA_NG; ++g2) L += xch[g2 * 128 + r].y;
           fa_named_sync(1 + quad, 32 * FA_NG);
+          if (own_stats) p.stats[srow] = make_float2(ref * c, L);
         }
         oscale = 1.f / L;
       } else {
@@ -662,6 +822,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       for (int g = 0; g < FA_NG; ++g) Lsum += hg[g].x == -INFINITY ? 0.f : hg[g].y * ex2f((hg[g].x - M) * c);
       const float Mc = M * c;
       const float inv_l = 1.f / Lsum;
+      if (own_stats && wact) p.stats[srow] = make_float2(Mc, Lsum);
       // ---- pass P: P = exp2(s - m) into tensor memory for the P V MMA
       oscale = inv_l;
       if (it.passP) {
@@ -748,6 +909,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     if (atomicAdd(&p.work_ctr[1], 1) == static_cast<int>(gridDim.x) - 1) {
       p.work_ctr[0] = 0;
       p.work_ctr[1] = 0;
+      if (p.mode == 1) p.fix[0] = 0;  // the fixup list is consumed
       __threadfence();
     }
   }
@@ -765,7 +927,7 @@ int attention_fused_launch(const AttnArgs &a, cudaStream_t st) {
   }
   const int rows_total = a.batch * a.N;
   const int qw = a.H * 128, kw = a.KVH * 128;
-  CUtensorMap tq, tqx, tk, tv, tkx, tdv;
+  CUtensorMap tq, tqx, tk, tv, tkx, tdv, tkxo;
   int rc;
   if ((rc = make_tmap3(&tq, a.Q, rows_total, qw, 128, 2))) return rc;
   if ((rc = make_tmap3(&tqx, a.Qx ? a.Qx : a.Q, rows_total, qw, 128, 2))) return rc;
@@ -773,6 +935,7 @@ int attention_fused_launch(const AttnArgs &a, cudaStream_t st) {
   if ((rc = make_tmap3(&tv, a.V, rows_total, kw, FA_BK, 2))) return rc;
   if ((rc = make_tmap3(&tkx, a.Kx ? a.Kx : a.K, rows_total, kw, FA_BK, 2))) return rc;
   if ((rc = make_tmap3(&tdv, a.dV ? a.dV : a.V, rows_total, kw, FA_BK, 2))) return rc;
+  if ((rc = make_tmap3(&tkxo, a.Kxo ? a.Kxo : a.K, rows_total, kw, FA_BK, 2))) return rc;
   FaParams p;
   p.N = a.N;
   p.row_lo = a.row_lo;
@@ -792,13 +955,25 @@ int attention_fused_launch(const AttnArgs &a, cudaStream_t st) {
   p.C_out = a.C_out;
   p.events = g_attn_events;
   p.work_ctr = a.work_ctr;
+  p.stats = a.stats_cache;
+  p.inc = a.inc && a.stats_cache && a.Kxo ? 1 : 0;
+  p.resp_lo = a.resp_lo;
+  p.mode = a.mode;
+  p.fix = a.fix;
+  p.fix_cap = a.fix_cap;
+  if (p.inc && !p.fix) {
+    set_error("fused attention: incremental statistics need the fixup list");
+    return DYLLM_E_ARG;
+  }
   if (!p.work_ctr) {
     set_error("fused attention: missing scheduler counters");
     return DYLLM_E_ARG;
   }
   if (p.items <= 0) return DYLLM_OK;
-  const int grid = p.items < a.num_sms ? p.items : a.num_sms;
-  DY_CUDA(launch_k(attn_fused_kernel, dim3(grid), dim3(FA_THREADS), FA_SMEM, st, 1, tq, tqx, tk, tv, tkx, tdv, p));
+  // fixup launch: a few CTAs claim the (rare, device-counted) listed tiles
+  const int grid = p.mode == 1 ? 16 : (p.items < a.num_sms ? p.items : a.num_sms);
+  DY_CUDA(launch_k(attn_fused_kernel, dim3(grid), dim3(FA_THREADS), FA_SMEM, st, 1, tq, tqx, tk, tv, tkx, tdv, tkxo,
+                   p));
   DY_CUDA(cudaGetLastError());
   return DYLLM_OK;
 }

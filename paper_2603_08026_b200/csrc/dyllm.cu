@@ -48,6 +48,7 @@ struct dyllm_ctx {
   float *sk_ws = nullptr;      // skinny GEMM split-K partials
   int *sk_ctr = nullptr;       // skinny GEMM split-K counters
   int *attn_ctr = nullptr;     // fused attention scheduler counters [2]
+  int *attn_fix = nullptr;     // fused attention fixup list [1 + kFixCap] (count zero between steps)
   // instrumentation
   bool prof = false;
   int cls_offset = 0;          // DYLLM_KC_FULL while a FullStep enqueues
@@ -92,6 +93,8 @@ struct KScope {
     stmt;                              \
   } while (0)
 static constexpr int64_t kMaskCap = 1 << 20;
+static constexpr int kFixCap = 1 << 16;
+static bool g_attn_inc_enabled = true;  // test hook: incremental attention statistics  // fused attention: tiles re-run densely after a cancelled update
 
 struct LayerW {
   bf16 *g_attn, *wqkv, *bqkv, *wo, *g_ffn, *wgu, *wd;
@@ -104,6 +107,9 @@ struct dyllm_weights {
 };
 struct LayerC {
   bf16 *K, *V, *Q, *C, *H;
+  float2 *st = nullptr;  // [rows][H] softmax statistics (m c, l) of the fused attention (head_dim 128)
+  mutable bool st_ok = false;  // statistics of the response rows are current (incremental tiles
+                               // allowed); cleared whenever K or Q may be written from outside
 };
 struct dyllm_cache {
   dyllm_model_cfg m;
@@ -112,7 +118,7 @@ struct dyllm_cache {
   int N, rows;
   std::vector<LayerC> L;
   bf16 *H0;
-  bf16 *Xn, *qkv, *dV, *Qx, *Kx, *Cn, *Cg, *h, *hn, *act, *ffo, *Xf;
+  bf16 *Xn, *qkv, *dV, *Qx, *Kx, *Kxo, *Cn, *Cg, *h, *hn, *act, *ffo, *Xf;
   uint8_t *rowflag;
   float4 *partials;
   int *lst[2], *lst_off[2];
@@ -204,6 +210,8 @@ int dyllm_ctx_create(int device, void *cuda_stream, dyllm_ctx **out) {
   DY_CUDA(cudaMemset(c->sk_ctr, 0, kSkinnyCtrCap * sizeof(int)));
   DY_CUDA(cudaMalloc(&c->attn_ctr, 2 * sizeof(int)));
   DY_CUDA(cudaMemset(c->attn_ctr, 0, 2 * sizeof(int)));
+  DY_CUDA(cudaMalloc(&c->attn_fix, (1 + kFixCap) * sizeof(int)));
+  DY_CUDA(cudaMemset(c->attn_fix, 0, (1 + kFixCap) * sizeof(int)));
   *out = c;
   return DYLLM_OK;
 }
@@ -222,6 +230,7 @@ void dyllm_ctx_destroy(dyllm_ctx *ctx) {
   cudaFree(ctx->sk_ws);
   cudaFree(ctx->sk_ctr);
   cudaFree(ctx->attn_ctr);
+  cudaFree(ctx->attn_fix);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -416,6 +425,7 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
     AL(L.Q, rows * qw);
     AL(L.C, rows * qw);
     AL(L.H, rows * d);
+    if (m.head_dim == 128) AL(L.st, rows * m.n_heads);
   }
   AL(c->H0, rows * d);
   AL(c->Xn, rows * d);
@@ -423,6 +433,7 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
   AL(c->dV, rows * kw);
   AL(c->Qx, rows * qw);
   AL(c->Kx, rows * kw);
+  AL(c->Kxo, rows * kw);
   AL(c->rowflag, rows);
   AL(c->Cn, rows * qw);
   AL(c->Cg, rows * qw);
@@ -455,6 +466,7 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
   // start them finite
   const bool ok = cudaMemsetAsync(c->dV, 0, rows * kw * 2, st) == cudaSuccess &&
                   cudaMemsetAsync(c->Kx, 0, rows * kw * 2, st) == cudaSuccess &&
+                  cudaMemsetAsync(c->Kxo, 0, rows * kw * 2, st) == cudaSuccess &&
                   cudaMemsetAsync(c->Qx, 0, rows * qw * 2, st) == cudaSuccess &&
                   cudaMemsetAsync(c->zero_off, 0, (r->batch + 1) * sizeof(int), st) == cudaSuccess;
   if (!ok) {
@@ -534,7 +546,7 @@ static int full_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c
     KL(GATHER, launch_gather_rmsnorm(Hprev, nullptr, nullptr, rows, L.g_attn, m.rms_eps, c->Xn, d, st));
     KL(QKV_GEMM, RET(gemm(ctx, nullptr, rows, qw + 2 * kw, d, c->Xn, L.wqkv, c->qkv, qw + 2 * kw, EPI_BF16)));
     KL(QKV_POST, launch_qkv_post(c->qkv, nullptr, nullptr, rows, L.bqkv, c->N, m.n_heads, m.n_kv_heads, m.head_dim,
-                                 c->rope_cs, C.Q, C.K, C.V, nullptr, nullptr, nullptr, st));
+                                 c->rope_cs, C.Q, C.K, C.V, nullptr, nullptr, nullptr, nullptr, st));
     AttnArgs a{};
     a.batch = c->r.batch;
     a.N = c->N;
@@ -560,7 +572,10 @@ static int full_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c
     a.num_sms = ctx->num_sms;
     a.full_only = true;  // every row exact: Qx = the Q cache, ex_rows = identity
     a.work_ctr = ctx->attn_ctr;
+    const bool fused = m.head_dim == 128 && g_attn_fused_enabled;
+    a.stats_cache = fused ? C.st : nullptr;  // every row's statistics written
     KL(ATTN, RET(attention_launch(a, st)));
+    C.st_ok = fused;
     int prc = post_attention(ctx, w, c, l, nullptr, C.C, Hprev, nullptr, C.H);
     if (prc) {
       ctx->cls_offset = 0;
@@ -593,8 +608,13 @@ static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *
   KL(GATHER, launch_gather_rmsnorm(Hprev, idx_in, M_in, rows, L.g_attn, m.rms_eps, c->Xn, d, st));
   KL(QKV_GEMM, RET(gemm(ctx, M_in, rows, qw + 2 * kw, d, c->Xn, L.wqkv, c->qkv, qw + 2 * kw, EPI_BF16)));
   // a3: RoPE, dV (before overwrite), in-place K/V/Q cache rows
+  const bool fused = m.head_dim == 128 && g_attn_fused_enabled;
+  // incremental statistics need the overwritten key rows (Kxo) and current
+  // statistics; under the literal layer-1 policy, decoded rows outside idx_in get a new Q at
+  // layer 0 without a statistics update, so that layer stays dense
+  const bool inc = fused && g_attn_inc_enabled && C.st_ok && !(l == 0 && c->r.layer1_policy == 0);
   KL(QKV_POST, launch_qkv_post(c->qkv, idx_in, M_in, rows, L.bqkv, N, m.n_heads, m.n_kv_heads, m.head_dim,
-                               c->rope_cs, C.Q, C.K, C.V, c->dV, c->Qx, c->Kx, st));
+                               c->rope_cs, C.Q, C.K, C.V, c->dV, c->Qx, c->Kx, inc ? c->Kxo : nullptr, st));
   // a4: exact rows + approximate rows (Alg. 4) -> Cn
   AttnArgs a{};
   a.batch = b;
@@ -623,7 +643,20 @@ static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *
   a.Kx = c->Kx;
   a.rowflag = c->rowflag;
   a.work_ctr = ctx->attn_ctr;
+  a.stats_cache = fused ? C.st : nullptr;
+  a.Kxo = c->Kxo;
+  a.inc = inc;
+  a.resp_lo = c->r.L_P;
+  a.fix = ctx->attn_fix;
+  a.fix_cap = kFixCap;
   KL(ATTN, RET(attention_launch(a, st)));
+  if (inc) {  // tiles whose incremental update cancelled (rare): dense recomputation
+    AttnArgs f = a;
+    f.mode = 1;
+    KL(OTHER, RET(attention_launch(f, st)));  // not an attention pass of its own (roofline accounting)
+  }
+  // every input row's statistics are now current (dense tiles, incremental tiles, exact rows)
+  C.st_ok = fused;
   // a5: cosine similarity + threshold + compaction; C_cache <- Cn for the input rows
   const bool fmode = c->r.select_mode == 1;
   const bool delta = attention_writes_delta(m.head_dim);  // fused kernel: Cn = dC for approximate rows
@@ -794,6 +827,11 @@ int dyllm_set_option(int option, int value) {
     g_pdl_enabled = value != 0;
     return prev;
   }
+  if (option == DYLLM_OPT_ATTN_INC) {
+    const int prev = g_attn_inc_enabled ? 1 : 0;
+    g_attn_inc_enabled = value != 0;
+    return prev;
+  }
   if (option == DYLLM_OPT_SKINNY_SPLIT) {
     const int prev = g_skinny_split;
     g_skinny_split = value < 0 ? 0 : value;
@@ -822,6 +860,10 @@ int dyllm_debug_trace_buffer(int which, void *d_buf) {
 
 // ------------------------------------------------------------------ ABI: cache access
 int dyllm_cache_tensor(const dyllm_cache *c, int layer, int which, void **d_ptr, int64_t *n_elems) {
+  // K / Q handed out writable: the incremental softmax statistics of that layer can no longer be
+  // trusted until the next dense pass (a denoising step, or dyllm_cache_refresh_stats)
+  if (c && (which == DYLLM_K || which == DYLLM_Q) && layer >= 0 && layer < static_cast<int>(c->L.size()))
+    c->L[layer].st_ok = false;
   CHECK_ARG(c && d_ptr, "null argument");
   const int64_t rows = c->rows, d = c->m.d_model, qw = static_cast<int64_t>(c->m.n_heads) * c->m.head_dim,
                 kw = static_cast<int64_t>(c->m.n_kv_heads) * c->m.head_dim;
@@ -870,6 +912,47 @@ int dyllm_cache_set_carried(dyllm_ctx *ctx, dyllm_cache *c, const int32_t *d_idx
   DY_CUDA(cudaMemcpyAsync(c->carried_off, d_off, sizeof(int) * (c->r.batch + 1), cudaMemcpyDeviceToDevice, ctx->stream));
   DY_CUDA(cudaMemcpyAsync(c->carried, d_idx, sizeof(int) * c->rows, cudaMemcpyDeviceToDevice, ctx->stream));
   c->carried_valid = true;
+  return DYLLM_OK;
+}
+
+int dyllm_cache_refresh_stats(dyllm_ctx *ctx, dyllm_cache *c, int layer) {
+  CHECK_ARG(ctx && c, "null argument");
+  if (layer < 0 || layer >= c->m.n_layers) {
+    set_error("layer out of range");
+    return DYLLM_E_INDEX;
+  }
+  RET(sticky(ctx));
+  const dyllm_model_cfg &m = c->m;
+  LayerC &C = c->L[layer];
+  if (m.head_dim != 128 || !g_attn_fused_enabled || !C.st) return DYLLM_OK;  // no incremental path
+  AttnArgs a{};
+  a.batch = c->r.batch;
+  a.N = c->N;
+  a.H = m.n_heads;
+  a.KVH = m.n_kv_heads;
+  a.hd = m.head_dim;
+  a.Q = C.Q;
+  a.K = C.K;
+  a.V = C.V;
+  a.C_cache = C.C;
+  a.C_out = c->Cn;
+  a.ex_rows = c->all_rows;
+  a.ex_off = c->zero_off;   // no salient key: no P pass, no output, statistics only
+  a.ap_rows = c->ap_rows;
+  a.ap_off = c->zero_off;
+  a.sal_rows = c->all_rows;
+  a.sal_off = c->zero_off;
+  a.max_rows_per_seq = 0;
+  a.scale = 1.f / sqrtf(static_cast<float>(m.head_dim));
+  a.row_lo = 0;
+  a.num_sms = ctx->num_sms;
+  a.rowflag = c->rowflag;
+  a.work_ctr = ctx->attn_ctr;
+  a.stats_cache = C.st;
+  a.mode = 2;
+  KL(ATTN, RET(attention_launch(a, ctx->stream)));
+  C.st_ok = true;
+  DY_CUDA(cudaGetLastError());
   return DYLLM_OK;
 }
 

@@ -125,6 +125,14 @@ struct AttnArgs {
   const uint8_t *rowflag = nullptr;  // [b*N] 1 = exact row
   bool full_only = false;       // FullStep: every row exact (ex_rows = identity), no approximate tiles
   int *work_ctr = nullptr;      // [2] fused kernel scheduler counters (ctx-owned, zero between launches)
+  // incremental softmax statistics (fused kernel)
+  float2 *stats_cache = nullptr;  // [b*N][H] per-layer (m c, l), written by every launch for its rows
+  const bf16 *Kxo = nullptr;      // [M_in][KVH*hd] compact keys of idx_in BEFORE this step's overwrite
+  bool inc = false;               // response-row statistics are current: type-3 tiles
+  int resp_lo = 0;                // first response position
+  int mode = 0;                   // 0 step, 1 fixup list, 2 statistics refresh
+  int *fix = nullptr;             // [1 + fix_cap] fixup list (ctx-owned, count zero between steps)
+  int fix_cap = 0;
 };
 int attention_launch(const AttnArgs &a, cudaStream_t st);
 int attention_fused_launch(const AttnArgs &a, cudaStream_t st);  // attn_fused.cu

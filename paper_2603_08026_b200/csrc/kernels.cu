@@ -143,7 +143,7 @@ __global__ void qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restr
                                 const int *__restrict__ M_ptr, int M_cap, const bf16 *__restrict__ bias, int N,
                                 int H, int KVH, int hd, const float2 *__restrict__ rope_cs, bf16 *__restrict__ Qc,
                                 bf16 *__restrict__ Kc, bf16 *__restrict__ Vc, bf16 *__restrict__ dV,
-                                bf16 *__restrict__ Qx, bf16 *__restrict__ Kx) {
+                                bf16 *__restrict__ Qx, bf16 *__restrict__ Kx, bf16 *__restrict__ Kxo) {
   pdl_wait();
   const int M = M_ptr ? *M_ptr : M_cap;
   const int qw = H * hd, kw = KVH * hd, W = qw + 2 * kw;
@@ -161,7 +161,7 @@ __global__ void qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restr
       // all loads of this thread first (one memory round trip): its q/k rotation pairs + table,
       // its V slice and the V cache slice it replaces
       int head = 0, k0 = 0, col = 0;
-      uint4 u1 = make_uint4(0, 0, 0, 0), u2 = u1, ub1 = u1, ub2 = u1, uv = u1, uvb = u1, uvo = u1;
+      uint4 u1 = make_uint4(0, 0, 0, 0), u2 = u1, ub1 = u1, ub2 = u1, uv = u1, uvb = u1, uvo = u1, uk1 = u1, uk2 = u1;
       float4 c4[4];
       if (has_qk) {
         head = v / hv;
@@ -175,6 +175,11 @@ __global__ void qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restr
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) c4[j] = reinterpret_cast<const float4 *>(cs + k0)[j];
+        if (Kxo && col >= qw) {  // the key row this step overwrites (incremental statistics)
+          const bf16 *ko = Kc + static_cast<int64_t>(r) * kw + (col - qw);
+          uk1 = *reinterpret_cast<const uint4 *>(ko);
+          uk2 = *reinterpret_cast<const uint4 *>(ko + half);
+        }
       }
       const int vc0 = v * 8;
       uint4 *vc = reinterpret_cast<uint4 *>(Vc + static_cast<int64_t>(r) * kw + vc0);
@@ -217,6 +222,11 @@ __global__ void qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restr
         if (cx) {
           *reinterpret_cast<uint4 *>(cx) = p1;
           *reinterpret_cast<uint4 *>(cx + half) = p2;
+        }
+        if (Kxo && col >= qw) {
+          bf16 *xo = Kxo + static_cast<int64_t>(i) * kw + (col - qw);
+          *reinterpret_cast<uint4 *>(xo) = uk1;
+          *reinterpret_cast<uint4 *>(xo + half) = uk2;
         }
       }
       // v: dV = v_new - V_cache (read before the overwrite), then V_cache <- v_new
@@ -825,12 +835,12 @@ void launch_rmsnorm_rows(const bf16 *src, const int *M_ptr, int M_cap, const bf1
 }
 void launch_qkv_post(const bf16 *qkv, const int *idx, const int *M_ptr, int M_cap, const bf16 *bias, int N, int H,
                      int KVH, int hd, const float2 *rope_cs, bf16 *Qc, bf16 *Kc, bf16 *Vc, bf16 *dV, bf16 *Qx,
-                     bf16 *Kx, cudaStream_t st) {
+                     bf16 *Kx, bf16 *Kxo, cudaStream_t st) {
   const int g = M_cap < 148 * 4 ? M_cap : 148 * 4;  // one row per CTA per pass; capped like grid_for
   const int work = std::max((H + KVH) * (hd / 16), KVH * hd / 8);  // vectors per row of each part
   const int threads = std::min(1024, std::max(32, (work + 31) / 32 * 32));
   DY_CUDA_LAUNCH(launch_k(qkv_post_kernel, dim3(g > 0 ? g : 1), dim3(threads), 0, st, 1, qkv, idx, M_ptr, M_cap, bias, N, H, KVH, hd, rope_cs, Qc, Kc, Vc,
-                                                 dV, Qx, Kx));
+                                                 dV, Qx, Kx, Kxo));
 }
 void launch_rope_table(float2 *cs, int N, int hd, double theta, cudaStream_t st) {
   DY_CUDA_LAUNCH(launch_k(rope_table_kernel, dim3(148), dim3(256), 0, st, 1, cs, N, hd, theta));

@@ -75,6 +75,7 @@ def _load():
         "dyllm_cache_tensor": (I, [P, I, I, PP, C.POINTER(C.c_int64)]),
         "dyllm_cache_copy": (I, [P, P, I, I, P, I, I]),
         "dyllm_cache_set_carried": (I, [P, P, P, P]),
+        "dyllm_cache_refresh_stats": (I, [P, P, I]),
         "dyllm_select_salient": (I, [P, I, I, I, I, P, P, F, I, P, P, P]),
         "dyllm_gemm_bf16": (I, [P, P, I, I, I, P, P, P, P, P]),
         "dyllm_unmask": (I, [P, P, P, P, P, P]),
@@ -99,7 +100,7 @@ def lib():
     return _lib
 
 
-OPT_SKINNY_GEMM, OPT_SKINNY_SPLIT, OPT_ATTN_FUSED, OPT_SKINNY_ONE_CHUNK, OPT_PDL = 1, 2, 3, 4, 5
+OPT_SKINNY_GEMM, OPT_SKINNY_SPLIT, OPT_ATTN_FUSED, OPT_SKINNY_ONE_CHUNK, OPT_PDL, OPT_ATTN_INC = 1, 2, 3, 4, 5, 6
 
 
 def set_option(option: int, value: int) -> int:
@@ -273,6 +274,9 @@ class Cache:
 
     def unmask(self, tokens, dec_pos, dec_tok):
         _check(_lib.dyllm_unmask(self.ctx.h, self.w.h, self.h, _ptr(tokens), _ptr(dec_pos), _ptr(dec_tok)))
+
+    def refresh_stats(self, layer):
+        _check(_lib.dyllm_cache_refresh_stats(self.ctx.h, self.h, layer))
 
     def set_carried(self, idx=None, off=None):
         _check(_lib.dyllm_cache_set_carried(self.ctx.h, self.h, _ptr(idx), _ptr(off)))

@@ -100,6 +100,9 @@ def _check_full_size(big, mode, frac_in, frac=0.10):
                  for _ in range(b)]
     cache = dy.Cache(ctx, w, run)
     _upload(dy, ctx, cache, host)
+    # current softmax statistics, as after the FullSteps: the bench's response tiles take the
+    # incremental path, full-input prompt tiles the dense one
+    cache.refresh_stats(0)
     h_before = cache.tensor(1, dy.H).clone()
     idx_d, off_d = pack_lists(idx_lists, N)
     out_d = torch.zeros(b * N, dtype=torch.int32, device="cuda")

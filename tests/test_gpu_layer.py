@@ -40,7 +40,13 @@ def test_full_step_caches_match_oracle(name):
 QK_STD = {"tiny": 0.18, "small128": 0.09, "small128_gqa": 0.09}   # sharper attention
 
 
-def _teacher_forced_layer(name, layer, mode, frac_in=0.4, seed=0, select_mode=0, frac=0.3):
+def _teacher_forced_layer(name, layer, mode, frac_in=0.4, seed=0, select_mode=0, frac=0.3, refresh=False,
+                          dominate=False):
+    """refresh: recompute the layer's softmax statistics on the GPU from the imported caches before
+    the step, so that response tiles take the incremental path — as in every
+    denoising step after the FullSteps. dominate: make one approximate row of sequence 0 attend
+    (head 0) almost only to a salient key whose old value is overwritten, so its incremental
+    normaliser cancels and its tile goes through the dense fixup launch."""
     m = Model(name, seed=seed, qk_std=QK_STD[name], select_mode=select_mode)
     cfg, run = m.cfg, m.run
     N = run.N
@@ -56,8 +62,16 @@ def _teacher_forced_layer(name, layer, mode, frac_in=0.4, seed=0, select_mode=0,
         x = st.H0 if layer == 0 else st.caches[layer - 1].H
         noise = rng.standard_normal((len(idx), cfg.d_model)) * 0.5 * np.abs(x[idx]).max(axis=1, keepdims=True)
         x[idx] = bf16_round(x[idx] + noise)
+    if dominate:
+        st, idx = states[0], idx_lists[0]
+        r = next(q for q in input_rows if q not in set(idx.tolist()))
+        j, hd = int(idx[0]), cfg.head_dim
+        lc = st.caches[layer]
+        lc.K[j, :hd] = bf16_round(lc.Q[r, :hd] * (24.0 / max(np.linalg.norm(lc.Q[r, :hd]) ** 2, 1e-12)) * np.sqrt(hd))
     cache = m.new_cache()
     import_states(m, cache, states)
+    if refresh:
+        cache.refresh_stats(layer)
     h_before = from_dev(cache.tensor(layer + 1, m.dyllm.H))
     # oracle reference from the same (rounded) state
     refs = []
@@ -123,6 +137,50 @@ def _teacher_forced_layer(name, layer, mode, frac_in=0.4, seed=0, select_mode=0,
 @pytest.mark.parametrize("mode", ["fi", "ro"])
 def test_layer_step_teacher_forced(name, layer, mode):
     _teacher_forced_layer(name, layer, mode)
+
+
+@pytest.mark.parametrize("name", ["small128", "small128_gqa"])
+@pytest.mark.parametrize("mode", ["fi", "ro"])
+@pytest.mark.parametrize("select_mode", [0, 1])
+def test_layer_step_incremental_statistics(name, mode, select_mode):
+    """Response tiles with current statistics: incremental normaliser == Alg. 4's dense one."""
+    _teacher_forced_layer(name, 1, mode, select_mode=select_mode, refresh=True)
+
+
+@pytest.mark.parametrize("mode", ["fi", "ro"])
+def test_layer_step_incremental_cancellation_fixup(mode):
+    """A row whose attention sat on an overwritten key: its tile is recomputed densely."""
+    _teacher_forced_layer("small128", 1, mode, refresh=True, dominate=True)
+
+
+def test_incremental_statistics_match_dense_over_steps():
+    """Many denoising steps with incremental statistics vs the same steps with dense normalisers
+    (DYLLM_OPT_ATTN_INC = 0): the same tokens and hidden states within the bf16 bar."""
+    outs = []
+    for inc in (1, 0):
+        m = Model("small128", qk_std=QK_STD["small128"], select_mode=1)
+        dy = m.dyllm
+        prev = dy.set_option(dy.OPT_ATTN_INC, inc)
+        try:
+            run = m.run
+            prompts = gen.prompt_tokens(21, run.batch, run.L_P, m.cfg.mask_id)
+            cache = m.new_cache()
+            toks = torch.tensor(np.stack([np.concatenate([p, np.full(run.L_R, m.cfg.mask_id)]) for p in prompts]),
+                                dtype=torch.int32).cuda()
+            dec_pos = torch.zeros(run.batch * run.n_u, dtype=torch.int32, device="cuda")
+            dec_tok = torch.zeros_like(dec_pos)
+            tau = np.full(m.cfg.n_layers, 0.25, np.float32)   # salient fraction per layer (D19)
+            for t in range(24):
+                cache.denoise_step(t, tau, toks, dec_pos, dec_tok)
+            torch.cuda.synchronize()
+            outs.append((toks.cpu().numpy(), from_dev(cache.tensor(m.cfg.n_layers, dy.H)),
+                         from_dev(cache.tensor(1, dy.CTX))))
+        finally:
+            dy.set_option(dy.OPT_ATTN_INC, prev)
+    (t1, h1, c1), (t0, h0, c0) = outs
+    assert np.array_equal(t1, t0)
+    assert row_rel_err(h1, h0).max() < TOL
+    assert row_rel_err(c1, c0).max() < TOL
 
 
 @pytest.mark.parametrize("name", ["tiny", "small128_gqa"])

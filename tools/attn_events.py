@@ -4,7 +4,7 @@ per-role event logs of CTAs 0-1 for the last layer of one denoising step of the 
     DYLLM_NVCC_FLAGS=-DDYLLM_ATTN_EVENTS=1 python -m paper_2603_08026_b200.build --force
     python tools/attn_events.py --mode ro|fi|full [--items 3]
 
-Codes: MMA 1/2 item (type 1/2), 10 QK begin, 11 S buffer free, 12 K tile ready, 13 QK issued,
+Codes: MMA 1/2/3 item (type 1/2/3), 10 QK begin, 11 S buffer free, 12 K tile ready, 13 QK issued,
 20 PV begin, 21 P ready, 22 V/acc ready, 23 PV issued. Softmax (warp 2) 1/2 item, 30 S wait,
 31 S ready, 32 S read (buffer released), 33 S tile done, 40 P-pass S wait, 41 ready, 42 P stored,
 50 acc wait, 51 acc ready, 52 epilogue done. Producer 60 K slot wait, 61 K issued. V 70, 71.
@@ -27,6 +27,7 @@ ap.add_argument("--mode", default="ro")
 ap.add_argument("--frac", type=float, default=0.10)
 ap.add_argument("--items", type=int, default=3)
 ap.add_argument("--ghz", type=float, default=1.9)
+ap.add_argument("--kind", type=int, default=0, help="timeline from the first item of this type (0: first item)")
 a = ap.parse_args()
 cfg, run = configs.preset("llada8b")
 run = replace(run, select_mode=1)
@@ -88,9 +89,9 @@ for role in range(4):
             print(f"   {name:18s} total {sums[name]:8.1f} us  n={cnt[name]:5d}  mean {sums[name] / cnt[name] * 1e3:7.0f} ns")
     if role in (0, 1):
         # per-item durations
-        starts = [(t, code) for code, t in ev if code in (1, 2)]
+        starts = [(t, code) for code, t in ev if code in (1, 2, 3)]
         durs = [((starts[i + 1][0] - starts[i][0]) * cyc, starts[i][1]) for i in range(len(starts) - 1)]
-        for kind in (1, 2):
+        for kind in (1, 2, 3):
             d = [x for x, k in durs if k == kind]
             if d:
                 print(f"   items type {kind}: n={len(d)} mean {np.mean(d):.2f} us  min {np.min(d):.2f}  max {np.max(d):.2f}")
@@ -99,10 +100,14 @@ mm = decode(raw[0, 0])
 sm = decode(raw[0, 1])
 t0 = min(mm[0][1], sm[0][1])
 merged = sorted([(t, "M", c) for c, t in mm] + [(t, "S", c) for c, t in sm])
+if a.kind:
+    k0 = next((i for i, (t, r, c) in enumerate(merged) if r == "M" and c == a.kind), 0)
+    t0 = merged[k0][0]
+    merged = merged[k0:]
 n_items = 0
 print("== timeline (first items): time_us role code")
 for t, r, c in merged:
-    if r == "M" and c in (1, 2):
+    if r == "M" and c in (1, 2, 3):
         n_items += 1
         if n_items > a.items:
             break
