@@ -218,7 +218,7 @@ uint64_t dyllm_launch_count(void);
  * up to fp32 summation order. */
 /* DYLLM_OPT_ATTN_FUSED (default 1): head_dim 128 uses the fused tcgen05 attention kernel
  * (attn_fused.cu); 0 = the two-kernel path (tcgen05 row statistics + mma.sync P.V). */
-/* DYLLM_OPT_SKINNY_ONE_CHUNK (default -1 = automatic): largest device row count the skinny kernel
+/* DYLLM_OPT_SKINNY_ONE_CHUNK (default 0 = automatic): largest device row count the skinny kernel
  * keeps in a single activation chunk (above it: chunks of <= 256 rows). */
 /* DYLLM_OPT_PDL (default 1): launch every kernel with programmatic dependent launch (a kernel's
  * setup overlaps its predecessor; each kernel waits for its predecessor before touching memory). */

@@ -56,7 +56,8 @@ struct FaParams {
   float c;                  // softmax scale * log2(e)
   const int *ex_off;        // [b+1]: exact rows (= salient keys) of each sequence, packed
   const int *ex_rows;       // packed row ids of the exact rows
-  const uint8_t *rowflag;   // [b*N]: 1 = exact row (type-1 tiles leave it to type 2)
+  const uint32_t *rowflag;  // [b*N]: == tag for the exact rows of this step (type-1 tiles leave them to type 2)
+  uint32_t tag;
   const bf16 *C_cache;
   bf16 *C_out;
   int *work_ctr;              // [2] dynamic scheduler: next item, finished CTAs (zero between launches)
@@ -510,12 +511,12 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       const bool rvalid = r < it.nrows;
       // type 1 writes approximate rows only: fetch the row kind early (its latency hides under pass S)
       const int64_t orow = it.type2 ? (rvalid ? p.ex_rows[it.q_row + r] : 0) : static_cast<int64_t>(it.q_row) + r;
-      const bool write_row = rvalid && (it.type2 || (it.passP && !p.rowflag[orow]));
+      const bool write_row = rvalid && (it.type2 || (it.passP && p.rowflag[orow] != p.tag));
       ev(it.inc ? 3 : it.type2 ? 2 : 1);
       float acc[FA_CW];
       float oscale;
       // statistics entry of this row (exact rows' entries belong to the type-2 items)
-      const bool own_stats = p.stats != nullptr && rvalid && hh == 0 && (it.type2 || p.mode == 2 || !p.rowflag[orow]);
+      const bool own_stats = p.stats != nullptr && rvalid && hh == 0 && (it.type2 || p.mode == 2 || p.rowflag[orow] != p.tag);
       const int64_t srow = orow * p.H + it.h;
       if (it.inc) {
         // ---- type 3, incremental statistics (exact up to rounding): only the salient
@@ -951,6 +952,7 @@ int attention_fused_launch(const AttnArgs &a, cudaStream_t st) {
   p.ex_off = a.ex_off;
   p.ex_rows = a.ex_rows;
   p.rowflag = a.rowflag;
+  p.tag = a.row_tag;
   p.C_cache = a.C_cache;
   p.C_out = a.C_out;
   p.events = g_attn_events;

@@ -119,7 +119,8 @@ struct dyllm_cache {
   std::vector<LayerC> L;
   bf16 *H0;
   bf16 *Xn, *qkv, *dV, *Qx, *Kx, *Kxo, *Cn, *Cg, *h, *hn, *act, *ffo, *Xf;
-  uint8_t *rowflag;
+  uint32_t *rowflag;     // [rows] == row_tag: exact row (idx_in) of the current layer step
+  uint32_t row_tag = 0;  // advanced by every layer step (no clearing pass over rowflag)
   float4 *partials;
   int *lst[2], *lst_off[2];
   int *carried, *carried_off;
@@ -467,6 +468,7 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
   const bool ok = cudaMemsetAsync(c->dV, 0, rows * kw * 2, st) == cudaSuccess &&
                   cudaMemsetAsync(c->Kx, 0, rows * kw * 2, st) == cudaSuccess &&
                   cudaMemsetAsync(c->Kxo, 0, rows * kw * 2, st) == cudaSuccess &&
+                  cudaMemsetAsync(c->rowflag, 0, rows * sizeof(uint32_t), st) == cudaSuccess &&
                   cudaMemsetAsync(c->Qx, 0, rows * qw * 2, st) == cudaSuccess &&
                   cudaMemsetAsync(c->zero_off, 0, (r->batch + 1) * sizeof(int), st) == cudaSuccess;
   if (!ok) {
@@ -494,7 +496,7 @@ void dyllm_cache_destroy(dyllm_cache *c) {
 // ------------------------------------------------------------------ step internals
 static int gemm(dyllm_ctx *ctx, const int *M_ptr, int M_cap, int N, int K, const bf16 *A, const bf16 *W, bf16 *D,
                 int ldd, int epi, const bf16 *resid = nullptr, int ldr = 0, const int *resid_rows = nullptr,
-                const bf16 *bias = nullptr, float4 *partials = nullptr) {
+                const bf16 *bias = nullptr, float4 *partials = nullptr, const int *out_rows = nullptr) {
   GemmCall g;
   g.M_ptr = M_ptr;
   g.M_cap = M_cap;
@@ -509,6 +511,7 @@ static int gemm(dyllm_ctx *ctx, const int *M_ptr, int M_cap, int N, int K, const
   g.resid_rows = resid_rows;
   g.bias = bias;
   g.partials = partials;
+  g.out_rows = out_rows;
   g.epi = epi;
   g.ws = ctx->sk_ws;
   g.ctr = ctx->sk_ctr;
@@ -528,7 +531,10 @@ static int post_attention(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c
   KL(O_GEMM, RET(gemm(ctx, M_ptr, rows, d, qw, A_c, L.wo, c->h, d, res ? EPI_RESID : EPI_BF16, Hprev, d, resid_rows)));
   KL(OTHER, launch_rmsnorm_rows(c->h, M_ptr, rows, L.g_ffn, m.rms_eps, c->hn, d, st));
   KL(GU_GEMM, RET(gemm(ctx, M_ptr, rows, 2 * F, d, c->hn, L.wgu, c->act, F, EPI_SWIGLU)));
-  KL(DOWN_GEMM, RET(gemm(ctx, M_ptr, rows, d, F, c->act, L.wd, out, d, res ? EPI_RESID : EPI_BF16, c->h, d, nullptr)));
+  // the down projection writes its rows straight into H_l at their row ids (scatter-back fused,
+  // rows outside the list keep their cached output)
+  KL(DOWN_GEMM, RET(gemm(ctx, M_ptr, rows, d, F, c->act, L.wd, out, d, res ? EPI_RESID : EPI_BF16, c->h, d, nullptr,
+                         nullptr, nullptr, resid_rows)));
   return DYLLM_OK;
 }
 
@@ -546,7 +552,7 @@ static int full_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c
     KL(GATHER, launch_gather_rmsnorm(Hprev, nullptr, nullptr, rows, L.g_attn, m.rms_eps, c->Xn, d, st));
     KL(QKV_GEMM, RET(gemm(ctx, nullptr, rows, qw + 2 * kw, d, c->Xn, L.wqkv, c->qkv, qw + 2 * kw, EPI_BF16)));
     KL(QKV_POST, launch_qkv_post(c->qkv, nullptr, nullptr, rows, L.bqkv, c->N, m.n_heads, m.n_kv_heads, m.head_dim,
-                                 c->rope_cs, C.Q, C.K, C.V, nullptr, nullptr, nullptr, nullptr, st));
+                                 c->rope_cs, C.Q, C.K, C.V, nullptr, nullptr, nullptr, nullptr, nullptr, 0u, st));
     AttnArgs a{};
     a.batch = c->r.batch;
     a.N = c->N;
@@ -602,19 +608,22 @@ static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *
   const bf16 *Hprev = l == 0 ? c->H0 : c->L[l - 1].H;
   cudaStream_t st = ctx->stream;
   const int *M_in = off_in + b;
-  // exact rows = idx_in; approximate rows = input rows \ idx_in
-  KL(OTHER, launch_approx_rows(idx_in, off_in, b, N, row_lo, c->ap_rows, c->ap_off, c->rowflag, st));
+  const bool fused = m.head_dim == 128 && g_attn_fused_enabled;
+  const uint32_t tag = ++c->row_tag;
+  // exact rows = idx_in; approximate rows = input rows \ idx_in: the fused path marks the exact
+  // rows in qkv_post (row tag), the other attention kernels take an explicit approximate list
+  if (!fused) KL(OTHER, launch_approx_rows(idx_in, off_in, b, N, row_lo, c->ap_rows, c->ap_off, st));
   // a1 + a2: RMSNorm(x[idx_in]) -> QKV projection of the changed rows
   KL(GATHER, launch_gather_rmsnorm(Hprev, idx_in, M_in, rows, L.g_attn, m.rms_eps, c->Xn, d, st));
   KL(QKV_GEMM, RET(gemm(ctx, M_in, rows, qw + 2 * kw, d, c->Xn, L.wqkv, c->qkv, qw + 2 * kw, EPI_BF16)));
   // a3: RoPE, dV (before overwrite), in-place K/V/Q cache rows
-  const bool fused = m.head_dim == 128 && g_attn_fused_enabled;
   // incremental statistics need the overwritten key rows (Kxo) and current
   // statistics; under the literal layer-1 policy, decoded rows outside idx_in get a new Q at
   // layer 0 without a statistics update, so that layer stays dense
   const bool inc = fused && g_attn_inc_enabled && C.st_ok && !(l == 0 && c->r.layer1_policy == 0);
   KL(QKV_POST, launch_qkv_post(c->qkv, idx_in, M_in, rows, L.bqkv, N, m.n_heads, m.n_kv_heads, m.head_dim,
-                               c->rope_cs, C.Q, C.K, C.V, c->dV, c->Qx, c->Kx, inc ? c->Kxo : nullptr, st));
+                               c->rope_cs, C.Q, C.K, C.V, c->dV, c->Qx, c->Kx, inc ? c->Kxo : nullptr,
+                               fused ? c->rowflag : nullptr, tag, st));
   // a4: exact rows + approximate rows (Alg. 4) -> Cn
   AttnArgs a{};
   a.batch = b;
@@ -642,6 +651,7 @@ static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *
   a.Qx = c->Qx;
   a.Kx = c->Kx;
   a.rowflag = c->rowflag;
+  a.row_tag = tag;
   a.work_ctr = ctx->attn_ctr;
   a.stats_cache = fused ? C.st : nullptr;
   a.Kxo = c->Kxo;
@@ -662,12 +672,11 @@ static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *
   const bool delta = attention_writes_delta(m.head_dim);  // fused kernel: Cn = dC for approximate rows
   KL(SELECT, launch_select(c->Cn, C.C, b, N, row_lo, qw, fmode ? 2.f : tau, c->r.cmp, fmode ? tau : -1.f, idx_out,
                            off_out, (fmode && !sim) ? c->sim : sim, ctx->masks, ctx->ticket, counts,
-                           delta ? c->rowflag : nullptr, delta ? off_in : nullptr, st));
+                           delta ? c->rowflag : nullptr, tag, delta ? off_in : nullptr, st));
   const int *M_out = off_out + b;
   // a6 + a7 on idx_out, a8 scatter-back into H_l (other rows keep FFN_OUT_cache)
   KL(GATHER, launch_gather_rows(C.C, idx_out, M_out, rows, c->Cg, qw, st));
-  RET(post_attention(ctx, w, c, l, M_out, c->Cg, Hprev, idx_out, c->ffo));
-  KL(SCATTER, launch_scatter_rows(c->ffo, idx_out, M_out, rows, C.H, d, st));
+  RET(post_attention(ctx, w, c, l, M_out, c->Cg, Hprev, idx_out, C.H));
   DY_CUDA(cudaGetLastError());
   return DYLLM_OK;
 }
@@ -969,7 +978,7 @@ int dyllm_select_salient(dyllm_ctx *ctx, int batch, int N, int row_lo, int width
   RET(sticky(ctx));
   KL(SELECT, launch_select(static_cast<const bf16 *>(d_c_new), static_cast<bf16 *>(d_c_cache), batch, N, row_lo, width,
                            tau, cmp, -1.f, d_idx_out, d_off_out, d_sim_out, ctx->masks, ctx->ticket, nullptr, nullptr,
-                           nullptr, ctx->stream));
+                           0u, nullptr, ctx->stream));
   DY_CUDA(cudaGetLastError());
   return DYLLM_OK;
 }

@@ -49,6 +49,7 @@ struct GemmParams {
   int ldr;
   const int *resid_rows;
   const bf16 *bias;
+  const int *out_rows;  // nullable: destination row of each output row (fused scatter-back, a8)
   float4 *partials;
   int m_skip_le;
 };
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tmem_ld32(tbase + gcol + kGuIl, u);
           if (row_ok) {
             const int col = nb * (BN / 2) + c0;
-            bf16 *dst = p.D + static_cast<int64_t>(row) * p.ldd + col;
+            bf16 *dst = p.D + static_cast<int64_t>(p.out_rows ? p.out_rows[row] : row) * p.ldd + col;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               float o[8];
@@ -233,7 +234,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tmem_ld32(tbase + c0, v);
           if (row_ok) {
             const int colb = nb * BN + c0;
-            bf16 *dst = p.D + static_cast<int64_t>(row) * p.ldd + colb;
+            bf16 *dst = p.D + static_cast<int64_t>(p.out_rows ? p.out_rows[row] : row) * p.ldd + colb;
             const bf16 *res = nullptr;
             if constexpr (EPI == EPI_RESID) {
               const int rr = p.resid_rows ? p.resid_rows[row] : row;
@@ -351,7 +352,8 @@ static int launch_t(const GemmCall &g, int num_sms, cudaStream_t st) {
   if (rc) return rc;
   rc = make_tmap(&tb, g.W, g.N, g.K, BN);
   if (rc) return rc;
-  GemmParams p{g.M_ptr, g.M_cap, g.N, g.K, g.D, g.ldd, g.resid, g.ldr, g.resid_rows, g.bias, g.partials, g.m_skip_le};
+  GemmParams p{g.M_ptr, g.M_cap, g.N, g.K, g.D, g.ldd, g.resid, g.ldr, g.resid_rows, g.bias, g.out_rows, g.partials,
+               g.m_skip_le};
   const int max_tiles = ((g.M_cap + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   const int grid = max_tiles < num_sms ? max_tiles : num_sms;
   DY_CUDA(launch_k(kern, dim3(grid), dim3(kGemmThreads), C::SMEM_BYTES, st, 1, ta, tb, p));

@@ -113,6 +113,7 @@ struct SkinnyParams {
   int ldr;
   const int *resid_rows;
   const bf16 *bias;
+  const int *out_rows;  // nullable: destination row of each output row (fused scatter-back, a8)
   float *ws;   // split-K partials: [2*P slots][512 m][256 weight rows] fp32
   int *ctr;    // per (item, rank) arrival counters, zero between launches
   int P_max;   // co-resident pairs of the grid (the partition uses P <= P_max of them)
@@ -423,7 +424,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             const float4 g = r[i], u = r[4 + i];
             const float o0 = g.x / (1.f + __expf(-g.x)) * u.x, o1 = g.y / (1.f + __expf(-g.y)) * u.y;
             const float o2 = g.z / (1.f + __expf(-g.z)) * u.z, o3 = g.w / (1.f + __expf(-g.w)) * u.w;
-            *reinterpret_cast<uint2 *>(p.D + static_cast<int64_t>(m) * p.ldd + ch) =
+            *reinterpret_cast<uint2 *>(p.D + static_cast<int64_t>(p.out_rows ? p.out_rows[m] : m) * p.ldd + ch) =
                 make_uint2(pack2(o0, o1), pack2(o2, o3));
           }
         }
@@ -448,7 +449,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
               const float2 r23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&rv.y));
               o[0] += r01.x; o[1] += r01.y; o[2] += r23.x; o[3] += r23.y;
             }
-            *reinterpret_cast<uint2 *>(p.D + static_cast<int64_t>(m) * p.ldd + n) =
+            *reinterpret_cast<uint2 *>(p.D + static_cast<int64_t>(p.out_rows ? p.out_rows[m] : m) * p.ldd + n) =
                 make_uint2(pack2(o[0], o[1]), pack2(o[2], o[3]));
           }
         }
@@ -654,15 +655,16 @@ static int launch_skinny_t(const GemmCall &g, int num_sms, cudaStream_t st) {
   if (rc) return rc;
   // the tile count (hence the split and the number of pairs used) depends on the device-side row
   // count: the kernel derives them; the grid is every co-resident pair
-  SkinnyParams p{g.M_ptr, g.M_cap, g.N, g.K, g.D, g.ldd, g.resid, g.ldr, g.resid_rows, g.bias, g.ws, g.ctr, max_pairs,
-                 g_skinny_trace, g_skinny_split, g_skinny_one_chunk};
+  SkinnyParams p{g.M_ptr, g.M_cap, g.N, g.K, g.D, g.ldd, g.resid, g.ldr, g.resid_rows, g.bias, g.out_rows, g.ws, g.ctr,
+                 max_pairs,
+                 g_skinny_trace, g_skinny_split, g_skinny_one_chunk > 0 ? g_skinny_one_chunk : -1};
   DY_CUDA(launch_k(kern, dim3(2 * max_pairs), dim3(SK_THREADS), SK_SMEM, st, 2, maps, p));
   return DYLLM_OK;
 }
 
 unsigned long long *g_skinny_trace = nullptr;
 int g_skinny_split = 0;
-int g_skinny_one_chunk = -1;  // -1: automatic
+int g_skinny_one_chunk = 0;  // 0: automatic
 
 bool skinny_eligible(const GemmCall &g) {
   return g.N % 256 == 0 && g.K % SK_KB == 0 && (g.epi == EPI_BF16 || g.epi == EPI_RESID || g.epi == EPI_SWIGLU);

@@ -80,6 +80,7 @@ struct GemmCall {
   const bf16 *resid = nullptr; // EPI_RESID: residual rows
   int ldr = 0;
   const int *resid_rows = nullptr;  // nullable: residual row index per output row
+  const int *out_rows = nullptr;    // nullable: destination row of each output row in D (scatter)
   const bf16 *bias = nullptr;       // nullable [N]
   float4 *partials = nullptr;       // EPI_LMHEAD: [M_cap][n_tiles] (max, sumexp, argmax, 0)
   int epi = EPI_BF16;
@@ -122,7 +123,8 @@ struct AttnArgs {
   // fused head_dim-128 kernel (attn_fused.cu)
   const bf16 *Qx = nullptr;     // [M_in][H*hd] compact new queries of the exact rows (aligned with ex_rows)
   const bf16 *Kx = nullptr;     // [M_in][KVH*hd] compact new keys of the salient rows (aligned with dV)
-  const uint8_t *rowflag = nullptr;  // [b*N] 1 = exact row
+  const uint32_t *rowflag = nullptr;  // [b*N] == row_tag: exact row (in idx_in) of this layer step
+  uint32_t row_tag = 0;
   bool full_only = false;       // FullStep: every row exact (ex_rows = identity), no approximate tiles
   int *work_ctr = nullptr;      // [2] fused kernel scheduler counters (ctx-owned, zero between launches)
   // incremental softmax statistics (fused kernel)

@@ -143,7 +143,8 @@ __global__ void qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restr
                                 const int *__restrict__ M_ptr, int M_cap, const bf16 *__restrict__ bias, int N,
                                 int H, int KVH, int hd, const float2 *__restrict__ rope_cs, bf16 *__restrict__ Qc,
                                 bf16 *__restrict__ Kc, bf16 *__restrict__ Vc, bf16 *__restrict__ dV,
-                                bf16 *__restrict__ Qx, bf16 *__restrict__ Kx, bf16 *__restrict__ Kxo) {
+                                bf16 *__restrict__ Qx, bf16 *__restrict__ Kx, bf16 *__restrict__ Kxo,
+                                uint32_t *__restrict__ rowflag, uint32_t tag) {
   pdl_wait();
   const int M = M_ptr ? *M_ptr : M_cap;
   const int qw = H * hd, kw = KVH * hd, W = qw + 2 * kw;
@@ -154,6 +155,7 @@ __global__ void qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restr
     const int r = idx ? idx[i] : i;
     const int pos = r % N;
     const bf16 *src = qkv + static_cast<int64_t>(i) * W;
+    if (rowflag && threadIdx.x == 0) rowflag[r] = tag;  // exact row of this layer step (fused attention)
     const float2 *cs = rope_cs + static_cast<int64_t>(pos) * half;
     for (int rd = 0; rd < rounds; ++rd) {
       const int v = rd * blockDim.x + threadIdx.x;
@@ -272,7 +274,7 @@ __global__ void rope_table_kernel(float2 *__restrict__ cs, int N, int hd, double
 // (exact rows = idx_in itself). One CTA per sequence. ap_off[s] = s*L - off_in[s].
 __global__ void approx_rows_kernel(const int *__restrict__ idx_in, const int *__restrict__ off_in, int N,
                                    int row_lo, int *__restrict__ ap_rows, int *__restrict__ ap_off, int batch,
-                                   uint8_t *__restrict__ rowflag) {
+                                   int) {
   pdl_wait();
   extern __shared__ uint8_t flag[];
   __shared__ int warp_cnt[32];
@@ -283,8 +285,6 @@ __global__ void approx_rows_kernel(const int *__restrict__ idx_in, const int *__
   const int b0 = off_in[s], b1 = off_in[s + 1];
   for (int j = b0 + threadIdx.x; j < b1; j += blockDim.x) flag[idx_in[j] - s * N] = 1;
   __syncthreads();
-  if (rowflag)  // per-row kind for the fused attention kernel: 1 = exact (in idx_in)
-    for (int p = threadIdx.x; p < N; p += blockDim.x) rowflag[static_cast<int64_t>(s) * N + p] = flag[p];
   int base = s * L - b0;
   if (threadIdx.x == 0) {
     ap_off[s] = base;
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
     const bf16 *__restrict__ c_new, bf16 *__restrict__ c_cache, int N, int row_lo, int width, float tau,
     int cmp, float frac, int *__restrict__ idx_out, int *__restrict__ off_out, float *__restrict__ sim_out,
     unsigned *__restrict__ masks, unsigned *__restrict__ ticket, int *__restrict__ counts_out,
-    const uint8_t *__restrict__ rowflag, const int *__restrict__ dl_off) {
+    const uint32_t *__restrict__ rowflag, uint32_t tag, const int *__restrict__ dl_off) {
   pdl_wait();
   __shared__ unsigned row_flag[kSelRowsPerCta];
   __shared__ bool is_last;
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
       // salient key, dC = 0) is formed here from the C_cache row this kernel reads anyway
       bool take_new = true, add = false;
       if (rowflag) {
-        take_new = rowflag[r] != 0;
+        take_new = rowflag[r] == tag;
         add = !take_new && dl_off[s + 1] > dl_off[s];
       }
       float dot = 0.f, na = 0.f, nb = 0.f;
@@ -835,19 +835,19 @@ void launch_rmsnorm_rows(const bf16 *src, const int *M_ptr, int M_cap, const bf1
 }
 void launch_qkv_post(const bf16 *qkv, const int *idx, const int *M_ptr, int M_cap, const bf16 *bias, int N, int H,
                      int KVH, int hd, const float2 *rope_cs, bf16 *Qc, bf16 *Kc, bf16 *Vc, bf16 *dV, bf16 *Qx,
-                     bf16 *Kx, bf16 *Kxo, cudaStream_t st) {
+                     bf16 *Kx, bf16 *Kxo, uint32_t *rowflag, uint32_t tag, cudaStream_t st) {
   const int g = M_cap < 148 * 4 ? M_cap : 148 * 4;  // one row per CTA per pass; capped like grid_for
   const int work = std::max((H + KVH) * (hd / 16), KVH * hd / 8);  // vectors per row of each part
   const int threads = std::min(1024, std::max(32, (work + 31) / 32 * 32));
   DY_CUDA_LAUNCH(launch_k(qkv_post_kernel, dim3(g > 0 ? g : 1), dim3(threads), 0, st, 1, qkv, idx, M_ptr, M_cap, bias, N, H, KVH, hd, rope_cs, Qc, Kc, Vc,
-                                                 dV, Qx, Kx, Kxo));
+                                                 dV, Qx, Kx, Kxo, rowflag, tag));
 }
 void launch_rope_table(float2 *cs, int N, int hd, double theta, cudaStream_t st) {
   DY_CUDA_LAUNCH(launch_k(rope_table_kernel, dim3(148), dim3(256), 0, st, 1, cs, N, hd, theta));
 }
 void launch_approx_rows(const int *idx_in, const int *off_in, int batch, int N, int row_lo, int *ap_rows,
-                        int *ap_off, uint8_t *rowflag, cudaStream_t st) {
-  DY_CUDA_LAUNCH(launch_k(approx_rows_kernel, dim3(batch), dim3(256), N, st, 1, idx_in, off_in, N, row_lo, ap_rows, ap_off, batch, rowflag));
+                        int *ap_off, cudaStream_t st) {
+  DY_CUDA_LAUNCH(launch_k(approx_rows_kernel, dim3(batch), dim3(256), N, st, 1, idx_in, off_in, N, row_lo, ap_rows, ap_off, batch, 0));
 }
 void launch_build_list(int mode, const int *carried, const int *carried_off, const int *dec_pos, int n_u, int policy,
                        int batch, int N, int row_lo, int resp_lo, int *out, int *out_off, cudaStream_t st) {
@@ -856,11 +856,11 @@ void launch_build_list(int mode, const int *carried, const int *carried_off, con
 }
 void launch_select(const bf16 *c_new, bf16 *c_cache, int batch, int N, int row_lo, int width, float tau, int cmp,
                    float frac, int *idx_out, int *off_out, float *sim_out, unsigned *masks, unsigned *ticket,
-                   int *counts, const uint8_t *rowflag, const int *dl_off, cudaStream_t st) {
+                   int *counts, const uint32_t *rowflag, uint32_t tag, const int *dl_off, cudaStream_t st) {
   const int L = N - row_lo;
   dim3 grid((L + kSelRowsPerCta - 1) / kSelRowsPerCta, batch);
   DY_CUDA_LAUNCH(launch_k(select_salient_kernel, dim3(grid), dim3(kSelThreads), 0, st, 1, c_new, c_cache, N, row_lo, width, tau, cmp, frac, idx_out, off_out,
-                                              sim_out, masks, ticket, counts, rowflag, dl_off));
+                                              sim_out, masks, ticket, counts, rowflag, tag, dl_off));
 }
 void launch_lm_candidates(const int *tokens, int batch, int L_P, int L_R, int block, int mask_id, int *rows, int *off,
                           cudaStream_t st) {

@@ -19,15 +19,16 @@ void launch_rmsnorm_rows(const bf16 *src, const int *M_ptr, int M_cap, const bf1
                          cudaStream_t st);
 void launch_qkv_post(const bf16 *qkv, const int *idx, const int *M_ptr, int M_cap, const bf16 *bias, int N, int H,
                      int KVH, int hd, const float2 *rope_cs, bf16 *Qc, bf16 *Kc, bf16 *Vc, bf16 *dV, bf16 *Qx,
-                     bf16 *Kx, bf16 *Kxo, cudaStream_t st);
+                     bf16 *Kx, bf16 *Kxo, uint32_t *rowflag, uint32_t tag,
+                     cudaStream_t st);
 void launch_rope_table(float2 *cs, int N, int hd, double theta, cudaStream_t st);
 void launch_approx_rows(const int *idx_in, const int *off_in, int batch, int N, int row_lo, int *ap_rows,
-                        int *ap_off, uint8_t *rowflag, cudaStream_t st);
+                        int *ap_off, cudaStream_t st);
 void launch_build_list(int mode, const int *carried, const int *carried_off, const int *dec_pos, int n_u, int policy,
                        int batch, int N, int row_lo, int resp_lo, int *out, int *out_off, cudaStream_t st);
 void launch_select(const bf16 *c_new, bf16 *c_cache, int batch, int N, int row_lo, int width, float tau, int cmp,
                    float frac, int *idx_out, int *off_out, float *sim_out, unsigned *masks, unsigned *ticket,
-                   int *counts, const uint8_t *rowflag, const int *dl_off, cudaStream_t st);
+                   int *counts, const uint32_t *rowflag, uint32_t tag, const int *dl_off, cudaStream_t st);
 void launch_lm_candidates(const int *tokens, int batch, int L_P, int L_R, int block, int mask_id, int *rows, int *off,
                           cudaStream_t st);
 void launch_lm_select_commit(const float4 *partials, int n_tiles, const int *rows, const int *off, int batch, int n_u,

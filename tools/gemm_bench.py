@@ -28,7 +28,7 @@ def main():
     ap.add_argument("--skinny", type=int, default=1)
     ap.add_argument("--split", default="0", help="comma list of skinny split granularities (0 = auto)")
     ap.add_argument("--which", default="qkv,o,gu,down")
-    ap.add_argument("--one-chunk", type=int, default=-1, help="largest M in one activation chunk (-1 auto)")
+    ap.add_argument("--one-chunk", type=int, default=0, help="largest M in one activation chunk (0 auto)")
     a = ap.parse_args()
     cfg, _ = configs.preset(a.config)
     d, F = cfg.d_model, cfg.d_ff
