@@ -110,6 +110,23 @@ def layer_bytes_flops(cfg):
     return {"qkv_w": 2 * d * (qw + 2 * kw), "o_w": 2 * d * qw, "gu_w": 2 * d * 2 * F, "down_w": 2 * d * F}
 
 
+def measured_traffic(cls, sparse_t, run):
+    """DRAM bytes per launch of a kernel class from the committed ncu --set full captures
+    (profiles/ncu_traffic.json), weighted by the response-only / full-input launch mix."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        t = json.load(open(p)).get(cls)
+    except (OSError, ValueError):
+        return None
+    if not t:
+        return None
+    n_fi = sum(1 for x in sparse_t if x % run.full_period == 0)
+    n_ro = len(sparse_t) - n_fi
+    if "fi" not in t:
+        return t.get("ro")
+    return (n_ro * t["ro"] + n_fi * t["fi"]) / max(n_ro + n_fi, 1)
+
+
 # ----------------------------------------------------------------------------- CPU oracle leg
 def cpu_oracle_sample(cfg, run, seconds: float, frac: float, seed: int = 0):
     """Time the oracle (as it stands) on one sequence of the bench workload: one response-only
@@ -259,8 +276,10 @@ def algo_cost(cls, cfg, run, M_in, M_out, L_tot):
     if cls == "down_gemm":
         return 2 * F * d + M_out * 2 * (F + 2 * d), 2.0 * M_out * F * d
     if cls == "attn":
+        # K and V of every sequence once, the input rows' queries in and contexts out (C_cache is
+        # read by the selection kernel, which forms C_new = C_cache + dC)
         sal = M_in / b
-        return (b * N * 2 * kw * 2 + L_tot * 3 * qw * 2,
+        return (b * N * 2 * kw * 2 + L_tot * 2 * qw * 2,
                 2.0 * L_tot * N * qw + 2.0 * M_in * N * qw + 2.0 * (L_tot - M_in) * sal * qw * 2)
     if cls == "select":
         return L_tot * 3 * qw * 2, 6.0 * L_tot * qw
@@ -429,7 +448,7 @@ def main():
                             "avg_us": round(float(v.mean()) * 1000.0, 2), "launches": int(len(v))}
         dom = max(per_class, key=lambda k: totals[k])
         roof = dict(per_class[dom])
-        roof.update({"kernel": dom, "traffic": None,
+        roof.update({"kernel": dom, "traffic": measured_traffic(dom, sparse_t, run),
                      "peak_source": src + (" sustained bf16" if roof["unit"] == "TFLOP/s" else " HBM copy")})
         full_ms = sum(float(v.sum()) for k, v in kc.items() if k.startswith("full_")) / max(run.T_full * nsteps, 1)
         full_tok_s = world * b * run.L_R / (T * full_ms / 1000.0) if full_ms > 0 else None
