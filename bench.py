@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="llada8b")
     ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (0 = config)")
+    ap.add_argument("--n-u", type=int, default=0, help="tokens unmasked per step (0 = config; f2: 2, 4)")
     ap.add_argument("--frac", type=float, default=0.10, help="target salient fraction for tau calibration")
     ap.add_argument("--tau", type=float, default=None, help="fixed tau for all layers (skips calibration)")
     ap.add_argument("--select-mode", default="fraction", choices=["fraction", "tau"],
@@ -308,6 +309,8 @@ def main():
     cfg, run = configs.preset(args.config)
     if args.batch:
         run = replace(run, batch=args.batch)
+    if args.n_u:
+        run = replace(run, n_u=args.n_u)
     fmode = args.select_mode == "fraction"
     run = replace(run, select_mode=1 if fmode else 0)
     b, N = run.batch, run.N
