@@ -73,7 +73,8 @@ struct FaParams {
 struct FaItem {
   int s, h, kvh, nrows, q_row, off, nkP, xc;
   bool type2, passP;
-  bool inc;  // type 3: incremental statistics (response tile, <= 128 salient keys, current stats)
+  bool inc;     // type 3: incremental statistics (response tile, <= 128 salient keys, current stats)
+  bool single;  // type 2 in one pass (online softmax); the fixup launch re-runs type 2 in two passes
 };
 
 // Item decode from its index and the exact-row range (off, e) of its sequence (the producer reads
@@ -97,6 +98,7 @@ __device__ __forceinline__ FaItem fa_item(const FaParams &p, int w, int off, int
     it.passP = e > 0 && p.mode != 2;
     it.nkP = e;
     it.inc = p.inc && p.mode == 0 && e > 0 && e <= FA_BK && p.row_lo + t * 128 >= p.resp_lo;
+    it.single = false;
     // no salient key in the sequence: the keys did not change, so neither did the statistics
     // (when current) nor the contexts: nothing to do
     if (e == 0 && p.inc && p.mode == 0) it.nrows = 0;
@@ -108,6 +110,7 @@ __device__ __forceinline__ FaItem fa_item(const FaParams &p, int w, int off, int
     it.passP = true;
     it.nkP = p.N;
     it.inc = false;
+    it.single = p.mode != 1;
   }
   return it;
 }
@@ -375,7 +378,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         continue;
       }
       // pass S (type 1): the N keys
-      if (!it.type2) {
+      if (!it.single) {
         for (int kt = 0; kt < NKT; ++kt) {
           load_kv(&tmK, seq0 + kt * FA_BK, it.kvh);
           if (kt == 0) after_first();
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         const CUtensorMap *mk = it.type2 ? &tmK : &tmKx, *mv = it.type2 ? &tmV : &tmDV;
         const int r0 = it.type2 ? seq0 : it.off;
         load_kv(mk, r0, it.kvh);
-        if (it.type2) after_first();
+        if (it.single) after_first();
         if (n2 > 1) load_kv(mk, r0 + FA_BK, it.kvh);
         for (int j = 0; j < n2; ++j) {
           if (j + 2 < n2) load_kv(mk, r0 + (j + 2) * FA_BK, it.kvh);
@@ -476,7 +479,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           umma_commit(&q_empty[qb]);
           continue;
         }
-        if (!it.type2)
+        if (!it.single)
           for (int kt = 0; kt < NKT; ++kt) qk();
         if (it.passP) {
           // two score tiles ahead of P V: the score tile j + 2 reuses the S buffer the softmax
@@ -634,9 +637,13 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty);
         oscale = 1.f / Lnew;
-      } else if (it.type2) {
-        // ---- exact rows: one pass over the N keys (online softmax, lazy rescale)
-        float ref = -INFINITY, l = 0.f;
+      } else if (it.single) {
+        // ---- exact rows: one pass over the N keys. P = 2^((s - ref) c) with ONE reference per
+        // row, the max of the first key tile (exchanged between the row's column groups once):
+        // no per-tile agreement is needed, P may exceed 1 (fp32 / bf16 keep their relative
+        // precision at any magnitude). A row whose later scores exceed the reference by more than
+        // 2^100 (overflow risk) sends the item to the fixup launch, which re-runs it in two passes.
+        float ref = -INFINITY, l = 0.f, over = -INFINITY;
         for (int j = 0; j < NKT; ++j) {
           const int sb = sc & 1;
           ev(40);
@@ -676,39 +683,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
 #pragma unroll
             for (int g2 = 0; g2 < FA_NG; ++g2) ref = fmaxf(ref, xch[g2 * 128 + r].x);
           } else {
-            // raise the reference only when some row of the quad grew by more than 2^8 (P stays
-            // <= 256, exact in bf16/fp32 range): one vote per tile, a rescale is rare
-            const unsigned need = __ballot_sync(0xffffffffu, (tmax - ref) * c > 8.f);
-            int *fv = flg + (j & 1) * 16 + quad * 4;
-            if (lane == 0) fv[hh] = need != 0u;
-            fa_named_sync(1 + quad, 32 * FA_NG);
-            int any = 0;
-#pragma unroll
-            for (int g2 = 0; g2 < FA_NG; ++g2) any |= fv[g2];
-            if (any) {
-              xch[hh * 128 + r].x = tmax;
-              fa_named_sync(1 + quad, 32 * FA_NG);
-              float nref = ref;
-#pragma unroll
-              for (int g2 = 0; g2 < FA_NG; ++g2) nref = fmaxf(nref, xch[g2 * 128 + r].x);
-              fa_named_sync(1 + quad, 32 * FA_NG);
-              const float f = ex2f((ref - nref) * c);
-              l *= f;
-              // the accumulator holds P V of tiles < j: wait for the last of those MMAs, scale
-              fa_wait(&p_empty[(pc - 2) & 1], ((pc - 2) >> 1) & 1);
-              tc_fence_after();
-#pragma unroll 1
-              for (int ch = 0; ch < NCH; ++ch) {
-                uint32_t a32[32];
-                tmem_ld32_issue(trow + FA_ACC_COL + hh * FA_CW + ch * 32, a32);
-                tmem_ld32_wait(a32);
-#pragma unroll
-                for (int t = 0; t < 32; ++t) a32[t] = __float_as_uint(__uint_as_float(a32[t]) * f);
-                tmem_st32(trow + FA_ACC_COL + hh * FA_CW + ch * 32, a32);
-              }
-              tmem_st_wait();
-              ref = nref;
-            }
+            over = fmaxf(over, (tmax - ref) * c);
           }
           const float rc = ref * c;
           // P = exp2((s - ref) c), bf16x2-packed into the P buffer; l sums the fp32 values
@@ -756,6 +731,10 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           if (own_stats) p.stats[srow] = make_float2(ref * c, L);
         }
         oscale = 1.f / L;
+        if (__ballot_sync(0xffffffffu, rvalid && over > 100.f) != 0u && lane == 0) {
+          const int pos = atomicAdd(&p.fix[0], 1);
+          if (pos < p.fix_cap) p.fix[1 + pos] = w;
+        }
       } else {
       // ---- pass S: running (m, l) of this column group of the row
       float m = -INFINITY, l = 0.f;
@@ -963,8 +942,8 @@ int attention_fused_launch(const AttnArgs &a, cudaStream_t st) {
   p.mode = a.mode;
   p.fix = a.fix;
   p.fix_cap = a.fix_cap;
-  if (p.inc && !p.fix) {
-    set_error("fused attention: incremental statistics need the fixup list");
+  if (!p.fix) {
+    set_error("fused attention: missing fixup list");
     return DYLLM_E_ARG;
   }
   if (!p.work_ctr) {

@@ -580,7 +580,14 @@ static int full_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c
     a.work_ctr = ctx->attn_ctr;
     const bool fused = m.head_dim == 128 && g_attn_fused_enabled;
     a.stats_cache = fused ? C.st : nullptr;  // every row's statistics written
+    a.fix = ctx->attn_fix;
+    a.fix_cap = kFixCap;
     KL(ATTN, RET(attention_launch(a, st)));
+    if (fused) {  // rows whose single-pass softmax could overflow (rare): two-pass recomputation
+      AttnArgs f = a;
+      f.mode = 1;
+      KL(OTHER, RET(attention_launch(f, st)));
+    }
     C.st_ok = fused;
     int prc = post_attention(ctx, w, c, l, nullptr, C.C, Hprev, nullptr, C.H);
     if (prc) {
@@ -660,7 +667,7 @@ static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *
   a.fix = ctx->attn_fix;
   a.fix_cap = kFixCap;
   KL(ATTN, RET(attention_launch(a, st)));
-  if (inc) {  // tiles whose incremental update cancelled (rare): dense recomputation
+  if (fused) {  // tiles whose incremental update cancelled or whose single pass could overflow (rare)
     AttnArgs f = a;
     f.mode = 1;
     KL(OTHER, RET(attention_launch(f, st)));  // not an attention pass of its own (roofline accounting)
@@ -958,6 +965,8 @@ int dyllm_cache_refresh_stats(dyllm_ctx *ctx, dyllm_cache *c, int layer) {
   a.rowflag = c->rowflag;
   a.work_ctr = ctx->attn_ctr;
   a.stats_cache = C.st;
+  a.fix = ctx->attn_fix;
+  a.fix_cap = kFixCap;
   a.mode = 2;
   KL(ATTN, RET(attention_launch(a, ctx->stream)));
   C.st_ok = true;

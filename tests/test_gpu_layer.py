@@ -41,12 +41,14 @@ QK_STD = {"tiny": 0.18, "small128": 0.09, "small128_gqa": 0.09}   # sharper atte
 
 
 def _teacher_forced_layer(name, layer, mode, frac_in=0.4, seed=0, select_mode=0, frac=0.3, refresh=False,
-                          dominate=False):
+                          dominate=False, overflow=False):
     """refresh: recompute the layer's softmax statistics on the GPU from the imported caches before
     the step, so that response tiles take the incremental path — as in every
     denoising step after the FullSteps. dominate: make one approximate row of sequence 0 attend
     (head 0) almost only to a salient key whose old value is overwritten, so its incremental
-    normaliser cancels and its tile goes through the dense fixup launch."""
+    normaliser cancels and its tile goes through the dense fixup launch. overflow: give one exact
+    row of sequence 0 a key, in its second key tile, scoring ~88 nats above everything else, so that
+    the single-pass softmax of exact rows hands its item to the two-pass fixup."""
     m = Model(name, seed=seed, qk_std=QK_STD[name], select_mode=select_mode)
     cfg, run = m.cfg, m.run
     N = run.N
@@ -62,6 +64,16 @@ def _teacher_forced_layer(name, layer, mode, frac_in=0.4, seed=0, select_mode=0,
         x = st.H0 if layer == 0 else st.caches[layer - 1].H
         noise = rng.standard_normal((len(idx), cfg.d_model)) * 0.5 * np.abs(x[idx]).max(axis=1, keepdims=True)
         x[idx] = bf16_round(x[idx] + noise)
+    if overflow:
+        st, idx = states[0], idx_lists[0]
+        r = int(idx[0])
+        x_all = st.H0 if layer == 0 else st.caches[layer - 1].H
+        xn = O.rms_norm(x_all, m.W["layers"][layer]["g_attn"], cfg.rms_eps)
+        q_new = O.qkv(xn[[r]], m.W["layers"][layer], cfg, np.array([r]))[0][0]
+        hd = cfg.head_dim
+        j = next(q for q in range(N - 1, 127, -1) if q not in set(idx.tolist()))
+        lc = st.caches[layer]
+        lc.K[j, :hd] = bf16_round(q_new[:hd] * (1000.0 / float(q_new[:hd] @ q_new[:hd])))
     if dominate:
         st, idx = states[0], idx_lists[0]
         r = next(q for q in input_rows if q not in set(idx.tolist()))
@@ -145,6 +157,12 @@ def test_layer_step_teacher_forced(name, layer, mode):
 def test_layer_step_incremental_statistics(name, mode, select_mode):
     """Response tiles with current statistics: incremental normaliser == Alg. 4's dense one."""
     _teacher_forced_layer(name, 1, mode, select_mode=select_mode, refresh=True)
+
+
+@pytest.mark.parametrize("mode", ["fi", "ro"])
+def test_layer_step_single_pass_overflow_fixup(mode):
+    """An exact row whose later key outscores its first key tile by ~2^127: two-pass fixup."""
+    _teacher_forced_layer("small128", 1, mode, refresh=True, overflow=True)
 
 
 @pytest.mark.parametrize("mode", ["fi", "ro"])
