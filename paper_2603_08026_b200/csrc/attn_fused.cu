@@ -36,7 +36,7 @@ constexpr int FA_KVST = 4;                 // unified K / V / dV tile ring, fill
 constexpr int FA_DATA = FA_QST * FA_Q_BYTES + FA_KVST * FA_KV_BYTES;
 // softmax warps: FA_NG column groups x 4 TMEM lane quadrants; each warp owns 32 rows x FA_CW keys
 // of a score tile (and FA_CW head dims of the output)
-constexpr int FA_NG = 2;
+constexpr int FA_NG = 4;
 constexpr int FA_CW = FA_BK / FA_NG;
 constexpr int FA_NSW = 4 * FA_NG;           // softmax warps 2 .. 1 + FA_NSW
 constexpr int FA_WV = 2 + FA_NSW;           // V / dV producer warp
