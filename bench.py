@@ -111,14 +111,20 @@ def layer_bytes_flops(cfg):
     return {"qkv_w": 2 * d * (qw + 2 * kw), "o_w": 2 * d * qw, "gu_w": 2 * d * 2 * F, "down_w": 2 * d * F}
 
 
+run_config_name = ["llada8b"]
+
+
 def measured_traffic(cls, sparse_t, run):
     """DRAM bytes per launch of a kernel class from the committed ncu --set full captures
     (profiles/ncu_traffic.json), weighted by the response-only / full-input launch mix."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        t = json.load(open(p)).get(cls)
+        meas = json.load(open(p))
     except (OSError, ValueError):
         return None
+    if meas.get("_config") != run_config_name[0]:
+        return None   # captured at another configuration
+    t = meas.get(cls)
     if not t:
         return None
     n_fi = sum(1 for x in sparse_t if x % run.full_period == 0)
@@ -307,6 +313,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     torch.cuda.set_device(local)
     cfg, run = configs.preset(args.config)
+    run_config_name[0] = args.config
     if args.batch:
         run = replace(run, batch=args.batch)
     if args.n_u:
