@@ -43,7 +43,8 @@ constexpr int FA_WV = 2 + FA_NSW;           // V / dV producer warp
 constexpr int FA_WK2 = 3 + FA_NSW;          // second K producer warp
 constexpr int FA_THREADS = 32 * (4 + FA_NSW);
 constexpr int FA_XCH = FA_NG * 128 * 8;     // (m, l) per column group per row
-constexpr int FA_SMEM = 1024 + FA_DATA + FA_XCH + 512;
+constexpr int FA_PF = 3 * 128 * 16;         // row metadata of 3 items in flight (FaRow per row)
+constexpr int FA_SMEM = 1024 + FA_DATA + FA_XCH + FA_PF + 512;
 static_assert(FA_CW % 32 == 0, "column groups are whole 32-column TMEM loads");
 // TMEM columns: S[2] (2 x 128 fp32), accumulator (128 fp32), P[2] (2 x 64: 128 keys bf16x2-packed,
 // the A operand of the P V MMA read straight from TMEM)
@@ -178,6 +179,20 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t v[32]) 
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void fa_wait(uint64_t *bar, uint32_t ph) { mbar_wait(bar, ph); }
+// per-row metadata of an item, fetched asynchronously one item ahead (cp.async -> shared memory):
+// output row id, its row-kind tag, its cached softmax statistics
+struct FaRow {
+  int orow;
+  uint32_t rf;
+  float2 so;
+};
+__device__ __forceinline__ void cp_async_4(void *smem, const void *gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_8(void *smem, const void *gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void fa_named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -217,7 +232,8 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   uint8_t *sQ = smem;                                   // [2][32 KB]
   uint8_t *sKV = sQ + FA_QST * FA_Q_BYTES;              // [4][32 KB] K, V or dV tiles
   float2 *xch = reinterpret_cast<float2 *>(sKV + FA_KVST * FA_KV_BYTES);  // [column group][128 rows]
-  uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(xch) + FA_XCH);
+  FaRow *rows_s = reinterpret_cast<FaRow *>(reinterpret_cast<uint8_t *>(xch) + FA_XCH);  // [3][128]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(rows_s) + FA_PF);
   uint64_t *q_full = bars, *q_empty = bars + 2;
   uint64_t *kv_full = bars + 4, *kv_empty = bars + 8;   // [FA_KVST]
   uint64_t *s_full = bars + 14, *s_empty = bars + 16;
@@ -226,7 +242,6 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   uint64_t *wq_full = bars + 24, *wq_empty = bars + 28;   // [4] work queue (producer -> other roles)
   int4 *wq = reinterpret_cast<int4 *>(bars + 32);          // [4] (item, off, e, -) ; item -1 = done
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wq + 4);
-  int *flg = reinterpret_cast<int *>(bars + 48);           // [2 parities][4 quads][FA_NG] rescale votes
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int NKT = (p.N + FA_BK - 1) / FA_BK;
@@ -276,13 +291,17 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   // and heavy exact-row items no longer pile up on fixed CTAs) and passes them to the other roles
   // through a 4-deep shared-memory queue. Consumers: one arrival per warp.
   int wn = 0;  // queue position of this role
-  auto next_item = [&](FaItem &it) -> int {
+  auto pop_item = [&]() -> int4 {
     const int slot = wn & 3;
     fa_wait(&wq_full[slot], (wn >> 2) & 1);
     const int4 q = wq[slot];
     __syncwarp();
     if (lane == 0) mbar_arrive(&wq_empty[slot]);
     ++wn;
+    return q;
+  };
+  auto next_item = [&](FaItem &it) -> int {
+    const int4 q = pop_item();
     if (q.x >= 0) it = fa_item(p, q.x, q.y, q.z);
     return q.x;
   };
@@ -310,6 +329,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     // latency and no exposed Q load
     int wnext = -1, onext = 0, enext = 0;
     auto claim = [&]() {  // warp 0, lane 0: next non-empty item (or -1) into the queue
+      ev(62);
       int w, off = 0, e = 0;
       for (;;) {
         w = atomicAdd(&p.work_ctr[0], 1);
@@ -330,6 +350,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       mbar_wait(&wq_empty[slot], ((wn >> 2) & 1) ^ 1);
       wq[slot] = make_int4(w, off, e, 0);
       mbar_arrive(&wq_full[slot]);
+      ev(63);
       ++wn;
       wnext = w;
       onext = off;
@@ -337,7 +358,9 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     };
     auto load_q = [&](const FaItem &it, int qi) {
       const int qb = qi & 1;
+      ev(64);
       fa_wait(&q_empty[qb], ((qi >> 1) & 1) ^ 1);
+      ev(65);
       mbar_expect_tx(&q_full[qb], FA_Q_BYTES);
       tma_load_3d(sQ + qb * FA_Q_BYTES, it.type2 ? &tmQx : &tmQ, &q_full[qb], 0, it.q_row, it.h * 2);
     };
@@ -427,6 +450,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         ev(it.inc ? 3 : it.type2 ? 2 : 1);
         const int qb = qi & 1;
         fa_wait(&q_full[qb], (qi >> 1) & 1);
+        ev(9);
         ++qi;
         const uint64_t qd = qdesc0 + qb * kSlot;
         auto qk = [&]() {
@@ -506,21 +530,54 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     const float c = p.c;
     constexpr int NCH = FA_CW / 32;       // 32-column TMEM loads per warp and tile
     int sc = 0, pc = 0, ai = 0;
+    // Row metadata of an item (output row id, row-kind tag, cached softmax statistics): global
+    // loads that miss L2 (the weights stream through it every layer). The column-group-0 warps
+    // fetch them with cp.async into shared memory one item ahead (the next item is taken from the
+    // work queue as soon as the current one starts — the producer claims one ahead), into 3 slots
+    // (no warp of a quad lags its group-0 warp by a whole item: they meet at a barrier in each);
+    // every thread reads its row's entry only after the item's first quad barrier.
+    auto fetch_rows = [&](const FaItem &x, int slot) {
+      if (r >= x.nrows) return;
+      FaRow *d = rows_s + slot * 128 + r;
+      if (x.type2) {
+        cp_async_4(&d->orow, p.ex_rows + x.q_row + r);
+      } else {
+        d->orow = x.q_row + r;
+        cp_async_4(&d->rf, p.rowflag + x.q_row + r);
+        if (x.inc) cp_async_8(&d->so, p.stats + static_cast<int64_t>(x.q_row + r) * p.H + x.h);
+      }
+    };
+    int4 cq = pop_item();
     FaItem it;
-    for (int w = next_item(it); w >= 0; w = next_item(it)) {
+    int ii = 0;  // item count of this warp
+    if (cq.x >= 0) {
+      it = fa_item(p, cq.x, cq.y, cq.z);
+      if (hh == 0) fetch_rows(it, 0);
+    }
+    while (cq.x >= 0) {
+      const int w = cq.x;
+      ev(4);
+      const int4 nq = pop_item();
+      ev(5);
+      if (hh == 0) {
+        cp_async_wait_all();  // this item's rows (issued one item ago)
+        if (nq.x >= 0) fetch_rows(fa_item(p, nq.x, nq.y, nq.z), (ii + 1) % 3);
+      }
+      const FaRow *rp = rows_s + (ii % 3) * 128 + r;
       // warps whose 32 rows are all past the item's row count skip the softmax work (they still
       // take part in every barrier; their garbage P rows only reach accumulator rows never stored)
       const bool wact = quad * 32 < it.nrows;
       const bool rvalid = r < it.nrows;
-      // type 1 writes approximate rows only: fetch the row kind early (its latency hides under pass S)
-      const int64_t orow = it.type2 ? (rvalid ? p.ex_rows[it.q_row + r] : 0) : static_cast<int64_t>(it.q_row) + r;
-      const bool write_row = rvalid && (it.type2 || (it.passP && p.rowflag[orow] != p.tag));
+      // (after the item's first quad barrier) type 1 / 3 write approximate rows only (exact rows
+      // belong to the type-2 items); statistics entries likewise
+      auto write_row = [&]() { return rvalid && (it.type2 || (it.passP && rp->rf != p.tag)); };
+      auto own_stats = [&]() {
+        return p.stats != nullptr && rvalid && hh == 0 && (it.type2 || p.mode == 2 || rp->rf != p.tag);
+      };
+      auto srow = [&]() { return static_cast<int64_t>(rp->orow) * p.H + it.h; };
       ev(it.inc ? 3 : it.type2 ? 2 : 1);
       float acc[FA_CW];
       float oscale;
-      // statistics entry of this row (exact rows' entries belong to the type-2 items)
-      const bool own_stats = p.stats != nullptr && rvalid && hh == 0 && (it.type2 || p.mode == 2 || p.rowflag[orow] != p.tag);
-      const int64_t srow = orow * p.H + it.h;
       if (it.inc) {
         // ---- type 3, incremental statistics (exact up to rounding): only the salient
         // keys changed since this row's statistics (m_old, l_old) were computed, so
@@ -529,11 +586,16 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         // exps on MUFU (no polynomial: the removed and added terms must carry no systematic error).
         // A row whose l_new cancels below 2^-14 of l_old (the changed keys held nearly all its
         // attention) sends its tile to the dense fixup launch.
-        const float2 so = rvalid ? p.stats[srow] : make_float2(0.f, 1.f);
+        float2 so = make_float2(0.f, 1.f);
+        // this warp's 32 key columns hold salient keys (else: no exps, P = 0 — the MUFU work
+        // follows the salient key count, not the 128-key tile)
+        const bool kact = hh * FA_CW < it.nkP;
         float part = 0.f, mref = 0.f;
         {
           const int sb = sc & 1;
+          ev(40);
           fa_wait(&s_full[sb], (sc >> 1) & 1);
+          ev(41);
           ++sc;
           const int pb = pc & 1;
           ++pc;
@@ -541,6 +603,28 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_empty[sb]);
             fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[pb]);
+          } else if (!kact) {  // no salient key in this warp's columns: P = 0, no exps
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[sb]);
+            xch[hh * 128 + r].x = -INFINITY;
+            fa_named_sync(1 + quad, 32 * FA_NG);
+            float mn = -INFINITY;
+#pragma unroll
+            for (int g2 = 0; g2 < FA_NG; ++g2) mn = fmaxf(mn, xch[g2 * 128 + r].x);
+            fa_named_sync(1 + quad, 32 * FA_NG);
+            if (rvalid) so = rp->so;
+            mref = fmaxf(so.x, mn * c);
+            fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1);
+            tc_fence_after();
+            uint32_t pk[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) pk[t] = 0u;
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch) tmem_st16(trow + FA_P_COL + pb * 64 + hh * (FA_CW / 2) + ch * 16, pk);
+            tmem_st_wait();
+            tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_full[pb]);
           } else {
@@ -563,6 +647,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
 #pragma unroll
             for (int g2 = 0; g2 < FA_NG; ++g2) mn = fmaxf(mn, xch[g2 * 128 + r].x);
             fa_named_sync(1 + quad, 32 * FA_NG);
+            if (rvalid) so = rp->so;
             mref = fmaxf(so.x, mn * c);
             fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1);
             tc_fence_after();
@@ -583,26 +668,33 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_full[pb]);
           }
+          ev(42);
         }
         {  // the same keys before this step's overwrite
           const int sb = sc & 1;
           fa_wait(&s_full[sb], (sc >> 1) & 1);
+          ev(43);
           ++sc;
           if (!wact) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_empty[sb]);
           } else {
-            tc_fence_after();
-            float v[FA_CW];
-#pragma unroll
-            for (int ch = 0; ch < NCH; ++ch) tmem_ld32(trow + sb * FA_BK + hh * FA_CW + ch * 32, v + ch * 32);
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&s_empty[sb]);
             float sub = 0.f;
+            if (kact) {
+              tc_fence_after();
+              float v[FA_CW];
 #pragma unroll
-            for (int t = 0; t < FA_CW; ++t)
-              sub += hh * FA_CW + t < it.nkP ? ex2f(fmaf(v[t], c, -mref)) : 0.f;
+              for (int ch = 0; ch < NCH; ++ch) tmem_ld32(trow + sb * FA_BK + hh * FA_CW + ch * 32, v + ch * 32);
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&s_empty[sb]);
+#pragma unroll
+              for (int t = 0; t < FA_CW; ++t)
+                sub += hh * FA_CW + t < it.nkP ? ex2f(fmaf(v[t], c, -mref)) : 0.f;
+            } else {
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&s_empty[sb]);
+            }
             part -= sub;
           }
         }
@@ -618,15 +710,17 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           const float base = so.y * ex2f(so.x - mref);
           Lnew = base + tot;
           bad = !(so.y > 0.f) || !(Lnew > base * 0x1p-14f) || !(Lnew < INFINITY);
-          if (own_stats && !bad) p.stats[srow] = make_float2(mref, Lnew);
+          if (own_stats() && !bad) p.stats[srow()] = make_float2(mref, Lnew);
         }
         // a tile with a cancelled row is recomputed densely by the fixup launch (duplicates of a
         // tile id are harmless: the dense recomputation is deterministic)
-        if (__ballot_sync(0xffffffffu, rvalid && bad) != 0u && lane == 0) {
+        if (__ballot_sync(0xffffffffu, bad && write_row()) != 0u && lane == 0) {
           const int pos = atomicAdd(&p.fix[0], 1);
           if (pos < p.fix_cap) p.fix[1 + pos] = w;
         }
+        ev(50);
         fa_wait(acc_full, ai & 1);
+        ev(51);
         ++ai;
         if (wact) {
           tc_fence_after();
@@ -728,7 +822,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
 #pragma unroll
           for (int g2 = 0; g2 < FA_NG; ++g2) L += xch[g2 * 128 + r].y;
           fa_named_sync(1 + quad, 32 * FA_NG);
-          if (own_stats) p.stats[srow] = make_float2(ref * c, L);
+          if (own_stats()) p.stats[srow()] = make_float2(ref * c, L);
         }
         oscale = 1.f / L;
         if (__ballot_sync(0xffffffffu, rvalid && over > 100.f) != 0u && lane == 0) {
@@ -802,7 +896,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       for (int g = 0; g < FA_NG; ++g) Lsum += hg[g].x == -INFINITY ? 0.f : hg[g].y * ex2f((hg[g].x - M) * c);
       const float Mc = M * c;
       const float inv_l = 1.f / Lsum;
-      if (own_stats && wact) p.stats[srow] = make_float2(Mc, Lsum);
+      if (wact && own_stats()) p.stats[srow()] = make_float2(Mc, Lsum);
       // ---- pass P: P = exp2(s - m) into tensor memory for the P V MMA
       oscale = inv_l;
       if (it.passP) {
@@ -829,16 +923,21 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           tc_fence_after();
 #pragma unroll
           for (int ch = 0; ch < NCH; ++ch) {
-            float v[32];
-            tmem_ld32(trow + sb * FA_BK + hh * FA_CW + ch * 32, v);
             const int k0 = j * FA_BK + hh * FA_CW + ch * 32;
             uint32_t pk[16];
+            if (k0 < it.nkP) {
+              float v[32];
+              tmem_ld32(trow + sb * FA_BK + hh * FA_CW + ch * 32, v);
 #pragma unroll
-            for (int t = 0; t < 16; ++t) {
-              const float e1 = (t & 1) ? ex2p(fmaf(v[2 * t + 1], c, -Mc)) : ex2f(fmaf(v[2 * t + 1], c, -Mc));
-              const float p0 = (k0 + 2 * t < it.nkP) ? ex2f(fmaf(v[2 * t], c, -Mc)) : 0.f;
-              const float p1 = (k0 + 2 * t + 1 < it.nkP) ? e1 : 0.f;
-              pk[t] = pack2(p0, p1);
+              for (int t = 0; t < 16; ++t) {
+                const float e1 = (t & 1) ? ex2p(fmaf(v[2 * t + 1], c, -Mc)) : ex2f(fmaf(v[2 * t + 1], c, -Mc));
+                const float p0 = (k0 + 2 * t < it.nkP) ? ex2f(fmaf(v[2 * t], c, -Mc)) : 0.f;
+                const float p1 = (k0 + 2 * t + 1 < it.nkP) ? e1 : 0.f;
+                pk[t] = pack2(p0, p1);
+              }
+            } else {  // past the salient keys: P = 0, no exps
+#pragma unroll
+              for (int t = 0; t < 16; ++t) pk[t] = 0u;
             }
             tmem_st16(trow + FA_P_COL + pb * 64 + hh * (FA_CW / 2) + ch * 16, pk);
           }
@@ -868,17 +967,53 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       // ---- epilogue: this thread's row, head columns [hh*FA_CW, (hh+1)*FA_CW). Exact rows
       // (type 2): C = O / l. Approximate rows (type 1): the delta dC / l only; the similarity
       // kernel, which reads C_cache anyway, forms C_new = C_cache + dC (no C_cache read here).
-      if (write_row) {
-        uint4 *dst = reinterpret_cast<uint4 *>(p.C_out + orow * p.qw + it.h * 128 + hh * FA_CW);
+      // Stores are made coalesced first: a 4 x 4 transpose of 16-byte chunks inside each group of
+      // 4 lanes (two xor-shuffle rounds) leaves lane c of group m holding chunk c of rows
+      // 4m .. 4m+3, so each store instruction writes 8 rows x 64 contiguous bytes instead of 32
+      // rows x 16 bytes.
+      static_assert(FA_CW == 32, "epilogue transpose assumes 4 chunks of 8 head dims per warp");
+      {
+        const unsigned wmask = __ballot_sync(0xffffffffu, write_row());
+        if (wmask) {
+          uint4 ch[4];
 #pragma unroll
-        for (int u = 0; u < FA_CW / 8; ++u) {
-          float o[8];
+          for (int u = 0; u < 4; ++u) {
+            float o[8];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) o[t] = acc[u * 8 + t] * oscale;
-          dst[u] = pack8(o);
+            for (int t = 0; t < 8; ++t) o[t] = acc[u * 8 + t] * oscale;
+            ch[u] = pack8(o);
+          }
+          auto shfl4 = [](uint4 v, int m) {
+            return make_uint4(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m),
+                              __shfl_xor_sync(0xffffffffu, v.z, m), __shfl_xor_sync(0xffffffffu, v.w, m));
+          };
+          const bool b0 = lane & 1, b1 = lane & 2;
+#pragma unroll
+          for (int a = 0; a < 4; a += 2) {  // round 1: chunk pairs (0,1), (2,3) with lane ^ 1
+            const uint4 rv = shfl4(b0 ? ch[a] : ch[a + 1], 1);
+            if (b0) ch[a] = rv; else ch[a + 1] = rv;
+          }
+#pragma unroll
+          for (int a = 0; a < 2; ++a) {     // round 2: chunk pairs (0,2), (1,3) with lane ^ 2
+            const uint4 rv = shfl4(b1 ? ch[a] : ch[a + 2], 2);
+            if (b1) ch[a] = rv; else ch[a + 2] = rv;
+          }
+          const int orow_l = rvalid ? rp->orow : 0;
+          const int g4 = lane & ~3;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int src = g4 | k;
+            const int orr = __shfl_sync(0xffffffffu, orow_l, src);
+            if ((wmask >> src) & 1u)
+              *reinterpret_cast<uint4 *>(p.C_out + static_cast<int64_t>(orr) * p.qw + it.h * 128 + hh * FA_CW +
+                                         (lane & 3) * 8) = ch[k];
+          }
         }
       }
       ev(52);
+      cq = nq;
+      if (cq.x >= 0) it = fa_item(p, cq.x, cq.y, cq.z);
+      ++ii;
     }
   }
   ev.finish();

@@ -4,10 +4,10 @@ per-role event logs of CTAs 0-1 for the last layer of one denoising step of the 
     DYLLM_NVCC_FLAGS=-DDYLLM_ATTN_EVENTS=1 python -m paper_2603_08026_b200.build --force
     python tools/attn_events.py --mode ro|fi|full [--items 3]
 
-Codes: MMA 1/2/3 item (type 1/2/3), 10 QK begin, 11 S buffer free, 12 K tile ready, 13 QK issued,
+Codes: MMA 1/2/3 item (type 1/2/3), 9 Q ready, 10 QK begin, 11 S buffer free, 12 K tile ready, 13 QK issued,
 20 PV begin, 21 P ready, 22 V/acc ready, 23 PV issued. Softmax (warp 2) 1/2 item, 30 S wait,
 31 S ready, 32 S read (buffer released), 33 S tile done, 40 P-pass S wait, 41 ready, 42 P stored,
-50 acc wait, 51 acc ready, 52 epilogue done. Producer 60 K slot wait, 61 K issued. V 70, 71.
+50 acc wait, 51 acc ready, 52 epilogue done. Producer 60 K slot wait, 61 K issued, 62/63 claim begin/end, 64/65 Q slot wait begin/end. V 70, 71.
 """
 import argparse
 import collections
@@ -66,7 +66,7 @@ pairs = {0: [(10, 11, "S buf free wait"), (11, 12, "K tile wait"), (12, 13, "QK 
              (21, 22, "V/acc wait"), (22, 23, "PV issue")],
          1: [(30, 31, "S wait (pass S)"), (31, 32, "S read"), (32, 33, "S math"), (40, 41, "S wait (pass P)"),
              (41, 42, "P math+store"), (50, 51, "acc wait"), (51, 52, "epilogue")],
-         2: [(60, 61, "K slot wait")], 3: [(70, 71, "V slot wait")]}
+         2: [(60, 61, "K slot wait"), (62, 63, "claim"), (64, 65, "Q slot wait")], 3: [(70, 71, "V slot wait")]}
 print(f"mode {a.mode} step {target}, last layer's launch, CTA 0 (us at {a.ghz} GHz)")
 for role in range(4):
     ev = decode(raw[0, role])
@@ -99,7 +99,8 @@ for role in range(4):
 mm = decode(raw[0, 0])
 sm = decode(raw[0, 1])
 t0 = min(mm[0][1], sm[0][1])
-merged = sorted([(t, "M", c) for c, t in mm] + [(t, "S", c) for c, t in sm])
+pp = decode(raw[0, 2])
+merged = sorted([(t, "M", c) for c, t in mm] + [(t, "S", c) for c, t in sm] + [(t, "P", c) for c, t in pp])
 if a.kind:
     k0 = next((i for i, (t, r, c) in enumerate(merged) if r == "M" and c == a.kind), 0)
     t0 = merged[k0][0]

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+DYLLM_NVCC_FLAGS=-DDYLLM_ATTN_EVENTS=1 python -m paper_2603_08026_b200.build --force > gpurun_out/exp36.log 2>&1
+timeout 300 python tools/attn_events.py --mode ro --items 4 >> gpurun_out/exp36.log 2>&1
+timeout 300 python tools/attn_events.py --mode ro --items 4 --kind 3 > gpurun_out/exp36_k3.log 2>&1
+timeout 300 python tools/attn_events.py --mode fi --items 2 > gpurun_out/exp36_fi.log 2>&1
