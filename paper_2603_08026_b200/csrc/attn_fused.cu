@@ -27,6 +27,8 @@
 
 namespace dy {
 
+int g_attn_t4_rows = 32;
+
 constexpr int FA_BK = 128;                 // keys per tile (MMA N = 128: the Q operand read per
                                            // instruction is amortised over 128 keys)
 constexpr int FA_Q_BYTES = 128 * 256;      // 128 rows x 128 bf16: two 64-column halves of 16 KB
@@ -44,7 +46,11 @@ constexpr int FA_WK2 = 3 + FA_NSW;          // second K producer warp
 constexpr int FA_THREADS = 32 * (4 + FA_NSW);
 constexpr int FA_XCH = FA_NG * 128 * 8;     // (m, l) per column group per row
 constexpr int FA_PF = 3 * 128 * 16;         // row metadata of 3 items in flight (FaRow per row)
-constexpr int FA_SMEM = 1024 + FA_DATA + FA_XCH + FA_PF + 512;
+constexpr int FA_PT_BYTES = 32 * 256;       // type 4: P^T tile, 32 rows x 128 keys bf16 (K-major, SW128)
+constexpr int FA_PT = 2 * FA_PT_BYTES;      // double-buffered
+constexpr int FA_X4 = 4 * 4 * 8 * 4;        // type 4: per (column group, quad, row) partial max / sum
+constexpr int FA_SMEM = 1024 + FA_DATA + FA_PT + FA_XCH + FA_PF + FA_X4 + 1024;
+constexpr int FA_T4_MAX = 32;               // type 4: at most 32 rows (MMA N = 32)
 static_assert(FA_CW % 32 == 0, "column groups are whole 32-column TMEM loads");
 // TMEM columns: S[2] (2 x 128 fp32), accumulator (128 fp32), P[2] (2 x 64: 128 keys bf16x2-packed,
 // the A operand of the P V MMA read straight from TMEM)
@@ -69,6 +75,7 @@ struct FaParams {
   int mode;                   // 0 denoising step, 1 fixup list (dense), 2 statistics refresh (no output)
   int *fix;                   // [0] count, [1 ..] ids of incremental tiles whose update cancelled
   int fix_cap;
+  int t4max;                  // exact-row items of <= t4max rows run transposed (type 4; 0: never)
 };
 
 struct FaItem {
@@ -76,6 +83,7 @@ struct FaItem {
   bool type2, passP;
   bool inc;     // type 3: incremental statistics (response tile, <= 128 salient keys, current stats)
   bool single;  // type 2 in one pass (online softmax); the fixup launch re-runs type 2 in two passes
+  bool t4;      // type 2, single pass, <= 32 rows: computed transposed (keys on the MMA rows)
 };
 
 // Item decode from its index and the exact-row range (off, e) of its sequence (the producer reads
@@ -100,6 +108,7 @@ __device__ __forceinline__ FaItem fa_item(const FaParams &p, int w, int off, int
     it.nkP = e;
     it.inc = p.inc && p.mode == 0 && e > 0 && e <= FA_BK && p.row_lo + t * 128 >= p.resp_lo;
     it.single = false;
+    it.t4 = false;
     // no salient key in the sequence: the keys did not change, so neither did the statistics
     // (when current) nor the contexts: nothing to do
     if (e == 0 && p.inc && p.mode == 0) it.nrows = 0;
@@ -112,6 +121,7 @@ __device__ __forceinline__ FaItem fa_item(const FaParams &p, int w, int off, int
     it.nkP = p.N;
     it.inc = false;
     it.single = p.mode != 1;
+    it.t4 = it.single && it.nrows <= p.t4max;
   }
   return it;
 }
@@ -145,6 +155,13 @@ __device__ __forceinline__ float ex2p(float x) {
   const float q = fmaf(fmaf(fmaf(0.05753576f, f, 0.24192697f), f, 0.69278964f), f, 1.0f);
   return __int_as_float(__float_as_int(t) * 8388608 + __float_as_int(q));
 }
+// Exps per group of 4 computed on the FMA pipe (ex2p) in the dense passes; the rest on MUFU.
+// ncu shows the XU pipe near saturation in full-input steps (profiles/r1l_attn_fi_full.md), but
+// 2 of 4 measured slower than 1 of 4 (tools/gpu_exp44.sh: full-input step 35.2 vs 34.7 ms).
+#ifndef DYLLM_FA_POLY
+#define DYLLM_FA_POLY 1
+#endif
+constexpr int FA_POLY = DYLLM_FA_POLY;
 // D[tmem] (+)= A[tmem] * B[smem]^T (kind::f16, A read from tensor memory: M lanes x K/2 packed
 // bf16x2 columns)
 __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
@@ -231,9 +248,11 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t *sQ = smem;                                   // [2][32 KB]
   uint8_t *sKV = sQ + FA_QST * FA_Q_BYTES;              // [4][32 KB] K, V or dV tiles
-  float2 *xch = reinterpret_cast<float2 *>(sKV + FA_KVST * FA_KV_BYTES);  // [column group][128 rows]
+  uint8_t *sPT = sKV + FA_KVST * FA_KV_BYTES;           // [2][8 KB] type-4 P^T tiles (1024-aligned)
+  float2 *xch = reinterpret_cast<float2 *>(sPT + FA_PT);  // [column group][128 rows]
   FaRow *rows_s = reinterpret_cast<FaRow *>(reinterpret_cast<uint8_t *>(xch) + FA_XCH);  // [3][128]
-  uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(rows_s) + FA_PF);
+  float *x4 = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(rows_s) + FA_PF);  // [4 hh][4 quads][8]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(x4) + FA_X4);
   uint64_t *q_full = bars, *q_empty = bars + 2;
   uint64_t *kv_full = bars + 4, *kv_empty = bars + 8;   // [FA_KVST]
   uint64_t *s_full = bars + 14, *s_empty = bars + 16;
@@ -242,6 +261,9 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   uint64_t *wq_full = bars + 24, *wq_empty = bars + 28;   // [4] work queue (producer -> other roles)
   int4 *wq = reinterpret_cast<int4 *>(bars + 32);          // [4] (item, off, e, -) ; item -1 = done
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wq + 4);
+  // the queue slots' items, decoded once by the claiming thread (the index arithmetic has three
+  // runtime divisions; 500 threads re-deriving it per item was measurable)
+  FaItem *wqi = reinterpret_cast<FaItem *>(bars + 48);  // [4]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int NKT = (p.N + FA_BK - 1) / FA_BK;
@@ -291,19 +313,15 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   // and heavy exact-row items no longer pile up on fixed CTAs) and passes them to the other roles
   // through a 4-deep shared-memory queue. Consumers: one arrival per warp.
   int wn = 0;  // queue position of this role
-  auto pop_item = [&]() -> int4 {
+  auto next_item = [&](FaItem &it) -> int {
     const int slot = wn & 3;
     fa_wait(&wq_full[slot], (wn >> 2) & 1);
-    const int4 q = wq[slot];
+    const int w = wq[slot].x;
+    if (w >= 0) it = wqi[slot];
     __syncwarp();
     if (lane == 0) mbar_arrive(&wq_empty[slot]);
     ++wn;
-    return q;
-  };
-  auto next_item = [&](FaItem &it) -> int {
-    const int4 q = pop_item();
-    if (q.x >= 0) it = fa_item(p, q.x, q.y, q.z);
-    return q.x;
+    return w;
   };
 
   if (warp == 0 || warp == FA_WK2 || warp == FA_WV) {
@@ -327,10 +345,12 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     // warp 0 claims one item ahead: the queue already holds item i+1 while item i's tiles are
     // issued, and Q of item i+1 is loaded early in item i, so item boundaries cost no claim
     // latency and no exposed Q load
-    int wnext = -1, onext = 0, enext = 0;
+    int wnext = -1;
+    FaItem inext;
     auto claim = [&]() {  // warp 0, lane 0: next non-empty item (or -1) into the queue
       ev(62);
       int w, off = 0, e = 0;
+      FaItem fi;
       for (;;) {
         w = atomicAdd(&p.work_ctr[0], 1);
         if (p.mode == 1) {  // fixup launch: the listed tiles, processed densely
@@ -344,17 +364,18 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         const int sq = fa_seq(p, w);
         off = p.ex_off[sq];
         e = p.ex_off[sq + 1] - off;
-        if (fa_item(p, w, off, e).nrows > 0) break;
+        fi = fa_item(p, w, off, e);
+        if (fi.nrows > 0) break;
       }
       const int slot = wn & 3;
       mbar_wait(&wq_empty[slot], ((wn >> 2) & 1) ^ 1);
       wq[slot] = make_int4(w, off, e, 0);
+      if (w >= 0) wqi[slot] = fi;
       mbar_arrive(&wq_full[slot]);
       ev(63);
       ++wn;
       wnext = w;
-      onext = off;
-      enext = e;
+      inext = fi;
     };
     auto load_q = [&](const FaItem &it, int qi) {
       const int qb = qi & 1;
@@ -367,7 +388,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     int qi = 0;
     if (warp == 0 && lane == 0) {
       claim();
-      if (wnext >= 0) load_q(fa_item(p, wnext, onext, enext), 0);
+      if (wnext >= 0) load_q(inext, 0);
     }
     for (;;) {
       FaItem it;
@@ -376,7 +397,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         if (lane == 0) {
           w = wnext;
           if (w >= 0) {
-            it = fa_item(p, w, onext, enext);
+            it = inext;
             claim();  // item i+1 into the queue now
           }
         }
@@ -390,7 +411,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       const int seq0 = it.s * p.N;
       // Q of the next item is loaded right after this item's first tile is queued
       auto after_first = [&]() {
-        if (warp == 0 && lane == 0 && wnext >= 0) load_q(fa_item(p, wnext, onext, enext), qi + 1);
+        if (warp == 0 && lane == 0 && wnext >= 0) load_q(inext, qi + 1);
       };
       if (it.inc) {  // type 3: new salient keys, their old keys, dV
         load_kv(&tmKx, it.off, it.kvh);
@@ -442,11 +463,12 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         // work queue (single-thread form of next_item)
         const int slot = wn1 & 3;
         fa_wait(&wq_full[slot], (wn1 >> 2) & 1);
-        const int4 q = wq[slot];
+        const int qw0 = wq[slot].x;
+        FaItem it;
+        if (qw0 >= 0) it = wqi[slot];
         mbar_arrive(&wq_empty[slot]);
         ++wn1;
-        if (q.x < 0) break;
-        const FaItem it = fa_item(p, q.x, q.y, q.z);
+        if (qw0 < 0) break;
         ev(it.inc ? 3 : it.type2 ? 2 : 1);
         const int qb = qi & 1;
         fa_wait(&q_full[qb], (qi >> 1) & 1);
@@ -503,6 +525,66 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           umma_commit(&q_empty[qb]);
           continue;
         }
+        if (it.t4) {
+          // type 4 (<= 32 exact rows), transposed: S^T = K Q^T (M = 128 keys, N = 32 rows: the K tile
+          // is the A operand, the Q tile's first 32 rows the B operand, both K-major as loaded) and
+          // O^T += V^T P^T (A = V, MN-major as loaded; B = P^T written by the softmax warps into a
+          // K-major shared-memory tile). A quarter of the tensor work of a 128-row tile.
+          constexpr uint32_t id_qkT = idesc_bf16_f32(128, FA_T4_MAX);
+          constexpr uint32_t id_pvT = idesc_bf16_f32(128, FA_T4_MAX) | (1u << 15);  // A (V) MN-major
+          const uint64_t ptdesc0 = sw128_kmajor_desc(smem_u32(sPT));
+          auto koffp = [](int kk) -> uint64_t { return static_cast<uint64_t>(((kk >> 2) * (FA_PT_BYTES / 2) + (kk & 3) * 32) >> 4); };
+          auto qkT = [&]() {
+            const int sb = sc & 1;
+            ev(10);
+            fa_wait(&s_empty[sb], ((sc >> 1) & 1) ^ 1);
+            ev(11);
+            const int ks = g % FA_KVST;
+            fa_wait(&kv_full[ks], (g / FA_KVST) & 1);
+            ev(12);
+            tc_fence_after();
+            const uint64_t kd = kdesc0 + ks * kSlot;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) umma_bf16(tmem + sb * FA_BK, kd + koff(kk), qd + koff(kk), id_qkT, kk > 0);
+            umma_commit(&kv_empty[ks]);
+            umma_commit(&s_full[sb]);
+            ev(13);
+            ++g;
+            ++sc;
+          };
+          auto pvT = [&](int j, int n2) {
+            const int pb = pc & 1;
+            ev(20);
+            fa_wait(&p_full[pb], (pc >> 1) & 1);
+            ev(21);
+            const int vs = g % FA_KVST;
+            fa_wait(&kv_full[vs], (g / FA_KVST) & 1);
+            if (j == 0) fa_wait(acc_empty, (ai & 1) ^ 1);
+            ev(22);
+            tc_fence_after();
+            const uint64_t vd = vdesc0 + vs * kSlot;
+            const uint64_t pd = ptdesc0 + pb * (FA_PT_BYTES >> 4);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)  // 16 keys per MMA
+              umma_bf16(tmem + FA_ACC_COL, vd + static_cast<uint64_t>(kk * 2048 >> 4), pd + koffp(kk), id_pvT,
+                        (j | kk) != 0);
+            umma_commit(&kv_empty[vs]);
+            umma_commit(&p_empty[pb]);
+            if (j == n2 - 1) umma_commit(acc_full);
+            ev(23);
+            ++g;
+            ++pc;
+          };
+          qkT();
+          if (NKT > 1) qkT();
+          for (int j = 0; j < NKT; ++j) {
+            if (j + 2 < NKT) qkT();
+            pvT(j, NKT);
+          }
+          ++ai;
+          umma_commit(&q_empty[qb]);
+          continue;
+        }
         if (!it.single)
           for (int kt = 0; kt < NKT; ++kt) qk();
         if (it.passP) {
@@ -547,21 +629,26 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         if (x.inc) cp_async_8(&d->so, p.stats + static_cast<int64_t>(x.q_row + r) * p.H + x.h);
       }
     };
-    int4 cq = pop_item();
+    // The softmax warps hold a queue slot until they finish its item (so the next item can be
+    // read in place while the current one runs) and release it at the item's end.
+    fa_wait(&wq_full[0], 0);
+    int cw = wq[0].x;
     FaItem it;
-    int ii = 0;  // item count of this warp
-    if (cq.x >= 0) {
-      it = fa_item(p, cq.x, cq.y, cq.z);
+    int ii = 0;  // item count of this warp = its queue position
+    if (cw >= 0) {
+      it = wqi[0];
       if (hh == 0) fetch_rows(it, 0);
     }
-    while (cq.x >= 0) {
-      const int w = cq.x;
+    while (cw >= 0) {
+      const int w = cw;
+      const int ns = (ii + 1) & 3;
       ev(4);
-      const int4 nq = pop_item();
+      fa_wait(&wq_full[ns], ((ii + 1) >> 2) & 1);
+      const int nw = wq[ns].x;
       ev(5);
       if (hh == 0) {
         cp_async_wait_all();  // this item's rows (issued one item ago)
-        if (nq.x >= 0) fetch_rows(fa_item(p, nq.x, nq.y, nq.z), (ii + 1) % 3);
+        if (nw >= 0) fetch_rows(wqi[ns], (ii + 1) % 3);
       }
       const FaRow *rp = rows_s + (ii % 3) * 128 + r;
       // warps whose 32 rows are all past the item's row count skip the softmax work (they still
@@ -577,8 +664,111 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       auto srow = [&]() { return static_cast<int64_t>(rp->orow) * p.H + it.h; };
       ev(it.inc ? 3 : it.type2 ? 2 : 1);
       float acc[FA_CW];
-      float oscale;
-      if (it.inc) {
+      float oscale = 1.f;
+      if (it.t4) {
+        // ---- type 4: <= 32 exact rows, transposed. S^T in TMEM: lane = key (this thread: key kq of
+        // each tile), column = row (this warp: rows n0 .. n0+7). One pass over the N keys as in the
+        // single-pass type 2: P = 2^((s - ref) c) with ref = the first tile's row max (reduced over the
+        // lanes with an order-preserving integer redux, over the 4 quads through shared memory),
+        // written bf16 into the K-major P^T tile (B operand of O^T += V^T P^T); l per row summed per
+        // key thread and reduced once at the end. A row whose later scores exceed ref by > 2^100
+        // sends the item to the fixup launch (two-pass, as type 2).
+        const int kq = quad * 32 + lane;
+        const int n0 = hh * 8;
+        auto ford = [](float f) { const int i = __float_as_int(f); return i >= 0 ? i : i ^ 0x7fffffff; };
+        auto unord = [](int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); };
+        float ref[8], lp[8];
+        float over = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) lp[i] = 0.f;
+        for (int j = 0; j < NKT; ++j) {
+          const int sb = sc & 1;
+          fa_wait(&s_full[sb], (sc >> 1) & 1);
+          ++sc;
+          const int pb = pc & 1;
+          ++pc;
+          tc_fence_after();
+          float v[8];
+          tmem_ld8(trow + sb * FA_BK + n0, v);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_empty[sb]);
+          const bool kvalid = j * FA_BK + kq < p.N;
+          if (j == 0) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int m = __reduce_max_sync(0xffffffffu, ford(kvalid ? v[i] : -INFINITY));
+              if (lane == 0) x4[(hh * 4 + quad) * 8 + i] = unord(m);
+            }
+            fa_named_sync(5 + hh, 128);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              float m = x4[(hh * 4) * 8 + i];
+#pragma unroll
+              for (int q2 = 1; q2 < 4; ++q2) m = fmaxf(m, x4[(hh * 4 + q2) * 8 + i]);
+              ref[i] = m * c;
+            }
+            fa_named_sync(5 + hh, 128);
+          }
+          fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1);
+          // P^T element (row n, key kq): half kq / 64, row line n (128 B), 16-byte chunk
+          // ((kq % 64) / 8) ^ (n % 8) (128-byte swizzle), 2 bytes at (kq % 8)
+          const uint32_t pt = smem_u32(sPT + pb * FA_PT_BYTES + (kq >> 6) * (FA_PT_BYTES / 2)) + (kq & 7) * 2;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int n = n0 + i;
+            const float x = kvalid ? fmaf(v[i], c, -ref[i]) : -INFINITY;
+            if (n < it.nrows) over = fmaxf(over, x);
+            const float pv = ex2f(x);
+            lp[i] += pv;
+            const __nv_bfloat16 hb = __float2bfloat16_rn(pv);
+            const uint32_t addr = pt + n * 128 + ((((kq & 63) >> 3) ^ (n & 7)) << 4);
+            asm volatile("st.shared.b16 [%0], %1;" ::"r"(addr), "h"(*reinterpret_cast<const unsigned short *>(&hb)) : "memory");
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[pb]);
+        }
+        fa_wait(acc_full, ai & 1);
+        ++ai;
+        tc_fence_after();
+        float o[8];
+        tmem_ld8(trow + FA_ACC_COL + n0, o);   // O^T: lane = head dim kq, columns = rows n0 ..
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty);
+        // row sums: lanes (fixed butterfly order), then quads 0..3
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float t = warp_sum(lp[i]);
+          if (lane == 0) x4[(hh * 4 + quad) * 8 + i] = t;
+        }
+        fa_named_sync(5 + hh, 128);
+        float L[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float t = x4[(hh * 4) * 8 + i];
+#pragma unroll
+          for (int q2 = 1; q2 < 4; ++q2) t += x4[(hh * 4 + q2) * 8 + i];
+          L[i] = t;
+        }
+        // every softmax warp reads the rows' output ids fetched by the column-group-0 warp of quad 0
+        fa_named_sync(9, 32 * FA_NSW);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int n = n0 + i;
+          if (n < it.nrows) {
+            const int orr = rows_s[(ii % 3) * 128 + n].orow;
+            p.C_out[static_cast<int64_t>(orr) * p.qw + it.h * 128 + kq] = __float2bfloat16_rn(o[i] / L[i]);
+            if (p.stats != nullptr && quad == 0 && lane == i)
+              p.stats[static_cast<int64_t>(orr) * p.H + it.h] = make_float2(ref[i], L[i]);
+          }
+        }
+        if (__ballot_sync(0xffffffffu, over > 100.f) != 0u && lane == 0) {
+          const int pos = atomicAdd(&p.fix[0], 1);
+          if (pos < p.fix_cap) p.fix[1 + pos] = w;
+        }
+      } else if (it.inc) {
         // ---- type 3, incremental statistics (exact up to rounding): only the salient
         // keys changed since this row's statistics (m_old, l_old) were computed, so
         //   l_new = l_old 2^(m_old - m) - sum_j 2^(s_old_j c - m) + sum_j 2^(s_new_j c - m),
@@ -790,7 +980,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             for (int t = 0; t < 16; ++t) {
               const float x0 = v[ch * 32 + 2 * t], x1 = v[ch * 32 + 2 * t + 1];
               const float p0 = ex2f(fmaf(x0, c, -rc));
-              const float p1 = (t & 1) ? ex2p(fmaf(x1, c, -rc)) : ex2f(fmaf(x1, c, -rc));
+              const float p1 = (FA_POLY >= 2 || (t & 1)) ? ex2p(fmaf(x1, c, -rc)) : ex2f(fmaf(x1, c, -rc));
               l += p0 + p1;
               pk[t] = pack2(p0, p1);
             }
@@ -873,9 +1063,9 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < FA_CW; j += 4) {
           a0 += ex2f(fmaf(v[j], c, -mnc));
-          a1 += ex2f(fmaf(v[j + 1], c, -mnc));
+          a1 += FA_POLY >= 2 ? ex2p(fmaf(v[j + 1], c, -mnc)) : ex2f(fmaf(v[j + 1], c, -mnc));
           a2 += ex2f(fmaf(v[j + 2], c, -mnc));
-          a3 += ex2p(fmaf(v[j + 3], c, -mnc));  // a quarter of the exps on the FMA pipe
+          a3 += ex2p(fmaf(v[j + 3], c, -mnc));  // FA_POLY of 4 exps on the FMA pipe
         }
         l = l * ex2f((m - mn) * c) + ((a0 + a1) + (a2 + a3));
         m = mn;
@@ -930,7 +1120,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
               tmem_ld32(trow + sb * FA_BK + hh * FA_CW + ch * 32, v);
 #pragma unroll
               for (int t = 0; t < 16; ++t) {
-                const float e1 = (t & 1) ? ex2p(fmaf(v[2 * t + 1], c, -Mc)) : ex2f(fmaf(v[2 * t + 1], c, -Mc));
+                const float e1 = (FA_POLY >= 2 || (t & 1)) ? ex2p(fmaf(v[2 * t + 1], c, -Mc)) : ex2f(fmaf(v[2 * t + 1], c, -Mc));
                 const float p0 = (k0 + 2 * t < it.nkP) ? ex2f(fmaf(v[2 * t], c, -Mc)) : 0.f;
                 const float p1 = (k0 + 2 * t + 1 < it.nkP) ? e1 : 0.f;
                 pk[t] = pack2(p0, p1);
@@ -973,7 +1163,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       // rows x 16 bytes.
       static_assert(FA_CW == 32, "epilogue transpose assumes 4 chunks of 8 head dims per warp");
       {
-        const unsigned wmask = __ballot_sync(0xffffffffu, write_row());
+        const unsigned wmask = it.t4 ? 0u : __ballot_sync(0xffffffffu, write_row());
         if (wmask) {
           uint4 ch[4];
 #pragma unroll
@@ -1011,10 +1201,14 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         }
       }
       ev(52);
-      cq = nq;
-      if (cq.x >= 0) it = fa_item(p, cq.x, cq.y, cq.z);
+      if (nw >= 0) it = wqi[ns];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&wq_empty[ii & 3]);
+      cw = nw;
       ++ii;
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&wq_empty[ii & 3]);  // the terminator's slot
   }
   ev.finish();
   __syncthreads();
@@ -1077,6 +1271,7 @@ int attention_fused_launch(const AttnArgs &a, cudaStream_t st) {
   p.mode = a.mode;
   p.fix = a.fix;
   p.fix_cap = a.fix_cap;
+  p.t4max = g_attn_t4_rows;
   if (!p.fix) {
     set_error("fused attention: missing fixup list");
     return DYLLM_E_ARG;

@@ -848,6 +848,11 @@ int dyllm_set_option(int option, int value) {
     g_attn_inc_enabled = value != 0;
     return prev;
   }
+  if (option == DYLLM_OPT_ATTN_T4) {
+    const int prev = g_attn_t4_rows;
+    g_attn_t4_rows = value < 0 ? 0 : (value > 32 ? 32 : value);
+    return prev;
+  }
   if (option == DYLLM_OPT_SKINNY_SPLIT) {
     const int prev = g_skinny_split;
     g_skinny_split = value < 0 ? 0 : value;

@@ -141,6 +141,7 @@ int attention_fused_launch(const AttnArgs &a, cudaStream_t st);  // attn_fused.c
 // true when attention_launch writes the delta dC (not C) for the approximate rows of a sparse step
 bool attention_writes_delta(int hd);
 extern bool g_attn_fused_enabled;  // test hook (dyllm_set_option)
+extern int g_attn_t4_rows;        // fused attention: exact-row items of <= this many rows run transposed (0: off)
 extern unsigned long long *g_attn_trace;  // debug hook (dyllm_debug_trace_buffer, which = 1)
 extern unsigned long long *g_attn_events;  // debug hook (dyllm_debug_trace_buffer, which = 2)
 

@@ -17,7 +17,11 @@ from synth import configs, gen  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--mode", default="ro")
+ap.add_argument("--opt", default="", help="option=value[,option=value] set before the run (dy.OPT_* numbers)")
 a = ap.parse_args()
+for kv in filter(None, a.opt.split(",")):
+    k, v = kv.split("=")
+    dy.set_option(int(k), int(v))
 cfg, run = configs.preset("llada8b")
 run = replace(run, select_mode=1)
 ctx = dy.Context(0)
