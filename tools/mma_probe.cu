@@ -24,7 +24,9 @@ __host__ __device__ constexpr uint32_t idesc(int M, int N, bool b_mn) {
          (static_cast<uint32_t>(M >> 4) << 24);
 }
 
-template <int MODE>  // 0: SS N=128, 1: SS N=256, 2: TS N=128 B MN-major, 3: TS N=128 B K-major
+// 0: SS N=128, 1: SS N=256, 2: TS N=128 B MN-major, 3: TS N=128 B K-major, 4: SS N=32, 5: SS N=64,
+// 6: SS N=32 with A MN-major (the transposed O^T = V^T P^T of the attention's type-4 tiles)
+template <int MODE>
 __global__ void __launch_bounds__(128, 1) mma_probe(unsigned long long *out, int iters) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *sm = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -47,13 +49,19 @@ __global__ void __launch_bounds__(128, 1) mma_probe(unsigned long long *out, int
   const uint32_t tm = slot;
   if (threadIdx.x == 0) {
     const uint32_t a = smem_u32(sm), b = a + 32768;
-    constexpr int N = MODE == 1 ? 256 : 128;
-    constexpr uint32_t id = idesc(128, N, MODE == 2);
+    constexpr int N = MODE == 1 ? 256 : (MODE == 4 || MODE == 6) ? 32 : MODE == 5 ? 64 : 128;
+    constexpr uint32_t id = idesc(128, N, MODE == 2) | (MODE == 6 ? (1u << 15) : 0u);
     const unsigned long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
       const uint32_t acc = i > 0;
       const int kk = i & 7;
-      if (MODE <= 1) {
+      if (MODE == 6) {
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tm),
+                     "l"(desc_mn(a + kk * 2048, 16384)), "l"(desc_k(b + (kk >> 2) * 4096 + (kk & 3) * 32)),
+                     "r"(id), "r"(acc)
+                     : "memory");
+      } else if (MODE <= 1 || MODE == 4 || MODE == 5) {
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tm),
                      "l"(desc_k(a + (kk >> 2) * 16384 + (kk & 3) * 32)), "l"(desc_k(b + (kk >> 2) * 16384 + (kk & 3) * 32)),
@@ -112,6 +120,9 @@ int main() {
     run<1>("SS K-major M128 N256", g, 128);
     run<2>("TS B MN-major M128 N128", g, 64);
     run<3>("TS B K-major M128 N128", g, 64);
+    run<4>("SS K-major M128 N32", g, 16);
+    run<5>("SS K-major M128 N64", g, 32);
+    run<6>("SS A MN-major M128 N32", g, 16);
   }
   printf("status: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
