@@ -25,8 +25,10 @@ __host__ __device__ constexpr uint32_t idesc(int M, int N, bool b_mn) {
 }
 
 // 0: SS N=128, 1: SS N=256, 2: TS N=128 B MN-major, 3: TS N=128 B K-major, 4: SS N=32, 5: SS N=64,
-// 6: SS N=32 with A MN-major (the transposed O^T = V^T P^T of the attention's type-4 tiles)
-template <int MODE>
+// 6: SS N=32 with A MN-major (the transposed O^T = V^T P^T of the attention's type-4 tiles),
+// 7 / 8: SS N=32 from one issuer alternating over 2 / 4 independent accumulators (is the ~73-cycle
+// single-issuer rate an accumulate dependency or an issue cost?)
+template <int MODE, int NW = 1, bool LANES = false>
 __global__ void __launch_bounds__(128, 1) mma_probe(unsigned long long *out, int iters) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *sm = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -35,7 +37,7 @@ __global__ void __launch_bounds__(128, 1) mma_probe(unsigned long long *out, int
   for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(sm)[i] = 0;
   const int warp = threadIdx.x / 32;
   if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar)), "r"(NW) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -46,10 +48,11 @@ __global__ void __launch_bounds__(128, 1) mma_probe(unsigned long long *out, int
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tm = slot;
-  if (threadIdx.x == 0) {
+  const int issuer = LANES ? threadIdx.x : warp;  // LANES: lanes 0..NW-1 of warp 0 (divergent)
+  const uint32_t tm = slot + (issuer % NW) * 128 * (MODE == 4 || MODE == 6 || MODE == 5);
+  if (LANES ? threadIdx.x < NW : (threadIdx.x % 32 == 0 && warp < NW)) {
     const uint32_t a = smem_u32(sm), b = a + 32768;
-    constexpr int N = MODE == 1 ? 256 : (MODE == 4 || MODE == 6) ? 32 : MODE == 5 ? 64 : 128;
+    constexpr int N = MODE == 1 ? 256 : (MODE == 4 || MODE >= 6) ? 32 : MODE == 5 ? 64 : 128;
     constexpr uint32_t id = idesc(128, N, MODE == 2) | (MODE == 6 ? (1u << 15) : 0u);
     const unsigned long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
@@ -59,6 +62,13 @@ __global__ void __launch_bounds__(128, 1) mma_probe(unsigned long long *out, int
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tm),
                      "l"(desc_mn(a + kk * 2048, 16384)), "l"(desc_k(b + (kk >> 2) * 4096 + (kk & 3) * 32)),
+                     "r"(id), "r"(acc)
+                     : "memory");
+      } else if (MODE == 7 || MODE == 8) {
+        const uint32_t dacc = tm + (MODE == 7 ? (i & 1) : (i & 3)) * 32;
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dacc),
+                     "l"(desc_k(a + (kk >> 2) * 16384 + (kk & 3) * 32)), "l"(desc_k(b + (kk >> 2) * 16384 + (kk & 3) * 32)),
                      "r"(id), "r"(acc)
                      : "memory");
       } else if (MODE <= 1 || MODE == 4 || MODE == 5) {
@@ -83,21 +93,21 @@ __global__ void __launch_bounds__(128, 1) mma_probe(unsigned long long *out, int
                    : "=r"(ok)
                    : "r"(smem_u32(&bar))
                    : "memory");
-    out[blockIdx.x] = clock64() - t0;
+    if (threadIdx.x == 0) out[blockIdx.x] = clock64() - t0;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
 }
 
-template <int MODE>
+template <int MODE, int NW = 1, bool LANES = false>
 void run(const char *name, int sms, int floor_cyc) {
   unsigned long long *d;
   cudaMalloc(&d, sms * sizeof(unsigned long long));
   const int smem = 96 * 1024 + 1024;
-  cudaFuncSetAttribute(mma_probe<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(mma_probe<MODE, NW, LANES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 8192;
-  for (int rep = 0; rep < 2; ++rep) mma_probe<MODE><<<sms, 128, smem>>>(d, iters);
+  for (int rep = 0; rep < 2; ++rep) mma_probe<MODE, NW, LANES><<<sms, 128, smem>>>(d, iters);
   cudaDeviceSynchronize();
   unsigned long long h[148];
   cudaMemcpy(h, d, sizeof(unsigned long long) * (sms < 148 ? sms : 148), cudaMemcpyDeviceToHost);
@@ -107,7 +117,7 @@ void run(const char *name, int sms, int floor_cyc) {
     sum += h[i];
     mx = h[i] > mx ? h[i] : mx;
   }
-  printf("%-28s grid=%3d: %.1f cycles/MMA (mean), %.1f (max CTA); floor %d  -> %.0f%% of floor rate\n", name, sms,
+  printf("%-28s x%d grid=%3d: %.1f cycles/MMA per issuer (mean), %.1f (max CTA); floor %d  -> %.0f%% of floor rate\n", name, NW, sms,
          sum / n / iters, mx / iters, floor_cyc, 100.0 * floor_cyc / (sum / n / iters));
   cudaFree(d);
 }
@@ -123,6 +133,12 @@ int main() {
     run<4>("SS K-major M128 N32", g, 16);
     run<5>("SS K-major M128 N64", g, 32);
     run<6>("SS A MN-major M128 N32", g, 16);
+    run<4, 2>("SS K-major M128 N32", g, 16);
+    run<5, 2>("SS K-major M128 N64", g, 32);
+    run<4, 4>("SS K-major M128 N32", g, 16);
+    run<4, 2, true>("SS N32 2 lanes of 1 warp", g, 16);
+    run<7>("SS N32 2 accumulators", g, 16);
+    run<8>("SS N32 4 accumulators", g, 16);
   }
   printf("status: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
