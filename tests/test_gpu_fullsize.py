@@ -84,6 +84,16 @@ def test_layer_step_full_size_sampled(big, mode, frac_in):
     _check_full_size(big, mode, frac_in)
 
 
+def test_layer_step_full_size_sampled_untransposed(big):
+    """Response-only step (26 exact rows per sequence) with the transposed exact-row tiles off."""
+    dy = big[0]
+    prev = dy.set_option(dy.OPT_ATTN_T4, 0)
+    try:
+        _check_full_size(big, "ro", 0.10)
+    finally:
+        dy.set_option(dy.OPT_ATTN_T4, prev)
+
+
 @pytest.mark.parametrize("mode,frac_in", [("ro", 0.06), ("fi", 0.06)])
 def test_layer_step_full_size_sampled_dream(big_dream, mode, frac_in):
     """Dream-7B layer shape (GQA 28 q / 4 kv heads, QKV bias, FFN 18944), L_P 160 + L_R 512."""

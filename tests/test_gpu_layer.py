@@ -159,6 +159,21 @@ def test_layer_step_incremental_statistics(name, mode, select_mode):
     _teacher_forced_layer(name, 1, mode, select_mode=select_mode, refresh=True)
 
 
+@pytest.mark.parametrize("name", ["small128", "small128_gqa"])
+@pytest.mark.parametrize("mode", ["fi", "ro"])
+@pytest.mark.parametrize("t4", [0, 32])
+def test_layer_step_exact_rows_transposed_option(name, mode, t4):
+    """Exact-row tiles of <= 32 rows run transposed by default (type 4: S^T = K Q^T, O^T = V^T P^T,
+    DYLLM_OPT_ATTN_T4 = 32); with the option at 0 they take the 128-row type-2 path. Both match
+    Alg. 3/4."""
+    from paper_2603_08026_b200 import dyllm as dyl
+    prev = dyl.set_option(dyl.OPT_ATTN_T4, t4)
+    try:
+        _teacher_forced_layer(name, 1, mode, refresh=True)
+    finally:
+        dyl.set_option(dyl.OPT_ATTN_T4, prev)
+
+
 @pytest.mark.parametrize("mode", ["fi", "ro"])
 def test_layer_step_single_pass_overflow_fixup(mode):
     """An exact row whose later key outscores its first key tile by ~2^127: two-pass fixup."""
