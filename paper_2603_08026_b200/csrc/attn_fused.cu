@@ -10,18 +10,23 @@
 //                dC = P dV (Alg. 4 lines 3-4, dV compact, aligned with idx_in);
 //       output : approximate rows (not in idx_in): the delta dC / l (C_new = C_cache + dC is
 //                formed by the similarity kernel, which reads C_cache anyway — no second read).
-//   type 2 — up to 128 exact rows (idx_in, compact new queries Qx) of s, one pass over the N keys
-//       (online softmax): P = exp2(s - ref) with a per-row reference ref = the first tile's row
-//       max, raised (and the accumulator rescaled in TMEM) only when a later tile's max exceeds it
-//       by more than 2^8; O = P V, l = sum P; output C = O / l scattered to the exact rows.
-// Roles (384 threads, 1 CTA per SM): warp 0 claims items and loads Q (double-buffered), warps 0 and
-// 11 load alternate 128-key K tiles (2-deep ring), warp 10 loads V / dV tiles (2-deep ring) — one
-// 32 KB 3D TMA op per tile, spread over three issuing warps, since TMA issue throughput is per
-// operation and per issuing thread (~700 cycles per op per thread, tools/tma_probe.cu) — warp 1
-// single-thread tcgen05.mma issuer (S = Q K^T, M = N = 128, into a double-buffered fp32 TMEM tile;
-// P V into a 128x128 fp32 TMEM accumulator with P read from TMEM and V as an MN-major smem
-// operand), warps 2-9 softmax/epilogue: two warps per TMEM lane quadrant, one row per thread, 64 of
-// the 128 columns of each score tile each; P is stored bf16x2-packed into TMEM with tcgen05.st.
+//   type 3 — (incremental statistics) a response tile whose cached (m, l) are
+//       current: S over the salient keys' new and old K only, l updated by the difference, P dV as
+//       in pass P; a row whose l cancels below 2^-14 sends its tile to the dense fixup launch.
+//   type 2 — 33..128 exact rows (idx_in, compact new queries Qx) of s, one pass over the N keys:
+//       P = exp2(s - ref) with ref = the first tile's row max (a row whose later scores exceed it by
+//       more than 2^100 sends the item to the fixup launch, which re-runs it in two passes);
+//       O = P V, l = sum P; output C = O / l scattered to the exact rows.
+//   type 4 — <= 32 exact rows: type 2 transposed (S^T = K Q^T with the keys on the 128 MMA rows,
+//       O^T += V^T P^T with P^T in shared memory), so the exps spread over all 16 softmax warps.
+// Roles (640 threads, 1 CTA per SM): warp 0 claims items (decoded once, passed through a 4-slot
+// shared-memory queue) and loads Q (double-buffered); warps 0, 18 and 19 load the K / V / dV tiles
+// of a unified 4-slot ring in the MMA's consumption order, each every third tile (one 32 KB 3-D TMA
+// op per tile; TMA issue throughput is per issuing thread, tools/tma_probe.cu); warp 1 lane 0 issues
+// every tcgen05.mma (S = Q K^T into a double-buffered fp32 TMEM tile; P V into a 128x128 fp32 TMEM
+// accumulator with P read from TMEM and V as an MN-major smem operand); warps 2-17 are the softmax /
+// epilogue warps: four per TMEM lane quadrant, one row per thread, 32 of the 128 key columns of
+// each score tile each; P is stored bf16x2-packed into TMEM with tcgen05.st.
 #include "common.cuh"
 #include "internal.h"
 
