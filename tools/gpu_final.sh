@@ -1,4 +1,5 @@
 mkdir -p gpurun_out
+python -m paper_2603_08026_b200.build > gpurun_out/final_build.log 2>&1
 python -c "import __graft_entry__ as g; g.smoke(); print('SMOKE OK')" > gpurun_out/final_smoke.log 2>&1; tail -2 gpurun_out/final_smoke.log
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/final_tests.log 2>&1; tail -2 gpurun_out/final_tests.log
 timeout 900 python bench.py > gpurun_out/final_bench.json 2>gpurun_out/final_bench.err; tail -1 gpurun_out/final_bench.json | cut -c1-160
