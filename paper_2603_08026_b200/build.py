@@ -30,6 +30,11 @@ def _newer(target, deps):
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
+    # objects built with other flags (e.g. a DYLLM_NVCC_FLAGS debug build) are not reused
+    stamp = os.path.join(OBJ, "flags.txt")
+    want = " ".join(FLAGS)
+    if not os.path.exists(stamp) or open(stamp).read() != want:
+        force = True
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(os.path.dirname(HERE), "include", "dyllm.h"))
     jobs = []
@@ -53,6 +58,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for s in ex.map(compile_one, jobs):
             if verbose:
                 print("compiled", s)
+    with open(stamp, "w") as f:
+        f.write(want)
     objs = [os.path.join(OBJ, s.replace(".cu", ".o")) for s in SOURCES]
     if force or jobs or _newer(LIB, objs):
         cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs,
