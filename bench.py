@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--profile-steps", type=int, default=1, help="extra untimed generations with per-kernel events")
+    ap.add_argument("--lib-opt", default="", help="library options for A/B runs: option=value[,...] (dyllm_set_option)")
     return ap.parse_args()
 
 
@@ -308,6 +309,9 @@ def main():
     from paper_2603_08026_b200 import dyllm as dy
     from paper_2603_08026_b200 import dist as pd
 
+    for kv in filter(None, args.lib_opt.split(",")):
+        k, v = kv.split("=")
+        dy.set_option(int(k), int(v))
     rank, world, local = pd.env_rank()
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))

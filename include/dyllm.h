@@ -224,9 +224,11 @@ uint64_t dyllm_launch_count(void);
  * setup overlaps its predecessor; each kernel waits for its predecessor before touching memory). */
 /* DYLLM_OPT_ATTN_INC (default 1): incremental softmax statistics for response tiles (see
  * dyllm_cache_refresh_stats); 0 = every tile computes its normaliser over all N keys. */
-/* DYLLM_OPT_ATTN_T4 (default 32, range 0..32): the fused attention computes exact-row tiles of at
- * most this many rows transposed (S^T = K Q^T with the keys on the 128 MMA rows, O^T = V^T P^T), so
- * the tensor and exp work follows the row count instead of a 128-row tile; 0 disables. */
+/* DYLLM_OPT_ATTN_T4 (default 32, range 0..32): in libraries built with -DDYLLM_FA_T4=1, the fused
+ * attention computes exact-row tiles of at most this many rows transposed (S^T = K Q^T with the
+ * keys on the 128 MMA rows, O^T = V^T P^T), so the tensor and exp work follows the row count
+ * instead of a 128-row tile; 0 disables. The default build compiles those tiles out (measured
+ * faster overall) and accepts the option without effect. */
 enum { DYLLM_OPT_SKINNY_GEMM = 1, DYLLM_OPT_SKINNY_SPLIT = 2, DYLLM_OPT_ATTN_FUSED = 3, DYLLM_OPT_SKINNY_ONE_CHUNK = 4,
        DYLLM_OPT_PDL = 5, DYLLM_OPT_ATTN_INC = 6, DYLLM_OPT_ATTN_T4 = 7 };
 int dyllm_set_option(int option, int value);

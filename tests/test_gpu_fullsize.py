@@ -85,7 +85,8 @@ def test_layer_step_full_size_sampled(big, mode, frac_in):
 
 
 def test_layer_step_full_size_sampled_untransposed(big):
-    """Response-only step (26 exact rows per sequence) with the transposed exact-row tiles off."""
+    """Response-only step (26 exact rows per sequence) with the transposed exact-row tiles off
+    (only differs from the default in -DDYLLM_FA_T4=1 builds)."""
     dy = big[0]
     prev = dy.set_option(dy.OPT_ATTN_T4, 0)
     try:

@@ -163,8 +163,9 @@ def test_layer_step_incremental_statistics(name, mode, select_mode):
 @pytest.mark.parametrize("mode", ["fi", "ro"])
 @pytest.mark.parametrize("t4", [0, 32])
 def test_layer_step_exact_rows_transposed_option(name, mode, t4):
-    """Exact-row tiles of <= 32 rows run transposed by default (type 4: S^T = K Q^T, O^T = V^T P^T,
-    DYLLM_OPT_ATTN_T4 = 32); with the option at 0 they take the 128-row type-2 path. Both match
+    """Exact-row tiles of <= 32 rows: with a -DDYLLM_FA_T4=1 build they run transposed (type 4:
+    S^T = K Q^T, O^T = V^T P^T) at DYLLM_OPT_ATTN_T4 = 32 and take the 128-row type-2 path at 0;
+    the default build compiles type 4 out and both settings take type 2. Every form matches
     Alg. 3/4."""
     from paper_2603_08026_b200 import dyllm as dyl
     prev = dyl.set_option(dyl.OPT_ATTN_T4, t4)

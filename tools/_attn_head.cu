@@ -34,15 +34,6 @@ namespace dy {
 
 int g_attn_t4_rows = 32;
 
-// Type-4 tiles (exact-row items of <= 32 rows computed transposed) are compiled only with
-// -DDYLLM_FA_T4=1. Measured on one box (tools/gpu_exp62.sh): with them compiled in, the kernel's
-// register allocation spills on the other item types' hot loops (76 B vs 12 B) and the attention
-// class averages 169 us per launch (type 4 on) against 152 us with the code compiled out; an
-// out-of-line type-4 function was slower still (199 us).
-#ifndef DYLLM_FA_T4
-#define DYLLM_FA_T4 0
-#endif
-
 constexpr int FA_BK = 128;                 // keys per tile (MMA N = 128: the Q operand read per
                                            // instruction is amortised over 128 keys)
 constexpr int FA_Q_BYTES = 128 * 256;      // 128 rows x 128 bf16: two 64-column halves of 16 KB
@@ -135,7 +126,7 @@ __device__ __forceinline__ FaItem fa_item(const FaParams &p, int w, int off, int
     it.nkP = p.N;
     it.inc = false;
     it.single = p.mode != 1;
-    it.t4 = DYLLM_FA_T4 && it.single && it.nrows <= p.t4max;
+    it.t4 = it.single && it.nrows <= p.t4max;
   }
   return it;
 }
@@ -539,7 +530,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           umma_commit(&q_empty[qb]);
           continue;
         }
-        if (DYLLM_FA_T4 && it.t4) {
+        if (it.t4) {
           // type 4 (<= 32 exact rows), transposed: S^T = K Q^T (M = 128 keys, N = 32 rows: the K tile
           // is the A operand, the Q tile's first 32 rows the B operand, both K-major as loaded) and
           // O^T += V^T P^T (A = V, MN-major as loaded; B = P^T written by the softmax warps into a
@@ -679,7 +670,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       ev(it.inc ? 3 : it.type2 ? 2 : 1);
       float acc[FA_CW];
       float oscale = 1.f;
-      if (DYLLM_FA_T4 && it.t4) {
+      if (it.t4) {
         // ---- type 4: <= 32 exact rows, transposed. S^T in TMEM: lane = key (this thread: key kq of
         // each tile), column = row (this warp: rows n0 .. n0+7). One pass over the N keys as in the
         // single-pass type 2: P = 2^((s - ref) c) with ref = the first tile's row max (reduced over the
@@ -1177,7 +1168,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       // rows x 16 bytes.
       static_assert(FA_CW == 32, "epilogue transpose assumes 4 chunks of 8 head dims per warp");
       {
-        const unsigned wmask = (DYLLM_FA_T4 && it.t4) ? 0u : __ballot_sync(0xffffffffu, write_row());
+        const unsigned wmask = it.t4 ? 0u : __ballot_sync(0xffffffffu, write_row());
         if (wmask) {
           uint4 ch[4];
 #pragma unroll
