@@ -1,3 +1,4 @@
+# needs tools/_attn_head.cu = git show b51de24:paper_2603_08026_b200/csrc/attn_fused.cu (not committed)
 mkdir -p gpurun_out
 : > gpurun_out/exp63.log
 python -m paper_2603_08026_b200.build --force > /dev/null 2>&1
