@@ -172,6 +172,9 @@ __device__ __forceinline__ float ex2p(float x) {
 // Exps per group of 4 computed on the FMA pipe (ex2p) in the dense passes; the rest on MUFU.
 // ncu shows the XU pipe near saturation in full-input steps (profiles/r1l_attn_fi_full.md), but
 // 2 of 4 measured slower than 1 of 4 (tools/gpu_exp44.sh: full-input step 35.2 vs 34.7 ms).
+#ifndef DYLLM_FA_KACT
+#define DYLLM_FA_KACT 1  // type 3: warps whose key columns hold no salient key skip their exps
+#endif
 #ifndef DYLLM_FA_POLY
 #define DYLLM_FA_POLY 1
 #endif
@@ -793,7 +796,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         float2 so = make_float2(0.f, 1.f);
         // this warp's 32 key columns hold salient keys (else: no exps, P = 0 — the MUFU work
         // follows the salient key count, not the 128-key tile)
-        const bool kact = hh * FA_CW < it.nkP;
+        const bool kact = !DYLLM_FA_KACT || hh * FA_CW < it.nkP;
         float part = 0.f, mref = 0.f;
         {
           const int sb = sc & 1;
