@@ -325,6 +325,16 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
   pdl_trigger();  // grid <= #SMs at one CTA per SM: resident, the next kernel may launch
+  // fixup launch with an empty list (the common case): nothing to claim, no counters touched
+  if (p.mode == 1 && *reinterpret_cast<volatile const int *>(p.fix) == 0) {
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+      tc_fence_after();
+      tmem_dealloc(tmem, FA_TMEM_COLS);
+    }
+    return;
+  }
   // Dynamic scheduling: the producer thread claims items with an atomic counter (items of one
   // (sequence, kv head) stay adjacent in claim order, so concurrently running CTAs share K/V in L2,
   // and heavy exact-row items no longer pile up on fixed CTAs) and passes them to the other roles
