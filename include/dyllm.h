@@ -63,7 +63,8 @@ typedef struct {
 typedef struct {
   int32_t batch, L_P, L_R;
   int32_t block;         /* semi-AR block size B; must divide L_R */
-  int32_t n_u;           /* tokens unmasked per step per sequence */
+  int32_t n_u;           /* tokens unmasked per step per sequence; must divide block so
+                            that T_total = L_R / n_u steps unmask every position */
   int32_t T_full;        /* warm-up FullSteps */
   int32_t full_period;   /* sparse step takes Concat(P,R) when t % full_period == 0 */
   int32_t layer1_policy; /* 0: carried (Alg. 1 literal); 1: carried ∪ decoded (D5, default) */
@@ -77,8 +78,11 @@ typedef struct {
 /* input_mode of dyllm_layer_step / dyllm_select_salient */
 enum { DYLLM_INPUT_FULL = 0 /* Concat(P,R): rows [0,N) */, DYLLM_INPUT_RESPONSE = 1 /* R: rows [L_P,N) */ };
 
-/* `which` of dyllm_cache_copy */
-enum { DYLLM_K = 0, DYLLM_V = 1, DYLLM_Q = 2, DYLLM_C = 3, DYLLM_H = 4 };
+/* `which` of dyllm_cache_tensor / dyllm_cache_copy. DYLLM_STATS (head_dim 128 only): the per-(row,
+ * head) softmax statistics of the fused attention, float2 (m, l) [batch][N][n_heads] with
+ * m = row max of the scores in the exp2 domain (s * log2(e) / sqrt(head_dim)) and l = sum of
+ * 2^(score - m) over all N keys, i.e. log2 of Alg. 4's softmax normaliser is m + log2(l). */
+enum { DYLLM_K = 0, DYLLM_V = 1, DYLLM_Q = 2, DYLLM_C = 3, DYLLM_H = 4, DYLLM_STATS = 5 };
 
 /* ------------------------------------------------------------------ context */
 const char *dyllm_last_error(void);
@@ -158,12 +162,16 @@ int dyllm_full_step(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int3
 int dyllm_unmask(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int32_t *d_tokens, int32_t *d_dec_pos,
                  int32_t *d_dec_tok);
 
-/* Device pointer to one cache tensor of one layer (layer in [0,n_layers); which = DYLLM_K..H;
+/* Device pointer to one cache tensor of one layer (layer in [0,n_layers); which = DYLLM_K..STATS;
  * for DYLLM_H, layer in [0, n_layers] where H_0 = embeddings). Synchronous, no copy. Handing out
- * K or Q invalidates the layer's incremental attention statistics (see dyllm_cache_refresh_stats). */
+ * K, Q or STATS (writable views) invalidates the layer's incremental attention statistics (see
+ * dyllm_cache_refresh_stats). DYLLM_E_STATE for STATS when the head_dim keeps none. */
 int dyllm_cache_tensor(const dyllm_cache *c, int layer, int which, void **d_ptr, int64_t *n_elems);
 /* Copy a cache tensor to (export=1) or from (export=0) `ptr`; `ptr_on_device` = 1 if ptr is
- * device memory. Asynchronous on the ctx stream. Test / teacher-forcing hook. */
+ * device memory (bf16 tensors: 2 B per element, STATS: 8 B). Asynchronous on the ctx stream.
+ * Test / teacher-forcing hook. An export leaves the statistics valid; importing K or
+ * Q invalidates them; importing STATS marks them current (the caller asserts they belong to the
+ * layer's K and Q). */
 int dyllm_cache_copy(dyllm_ctx *ctx, dyllm_cache *c, int layer, int which, void *ptr,
                      int ptr_on_device, int export_);
 /* Recompute, densely, the per-(row, head) softmax statistics (row max, sum of exps) of one layer
@@ -176,6 +184,18 @@ int dyllm_cache_copy(dyllm_ctx *ctx, dyllm_cache *c, int layer, int which, void 
 int dyllm_cache_refresh_stats(dyllm_ctx *ctx, dyllm_cache *c, int layer);
 /* Set the carried salient list (idx_sal between steps) — test hook; NULL resets to None. */
 int dyllm_cache_set_carried(dyllm_ctx *ctx, dyllm_cache *c, const int32_t *d_idx, const int32_t *d_off);
+
+/* Set the rows decoded at the previous step (Alg. 1 line 21; their embeddings changed and
+ * they enter layer-1 idx_in under layer1_policy 1, D5, or get a Q-only refresh under policy 0) —
+ * test hook for resynchronised multi-step parity. d_dec = [batch][n_u] row ids
+ * (-1 = none), device memory; NULL = no decoded rows. Asynchronous. */
+int dyllm_cache_set_decoded(dyllm_ctx *ctx, dyllm_cache *c, const int32_t *d_dec);
+/* Per-layer trace of dyllm_denoise_step's sparse steps (parity and paper-analysis hook, SURVEY
+ * §8c.4 / §8f4): when d_lists != NULL, layer l's selected list idx_out (row ids) is copied to
+ * d_lists + l*batch*N and its offsets to d_offs + l*(batch+1); when d_sims != NULL, s of every
+ * input row r of layer l is written to d_sims[l*batch*N + r]. Caller-owned device buffers that
+ * must outlive the traced steps; NULLs disable. d_lists and d_offs are both set or both NULL. */
+int dyllm_cache_set_trace(dyllm_ctx *ctx, dyllm_cache *c, int32_t *d_lists, int32_t *d_offs, float *d_sims);
 
 /* ------------------------------------------------------------------ kernel-level calls */
 /* K1: temporal cosine similarity of C_new vs C_cache for the input rows of every

@@ -362,6 +362,7 @@ class SeqState:
     idx_carried: np.ndarray = None                  # idx_sal across steps (None until first sparse step)
     decoded_prev: np.ndarray = field(default_factory=lambda: np.zeros(0, dtype=np.int64))
     sal_counts: list = field(default_factory=list)  # per step: [n_layers] salient counts
+    layer_results: list = field(default_factory=list)  # SparseLayerResult per layer of the last sparse step
 
 
 def init_state(prompt, cfg, run):
@@ -404,6 +405,7 @@ def sparse_step(st, W, cfg, run, mode, tau, q_mode="cache"):
     st.H0 = W["emb"][st.tokens]                                     # Alg. 3 line 1
     x_all = st.H0
     counts = []
+    st.layer_results = []
     taus = np.broadcast_to(np.asarray(tau, dtype=np.float64), (cfg.n_layers,))
     for l, lw in enumerate(W["layers"]):
         thr = taus[l]
@@ -412,6 +414,7 @@ def sparse_step(st, W, cfg, run, mode, tau, q_mode="cache"):
         r = sparse_layer(x_all, st.caches[l], lw, cfg, idx, thr, input_rows, run.cmp,
                          q_mode=q_mode, q_extra=q_extra if l == 0 else ())
         idx = r.idx_out
+        st.layer_results.append(r)
         counts.append(len(idx))
         x_all = st.caches[l].H
     st.idx_carried = idx                                              # P:819 / P:902

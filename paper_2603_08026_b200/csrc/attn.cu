@@ -595,11 +595,11 @@ __global__ void __launch_bounds__(128) attn_pv_kernel(const AttnArgs a) {
 
 template <int HD>
 static int launch_fused(const AttnArgs &a, cudaStream_t st) {
-  static bool attr = false;
+  static DeviceOnce attr;
   const int smem = AttnSmem<HD>::BYTES;
-  if (!attr) {
+  if (attr.todo()) {
     DY_CUDA(cudaFuncSetAttribute(attn_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
+    attr.done();
   }
   const int T = (a.max_rows_per_seq + BQ - 1) / BQ;
   if (T <= 0) return DYLLM_OK;
@@ -614,12 +614,12 @@ static int launch_split(const AttnArgs &a, cudaStream_t st) {
   // 1) tcgen05 row statistics over all input rows
   constexpr int KB = HD / 64;
   const int smem_stats = 1024 + 2 * KB * 128 * 128 + ST_STAGES * ST_BN * 128 + 256;
-  static bool attr = false;
-  if (!attr) {
+  static DeviceOnce attr;
+  if (attr.todo()) {
     DY_CUDA(cudaFuncSetAttribute(attn_stats_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_stats));
     DY_CUDA(cudaFuncSetAttribute(attn_pv_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  AttnSmem<HD>::BYTES));
-    attr = true;
+    attr.done();
   }
   const int rows_total = a.batch * a.N;
   CUtensorMap tq, tk;

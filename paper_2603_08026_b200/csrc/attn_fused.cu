@@ -381,8 +381,11 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       for (;;) {
         w = atomicAdd(&p.work_ctr[0], 1);
         if (p.mode == 1) {  // fixup launch: the listed tiles, processed densely
-          const int nfix = min(p.fix[0], p.fix_cap);
-          w = w < nfix ? p.fix[1 + w] : -1;
+          const int nfix = p.fix[0];
+          if (nfix > p.fix_cap)  // the list overflowed (entries were dropped): every item, densely
+            w = w < p.items ? w : -1;
+          else
+            w = w < nfix ? p.fix[1 + w] : -1;
           if (w < 0) break;
         } else if (w >= p.items) {
           w = -1;
@@ -1256,10 +1259,10 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
 }
 
 int attention_fused_launch(const AttnArgs &a, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static DeviceOnce attr;
+  if (attr.todo()) {
     DY_CUDA(cudaFuncSetAttribute(attn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_SMEM));
-    attr = true;
+    attr.done();
   }
   const int rows_total = a.batch * a.N;
   const int qw = a.H * 128, kw = a.KVH * 128;

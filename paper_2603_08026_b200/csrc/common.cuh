@@ -11,7 +11,24 @@
 
 typedef __nv_bfloat16 bf16;
 
+#include <atomic>
+
 namespace dy {
+
+// Per-device "once" flag for host-side kernel attributes (cudaFuncSetAttribute is per device): a
+// second context on another GPU of the same process sets them again. Setting an attribute twice
+// is harmless, so concurrent first calls need no lock.
+struct DeviceOnce {
+  static constexpr int kMaxDev = 64;
+  std::atomic<uint64_t> mask{0};
+  static int device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d < kMaxDev ? d : kMaxDev - 1;
+  }
+  bool todo() const { return !(mask.load(std::memory_order_acquire) & (1ull << device())); }
+  void done() { mask.fetch_or(1ull << device(), std::memory_order_release); }
+};
 
 constexpr int kWarp = 32;
 

@@ -127,6 +127,9 @@ struct dyllm_cache {
   bool carried_valid = false;
   int *ap_rows, *ap_off, *all_rows, *all_off, *zero_off, *lm_rows, *lm_off;
   int *dec_prev;
+  int *qx_rows, *qx_off;  // layer1_policy 0: decoded rows outside idx_in (Q-only refresh, D6)
+  int32_t *tr_lists = nullptr, *tr_offs = nullptr;  // dyllm_cache_set_trace (caller-owned)
+  float *tr_sims = nullptr;
   float *sim;  // per-row similarity scratch (fraction mode)
   float2 *rope_cs;  // [N][head_dim/2] (cos, sin) table
   float2 *stats;    // [b*N][H] attention row statistics scratch
@@ -394,10 +397,10 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
   CHECK_ARG(ctx && w && r && out, "null argument");
   const dyllm_model_cfg &m = w->cfg;
   if (r->batch < 1 || r->batch > 1024 || r->L_P < 1 || r->L_R < 1 || r->block < 1 || r->block > 256 ||
-      r->L_R % r->block || r->n_u < 1 || r->n_u > 64 || r->n_u > r->block || r->T_full < 0 || r->full_period < 1 ||
+      r->L_R % r->block || r->n_u < 1 || r->n_u > 64 || r->n_u > r->block || r->block % r->n_u || r->T_full < 0 || r->full_period < 1 ||
       r->layer1_policy < 0 || r->layer1_policy > 1 || r->cmp < 0 || r->cmp > 1 || r->L_P + r->L_R > 32768 ||
       r->select_mode < 0 || r->select_mode > 1) {
-    set_error("run cfg out of range (batch<=1024, block<=256 | L_R, n_u<=min(64,block), N<=32768)");
+    set_error("run cfg out of range (batch<=1024, block<=256 | L_R, n_u<=64 | block, N<=32768)");
     return DYLLM_E_ARG;
   }
   dyllm_cache *c = new dyllm_cache();
@@ -458,6 +461,8 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
   AL(c->lm_rows, lm_cap);
   AL(c->lm_off, r->batch + 1);
   AL(c->dec_prev, static_cast<int64_t>(r->batch) * r->n_u);
+  AL(c->qx_rows, rows);
+  AL(c->qx_off, r->batch + 1);
   AL(c->sim, rows);
   AL(c->rope_cs, static_cast<int64_t>(c->N) * (m.head_dim / 2));
   AL(c->stats, rows * m.n_heads);
@@ -760,11 +765,34 @@ int dyllm_denoise_step(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, i
     KL(OTHER, launch_build_list(1, c->carried_valid ? c->carried : nullptr, c->carried_off,
                                 c->have_dec_prev ? c->dec_prev : nullptr, r.n_u, r.layer1_policy, r.batch, c->N, row_lo,
                                 r.L_P, c->lst[0], c->lst_off[0], st));
+    if (r.layer1_policy == 0 && c->have_dec_prev) {
+      // literal Alg. 1: rows decoded at t-1 stay out of layer-1 idx_in unless carried, but their
+      // embedding changed, so their query does too (Alg. 3 line 4 recomputes Q for every input
+      // row; D6 keeps a Q cache): refresh Q alone for decoded rows outside idx_in
+      const dyllm_model_cfg &m = c->m;
+      const int d = m.d_model, qw = m.n_heads * m.head_dim, kw = m.n_kv_heads * m.head_dim;
+      const LayerW &L0 = w->L[0];
+      KL(OTHER, launch_build_list(2, c->carried_valid ? c->carried : nullptr, c->carried_off, c->dec_prev, r.n_u, 0,
+                                  r.batch, c->N, row_lo, r.L_P, c->qx_rows, c->qx_off, st));
+      const int *M_q = c->qx_off + r.batch;
+      KL(GATHER, launch_gather_rmsnorm(c->H0, c->qx_rows, M_q, c->rows, L0.g_attn, m.rms_eps, c->Xn, d, st));
+      KL(QKV_GEMM, RET(gemm(ctx, M_q, c->rows, qw + 2 * kw, d, c->Xn, L0.wqkv, c->qkv, qw + 2 * kw, EPI_BF16)));
+      KL(QKV_POST, launch_qkv_post(c->qkv, c->qx_rows, M_q, c->rows, L0.bqkv, c->N, m.n_heads, m.n_kv_heads,
+                                   m.head_dim, c->rope_cs, c->L[0].Q, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                   nullptr, nullptr, 0u, st, 1));
+    }
     int cur = 0;
     for (int l = 0; l < c->m.n_layers; ++l) {
+      float *sim_tr = c->tr_sims ? c->tr_sims + static_cast<int64_t>(l) * c->rows : nullptr;
       RET(layer_step_impl(ctx, w, c, l, row_lo, c->lst[cur], c->lst_off[cur], h_tau[l], c->lst[cur ^ 1],
-                          c->lst_off[cur ^ 1], nullptr, d_sal_counts ? d_sal_counts + l * r.batch : nullptr));
+                          c->lst_off[cur ^ 1], sim_tr, d_sal_counts ? d_sal_counts + l * r.batch : nullptr));
       cur ^= 1;
+      if (c->tr_lists) {
+        DY_CUDA(cudaMemcpyAsync(c->tr_lists + static_cast<int64_t>(l) * c->rows, c->lst[cur], sizeof(int) * c->rows,
+                                cudaMemcpyDeviceToDevice, st));
+        DY_CUDA(cudaMemcpyAsync(c->tr_offs + static_cast<int64_t>(l) * (r.batch + 1), c->lst_off[cur],
+                                sizeof(int) * (r.batch + 1), cudaMemcpyDeviceToDevice, st));
+      }
     }
     DY_CUDA(cudaMemcpyAsync(c->carried, c->lst[cur], sizeof(int) * c->rows, cudaMemcpyDeviceToDevice, st));
     DY_CUDA(cudaMemcpyAsync(c->carried_off, c->lst_off[cur], sizeof(int) * (r.batch + 1), cudaMemcpyDeviceToDevice, st));
@@ -880,34 +908,52 @@ int dyllm_debug_trace_buffer(int which, void *d_buf) {
 }
 
 // ------------------------------------------------------------------ ABI: cache access
-int dyllm_cache_tensor(const dyllm_cache *c, int layer, int which, void **d_ptr, int64_t *n_elems) {
-  // K / Q handed out writable: the incremental softmax statistics of that layer can no longer be
-  // trusted until the next dense pass (a denoising step, or dyllm_cache_refresh_stats)
-  if (c && (which == DYLLM_K || which == DYLLM_Q) && layer >= 0 && layer < static_cast<int>(c->L.size()))
-    c->L[layer].st_ok = false;
+// device pointer, element count and element size of one cache tensor (no side effects)
+static int tensor_ptr(const dyllm_cache *c, int layer, int which, void **d_ptr, int64_t *n_elems, int *elem_bytes) {
   CHECK_ARG(c && d_ptr, "null argument");
   const int64_t rows = c->rows, d = c->m.d_model, qw = static_cast<int64_t>(c->m.n_heads) * c->m.head_dim,
                 kw = static_cast<int64_t>(c->m.n_kv_heads) * c->m.head_dim;
+  int eb = 2;
+  int64_t n = 0;
   if (which == DYLLM_H) {
     if (layer < 0 || layer > c->m.n_layers) {
       set_error("layer out of range");
       return DYLLM_E_INDEX;
     }
     *d_ptr = layer == 0 ? c->H0 : c->L[layer - 1].H;
-    if (n_elems) *n_elems = rows * d;
-    return DYLLM_OK;
+    n = rows * d;
+  } else {
+    if (layer < 0 || layer >= c->m.n_layers || which < 0 || which > DYLLM_STATS) {
+      set_error("layer/which out of range");
+      return DYLLM_E_INDEX;
+    }
+    const LayerC &L = c->L[layer];
+    switch (which) {
+      case DYLLM_K: *d_ptr = L.K; n = rows * kw; break;
+      case DYLLM_V: *d_ptr = L.V; n = rows * kw; break;
+      case DYLLM_Q: *d_ptr = L.Q; n = rows * qw; break;
+      case DYLLM_C: *d_ptr = L.C; n = rows * qw; break;
+      default:
+        if (!L.st) {
+          set_error("no softmax statistics for this head_dim");
+          return DYLLM_E_STATE;
+        }
+        *d_ptr = L.st;
+        n = rows * c->m.n_heads;
+        eb = 8;
+        break;
+    }
   }
-  if (layer < 0 || layer >= c->m.n_layers || which < 0 || which > 4) {
-    set_error("layer/which out of range");
-    return DYLLM_E_INDEX;
-  }
-  const LayerC &L = c->L[layer];
-  switch (which) {
-    case DYLLM_K: *d_ptr = L.K; if (n_elems) *n_elems = rows * kw; break;
-    case DYLLM_V: *d_ptr = L.V; if (n_elems) *n_elems = rows * kw; break;
-    case DYLLM_Q: *d_ptr = L.Q; if (n_elems) *n_elems = rows * qw; break;
-    default: *d_ptr = L.C; if (n_elems) *n_elems = rows * qw; break;
-  }
+  if (n_elems) *n_elems = n;
+  if (elem_bytes) *elem_bytes = eb;
+  return DYLLM_OK;
+}
+
+int dyllm_cache_tensor(const dyllm_cache *c, int layer, int which, void **d_ptr, int64_t *n_elems) {
+  RET(tensor_ptr(c, layer, which, d_ptr, n_elems, nullptr));
+  // K / Q / statistics handed out writable: the incremental softmax statistics of that layer can
+  // no longer be trusted until the next dense pass (a denoising step, or dyllm_cache_refresh_stats)
+  if (which == DYLLM_K || which == DYLLM_Q || which == DYLLM_STATS) c->L[layer].st_ok = false;
   return DYLLM_OK;
 }
 
@@ -915,12 +961,41 @@ int dyllm_cache_copy(dyllm_ctx *ctx, dyllm_cache *c, int layer, int which, void 
   CHECK_ARG(ctx && c && ptr, "null argument");
   void *dp = nullptr;
   int64_t n = 0;
-  RET(dyllm_cache_tensor(c, layer, which, &dp, &n));
+  int eb = 2;
+  RET(tensor_ptr(c, layer, which, &dp, &n, &eb));
   const cudaMemcpyKind k = export_ ? (ptr_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost)
                                    : (ptr_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
-  if (export_) DY_CUDA(cudaMemcpyAsync(ptr, dp, n * 2, k, ctx->stream));
-  else DY_CUDA(cudaMemcpyAsync(dp, ptr, n * 2, k, ctx->stream));
-  if (!export_) c->initialized = true;
+  if (export_) {  // read-only: the incremental statistics stay valid
+    DY_CUDA(cudaMemcpyAsync(ptr, dp, n * eb, k, ctx->stream));
+    return DYLLM_OK;
+  }
+  DY_CUDA(cudaMemcpyAsync(dp, ptr, n * eb, k, ctx->stream));
+  c->initialized = true;
+  // imported K / Q invalidate the statistics; imported statistics are the caller's claim that
+  // they belong to the current K and Q
+  if (which == DYLLM_K || which == DYLLM_Q) c->L[layer].st_ok = false;
+  if (which == DYLLM_STATS) c->L[layer].st_ok = true;
+  return DYLLM_OK;
+}
+
+int dyllm_cache_set_decoded(dyllm_ctx *ctx, dyllm_cache *c, const int32_t *d_dec) {
+  CHECK_ARG(ctx && c, "null argument");
+  if (!d_dec) {
+    c->have_dec_prev = false;
+    return DYLLM_OK;
+  }
+  DY_CUDA(cudaMemcpyAsync(c->dec_prev, d_dec, sizeof(int) * c->r.batch * c->r.n_u, cudaMemcpyDeviceToDevice,
+                          ctx->stream));
+  c->have_dec_prev = true;
+  return DYLLM_OK;
+}
+
+int dyllm_cache_set_trace(dyllm_ctx *ctx, dyllm_cache *c, int32_t *d_lists, int32_t *d_offs, float *d_sims) {
+  CHECK_ARG(ctx && c, "null argument");
+  CHECK_ARG((d_lists == nullptr) == (d_offs == nullptr), "d_lists and d_offs go together");
+  c->tr_lists = d_lists;
+  c->tr_offs = d_offs;
+  c->tr_sims = d_sims;
   return DYLLM_OK;
 }
 

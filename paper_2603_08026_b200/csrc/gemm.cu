@@ -342,10 +342,10 @@ template <int BN, int EPI>
 static int launch_t(const GemmCall &g, int num_sms, cudaStream_t st) {
   using C = GemmCfg<BN>;
   auto kern = gemm_tcgen05_kernel<BN, EPI>;
-  static bool attr_done = false;
-  if (!attr_done) {
+  static DeviceOnce attr_done;
+  if (attr_done.todo()) {
     DY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
-    attr_done = true;
+    attr_done.done();
   }
   CUtensorMap ta, tb;
   int rc = make_tmap(&ta, g.A, g.M_cap, g.K, BM);

@@ -611,8 +611,8 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
 template <int EPI>
 static int launch_skinny_t(const GemmCall &g, int num_sms, cudaStream_t st) {
   auto kern = gemm_skinny_kernel<EPI>;
-  static bool attr_done = false;
-  static int max_pairs = 0;
+  static DeviceOnce attr_done;
+  static int max_pairs_dev[DeviceOnce::kMaxDev] = {};
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -624,7 +624,9 @@ static int launch_skinny_t(const GemmCall &g, int num_sms, cudaStream_t st) {
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (!attr_done) {
+  const int dev = DeviceOnce::device();
+  int &max_pairs = max_pairs_dev[dev];
+  if (attr_done.todo()) {
     DY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SK_SMEM));
     DY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
     // split-K contributors spin on each other: every pair of the grid must be co-resident
@@ -636,7 +638,7 @@ static int launch_skinny_t(const GemmCall &g, int num_sms, cudaStream_t st) {
       set_error("skinny gemm: no co-resident 2-CTA cluster");
       return DYLLM_E_CUDA;
     }
-    attr_done = true;
+    attr_done.done();
   }
   // split-K counters are used only when tiles < pairs (2 per tile): at most 2 * max_pairs
   if (!g.ws || !g.ctr || 2 * max_pairs > kSkinnyCtrCap) {

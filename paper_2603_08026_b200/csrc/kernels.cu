@@ -144,18 +144,19 @@ __global__ void qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restr
                                 int H, int KVH, int hd, const float2 *__restrict__ rope_cs, bf16 *__restrict__ Qc,
                                 bf16 *__restrict__ Kc, bf16 *__restrict__ Vc, bf16 *__restrict__ dV,
                                 bf16 *__restrict__ Qx, bf16 *__restrict__ Kx, bf16 *__restrict__ Kxo,
-                                uint32_t *__restrict__ rowflag, uint32_t tag) {
+                                uint32_t *__restrict__ rowflag, uint32_t tag, int q_only) {
   pdl_wait();
   const int M = M_ptr ? *M_ptr : M_cap;
   const int qw = H * hd, kw = KVH * hd, W = qw + 2 * kw;
   const int half = hd / 2, hv = half / 8;  // 8 rotation pairs per thread (16-byte vectors)
-  const int nqk = (H + KVH) * hv, nvv = kw / 8;
+  // q_only: refresh the Q cache rows alone (K / V / dV / row flag untouched)
+  const int nqk = (q_only ? H : H + KVH) * hv, nvv = q_only ? 0 : kw / 8;
   const int rounds = (max(nqk, nvv) + blockDim.x - 1) / blockDim.x;  // 1 with the host's block size
   for (int i = blockIdx.x; i < M; i += gridDim.x) {
     const int r = idx ? idx[i] : i;
     const int pos = r % N;
     const bf16 *src = qkv + static_cast<int64_t>(i) * W;
-    if (rowflag && threadIdx.x == 0) rowflag[r] = tag;  // exact row of this layer step (fused attention)
+    if (rowflag && !q_only && threadIdx.x == 0) rowflag[r] = tag;  // exact row of this layer step (fused attention)
     const float2 *cs = rope_cs + static_cast<int64_t>(pos) * half;
     for (int rd = 0; rd < rounds; ++rd) {
       const int v = rd * blockDim.x + threadIdx.x;
@@ -311,6 +312,8 @@ __global__ void approx_rows_kernel(const int *__restrict__ idx_in, const int *__
 // Single-CTA list builder used once per step: for each sequence, rows in [row_lo, N) that are
 //   mode 0: all rows (identity list)
 //   mode 1: in `carried` (its list), or (policy 1) in the decoded set dec_pos[b][n_u]  (D5)
+//   mode 2: in the decoded set but NOT in `carried` (the rows whose embedding changed but which the
+//           literal layer-1 policy leaves out of idx_in: they get a Q-only refresh, D6)
 // Writes a packed row-id list + offsets [b+1].
 __global__ void build_list_kernel(int mode, const int *__restrict__ carried, const int *__restrict__ carried_off,
                                   const int *__restrict__ dec_pos, int n_u, int policy, int batch, int N,
@@ -336,6 +339,19 @@ __global__ void build_list_kernel(int mode, const int *__restrict__ carried, con
           const int r = dec_pos[s * n_u + j];
           if (r >= 0) flag[r - s * N] = 1;
         }
+      }
+    } else if (mode == 2) {
+      if (dec_pos)
+        for (int j = threadIdx.x; j < n_u; j += blockDim.x) {
+          const int r = dec_pos[s * n_u + j];
+          if (r >= 0) flag[r - s * N] = 1;
+        }
+      __syncthreads();
+      if (carried) {
+        for (int j = carried_off[s] + threadIdx.x; j < carried_off[s + 1]; j += blockDim.x)
+          flag[carried[j] - s * N] = 0;
+      } else {
+        for (int p = resp_lo + threadIdx.x; p < N; p += blockDim.x) flag[p] = 0;
       }
     }
     __syncthreads();
@@ -478,7 +494,7 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
   if (frac >= 0.f) {
     // fraction-controlled mode (D19): per sequence, tau* = the similarity of rank k = round(f*L)
     // (0-based) found by an 8-bit radix select over the order-preserving uint32 keys of s, then
-    // the masks are rebuilt as s < tau* (k rows when there are no ties).
+    // the masks are rebuilt as s < tau* (k rows when there are no ties), s <= tau* under cmp = 1.
     __shared__ unsigned hist[kSelWarps][256];
     for (int sq = warp; sq < batch; sq += kSelWarps) {
       const float *sv = sim_out + static_cast<int64_t>(sq) * N + row_lo;
@@ -568,7 +584,7 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
 #pragma unroll
         for (int w = 0; w < kRegRows; ++w) {
           if (w < nchunks) {
-            const bool fl = w * 32 + lane < L && sreg[w] < thr;
+            const bool fl = w * 32 + lane < L && (cmp ? sreg[w] <= thr : sreg[w] < thr);
             const unsigned m = __ballot_sync(0xffffffffu, fl);
             if (lane == 0) masks[sq * nchunks + w] = m;
           }
@@ -576,7 +592,8 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
       } else {
         for (int w = 0; w < nchunks; ++w) {
           const int i = w * kSelRowsPerCta + lane;
-          const bool fl = i < L && __ldcg(sv + i) < thr;
+          const float sv_i = i < L ? __ldcg(sv + i) : INFINITY;
+          const bool fl = i < L && (cmp ? sv_i <= thr : sv_i < thr);
           const unsigned m = __ballot_sync(0xffffffffu, fl);
           if (lane == 0) masks[sq * nchunks + w] = m;
         }
@@ -835,12 +852,12 @@ void launch_rmsnorm_rows(const bf16 *src, const int *M_ptr, int M_cap, const bf1
 }
 void launch_qkv_post(const bf16 *qkv, const int *idx, const int *M_ptr, int M_cap, const bf16 *bias, int N, int H,
                      int KVH, int hd, const float2 *rope_cs, bf16 *Qc, bf16 *Kc, bf16 *Vc, bf16 *dV, bf16 *Qx,
-                     bf16 *Kx, bf16 *Kxo, uint32_t *rowflag, uint32_t tag, cudaStream_t st) {
+                     bf16 *Kx, bf16 *Kxo, uint32_t *rowflag, uint32_t tag, cudaStream_t st, int q_only) {
   const int g = M_cap < 148 * 4 ? M_cap : 148 * 4;  // one row per CTA per pass; capped like grid_for
   const int work = std::max((H + KVH) * (hd / 16), KVH * hd / 8);  // vectors per row of each part
   const int threads = std::min(1024, std::max(32, (work + 31) / 32 * 32));
   DY_CUDA_LAUNCH(launch_k(qkv_post_kernel, dim3(g > 0 ? g : 1), dim3(threads), 0, st, 1, qkv, idx, M_ptr, M_cap, bias, N, H, KVH, hd, rope_cs, Qc, Kc, Vc,
-                                                 dV, Qx, Kx, Kxo, rowflag, tag));
+                                                 dV, Qx, Kx, Kxo, rowflag, tag, q_only));
 }
 void launch_rope_table(float2 *cs, int N, int hd, double theta, cudaStream_t st) {
   DY_CUDA_LAUNCH(launch_k(rope_table_kernel, dim3(148), dim3(256), 0, st, 1, cs, N, hd, theta));

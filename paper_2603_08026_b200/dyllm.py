@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libdyllm.so")
 
 OK, DONE = 0, 1
 INPUT_FULL, INPUT_RESPONSE = 0, 1
-K, V, Q, CTX, H = 0, 1, 2, 3, 4
+K, V, Q, CTX, H, STATS = 0, 1, 2, 3, 4, 5
 _CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
 
 
@@ -76,6 +76,8 @@ def _load():
         "dyllm_cache_copy": (I, [P, P, I, I, P, I, I]),
         "dyllm_cache_set_carried": (I, [P, P, P, P]),
         "dyllm_cache_refresh_stats": (I, [P, P, I]),
+        "dyllm_cache_set_decoded": (I, [P, P, P]),
+        "dyllm_cache_set_trace": (I, [P, P, P, P, P]),
         "dyllm_select_salient": (I, [P, I, I, I, I, P, P, F, I, P, P, P]),
         "dyllm_gemm_bf16": (I, [P, P, I, I, I, P, P, P, P, P]),
         "dyllm_unmask": (I, [P, P, P, P, P, P]),
@@ -281,14 +283,41 @@ class Cache:
     def set_carried(self, idx=None, off=None):
         _check(_lib.dyllm_cache_set_carried(self.ctx.h, self.h, _ptr(idx), _ptr(off)))
 
+    def set_decoded(self, dec=None):
+        _check(_lib.dyllm_cache_set_decoded(self.ctx.h, self.h, _ptr(dec)))
+
+    def set_trace(self, lists=None, offs=None, sims=None):
+        _check(_lib.dyllm_cache_set_trace(self.ctx.h, self.h, _ptr(lists), _ptr(offs), _ptr(sims)))
+
     def tensor(self, layer, which) -> torch.Tensor:
-        """Zero-copy bf16 torch view of one cache tensor (H: layer 0 = embeddings)."""
+        """Zero-copy torch view of one cache tensor (bf16; H: layer 0 = embeddings; STATS: float32
+        [b][N][H][2]). A writable view: K / Q / STATS views invalidate the incremental statistics."""
         p = C.c_void_p()
         n = C.c_int64()
         _check(_lib.dyllm_cache_tensor(self.h, layer, which, C.byref(p), C.byref(n)))
         width = n.value // (self.run.batch * self.N)
+        dev = f"cuda:{self.ctx.device}"
+        if which == STATS:
+            arr = _CudaArray(p.value, (self.run.batch, self.N, width, 2), "<f4")
+            return torch.as_tensor(arr, device=dev)
         arr = _CudaArray(p.value, (self.run.batch, self.N, width), "<i2")
-        return torch.as_tensor(arr, device=f"cuda:{self.ctx.device}").view(torch.bfloat16)
+        return torch.as_tensor(arr, device=dev).view(torch.bfloat16)
+
+    def export(self, layer, which) -> torch.Tensor:
+        """Read-only copy of one cache tensor (does not invalidate the statistics)."""
+        b, N = self.run.batch, self.N
+        dev = f"cuda:{self.ctx.device}"
+        if which == STATS:
+            out = torch.empty((b, N, self.cfg.n_heads, 2), dtype=torch.float32, device=dev)
+        else:
+            w = {K: self.cfg.kv_width, V: self.cfg.kv_width, Q: self.cfg.q_width, CTX: self.cfg.q_width,
+                 H: self.cfg.d_model}[which]
+            out = torch.empty((b, N, w), dtype=torch.bfloat16, device=dev)
+        _check(_lib.dyllm_cache_copy(self.ctx.h, self.h, layer, which, _ptr(out), 1, 1))
+        return out
+
+    def import_(self, layer, which, src: torch.Tensor):
+        _check(_lib.dyllm_cache_copy(self.ctx.h, self.h, layer, which, _ptr(src.contiguous()), 1, 0))
 
 
 class Engine:

@@ -24,6 +24,7 @@ class ModelCfg:
     residual_mode: int = 0      # 0 = pre-norm residual block (LLaDA/Dream), 1 = paper_literal Alg.2/3
     w_std: float = 0.02         # std of every projection / embedding / lm-head weight
     qk_std: float = 0.0         # std of W_q / W_k (0 -> w_std); the sigma_qk sharpness knob
+    lm_std: float = 0.0         # std of the LM head (0 -> w_std); > w_std gives distinct confidences (tests)
     name: str = ""
 
     @property
@@ -71,6 +72,8 @@ SMALL128 = ModelCfg(n_layers=2, d_model=256, n_heads=2, n_kv_heads=2, head_dim=1
                     vocab=512, mask_id=511, rope_theta=5e5, rms_eps=1e-5, name="small128")
 SMALL128_GQA = replace(SMALL128, n_kv_heads=1, qkv_bias=True, rope_theta=1e6, rms_eps=1e-6,
                        name="small128_gqa")
+SMALL64 = ModelCfg(n_layers=2, d_model=256, n_heads=4, n_kv_heads=2, head_dim=64, d_ff=768,
+                   vocab=512, mask_id=511, rope_theta=1e4, rms_eps=1e-6, name="small64")
 SMALL128_RUN = RunCfg(batch=2, L_P=96, L_R=64, block=32, n_u=1, T_full=4, full_period=4)
 
 LLADA8B = ModelCfg(n_layers=32, d_model=4096, n_heads=32, n_kv_heads=32, head_dim=128,
@@ -87,6 +90,7 @@ PRESETS = {
     "tiny": (TINY, TINY_RUN),
     "small128": (SMALL128, SMALL128_RUN),
     "small128_gqa": (SMALL128_GQA, SMALL128_RUN),
+    "small64": (SMALL64, SMALL128_RUN),
     "llada8b": (LLADA8B, LLADA8B_RUN),
     "dream7b": (DREAM7B, DREAM7B_RUN),
 }

@@ -145,7 +145,8 @@ def global_weights(cfg, seed: int, dtype=np.float64) -> dict:
     return {
         "emb": ih4_normal(seed, stream_id(GLOBAL_LAYER, "emb"), (cfg.vocab, d), s, dtype),
         "g_final": np.ones(d, dtype=dtype),
-        "lm_head": ih4_normal(seed, stream_id(GLOBAL_LAYER, "lm_head"), (cfg.vocab, d), s, dtype),
+        "lm_head": ih4_normal(seed, stream_id(GLOBAL_LAYER, "lm_head"), (cfg.vocab, d),
+                              getattr(cfg, "lm_std", 0.0) or s, dtype),
     }
 
 

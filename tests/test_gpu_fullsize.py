@@ -173,3 +173,40 @@ def _check_full_size(big, mode, frac_in, frac=0.10):
     k = int(np.floor(frac * len(input_rows) + 0.5))
     assert all(abs(len(g) - k) <= 1 for g in got_lists)
     cache.close()
+
+
+def test_incremental_statistics_drift_full_size():
+    """Incremental softmax statistics over a whole LLaDA-8B-shape generation
+    prefix (batch 16, N = 956, 4 FullSteps + 64 denoising steps, f = 0.1): after every step, the
+    statistics the attention kept incrementally for each layer are compared with a dense
+    recomputation from the same K and Q caches (dyllm_cache_refresh_stats), then restored so the
+    incremental state keeps accumulating. log2 of Alg. 4's normaliser (m + log2 l, DYLLM_STATS)
+    must agree within 1e-3 on every row whose statistics are current (response rows after every
+    step; all rows after full-input steps)."""
+    from paper_2603_08026_b200 import dyllm as dy
+    cfg, run = configs.preset("llada8b")
+    cfg = replace(cfg, n_layers=2)
+    run = replace(run, select_mode=1)
+    ctx = dy.Context(0)
+    w = dy.Weights.random(ctx, cfg, seed=SEED)
+    eng = dy.Engine(ctx, w, run)
+    prompts = torch.tensor(gen.prompt_tokens(SEED, run.batch, run.L_P, cfg.mask_id), dtype=torch.int32)
+    eng.load_prompts(prompts.cuda())
+    taus = np.full(cfg.n_layers, 0.1, np.float32)
+    worst = 0.0
+    for t in range(run.T_full + 64):
+        eng.cache.denoise_step(t, taus, eng.tokens, eng.dec_pos, eng.dec_tok)
+        if t < run.T_full:
+            continue
+        lo = 0 if t % run.full_period == 0 else run.L_P
+        for l in range(cfg.n_layers):
+            inc = eng.cache.export(l, dy.STATS)
+            eng.cache.refresh_stats(l)
+            dense = eng.cache.export(l, dy.STATS)
+            eng.cache.import_(l, dy.STATS, inc)
+            torch.cuda.synchronize()
+            lse = lambda s: (s[..., 0].double() + torch.log2(s[..., 1].double()))[:, lo:]
+            err = (lse(inc) - lse(dense)).abs().max().item()
+            worst = max(worst, err)
+            assert err < 1e-3, (t, l, err)
+    print(f"max |log2 normaliser| drift over 64 steps: {worst:.3e}")
