@@ -53,7 +53,21 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--profile-steps", type=int, default=1, help="extra untimed generations with per-kernel events")
     ap.add_argument("--lib-opt", default="", help="library options for A/B runs: option=value[,...] (dyllm_set_option)")
+    ap.add_argument("--full-gens", type=int, default=1,
+                    help="timed generations of the library's full-recompute path (FullStep every step)")
     return ap.parse_args()
+
+
+def spawn_ranks(args):
+    """`--gpus N` without a torchrun environment: relaunch this script under torchrun with one
+    rank per GPU (127.0.0.1 rendezvous), so `python bench.py --gpus N` runs N processes."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 # ----------------------------------------------------------------------------- helpers
@@ -293,6 +307,8 @@ def algo_cost(cls, cfg, run, M_in, M_out, L_tot):
         return L_tot * 3 * qw * 2, 6.0 * L_tot * qw
     if cls == "lm_gemm":
         return 2 * d * cfg.vocab + M_in * 2 * d, 2.0 * M_in * d * cfg.vocab
+    if cls == "qkv_post":   # read q,k,v rows + V_cache rows; write Q, K, V cache rows + dV
+        return M_in * 2 * (qw + 2 * kw + kw) + M_in * 2 * (qw + 2 * kw + kw), 0.0
     return None, None
 
 
@@ -301,6 +317,8 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and "RANK" not in os.environ:
+        spawn_ranks(args)
     import torch
     import torch.distributed as dist
     from dataclasses import replace
@@ -313,8 +331,11 @@ def main():
         k, v = kv.split("=")
         dy.set_option(int(k), int(v))
     rank, world, local = pd.env_rank()
+    if args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world} (launch with torchrun --nproc-per-node {args.gpus})")
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        assert dist.get_world_size() == args.gpus
     torch.cuda.set_device(local)
     cfg, run = configs.preset(args.config)
     run_config_name[0] = args.config
@@ -381,6 +402,23 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     ms_e2e = e0.elapsed_time(e1)
+    # ---- the library's full-recompute path, timed the same way (FullStep at every step, same LM
+    #      head and unmasking rule): the comparison path the north_star's speedup refers to
+    ms_full = None
+    if args.full_gens > 0:
+        eng.tokens[:, : run.L_P].copy_(prompts_dev)
+        eng.tokens[:, run.L_P:].fill_(cfg.mask_id)
+        eng.cache.full_step(eng.tokens, eng.dec_pos, eng.dec_tok)      # warm-up step (untimed)
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.full_gens):
+            eng.tokens[:, : run.L_P].copy_(prompts_dev, non_blocking=True)
+            eng.tokens[:, run.L_P:].fill_(cfg.mask_id)
+            eng.run_steps(taus, full_recompute=True)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ms_full = f0.elapsed_time(f1) / args.full_gens
     # ---- per-kernel CUDA events (one extra generation, same workload, untimed)
     ctx.profile(True)
     for _ in range(max(args.profile_steps, 1)):
@@ -394,8 +432,15 @@ def main():
         kc["full_" + n] = ctx.profile_read(16 + i)
     ctx.profile(False)
     sal = eng.sal_counts.cpu().numpy().astype(np.float64)     # [T][n_layers][b] of the profiled generation
+    # every rank's generated tokens, gathered (rank order = global batch order)
+    all_tokens = pd.gather_tokens(eng.tokens, b * world)
+    assert all_tokens.shape == (b * world, N)
+    assert not bool((all_tokens[:, run.L_P:] == cfg.mask_id).any()), "masked tokens left after a generation"
 
-    ms, ms_e2e = pd.max_over_ranks([ms, ms_e2e], device=f"cuda:{local}")
+    vals = [ms, ms_e2e] + ([ms_full] if ms_full is not None else [])
+    vals = pd.max_over_ranks(vals, device=f"cuda:{local}")
+    ms, ms_e2e = vals[0], vals[1]
+    ms_full = vals[2] if ms_full is not None else None
     tokens = world * b * run.L_R * args.steps
     value = tokens / (ms / 1000.0)
     e2e = tokens / (ms_e2e / 1000.0)
@@ -412,9 +457,11 @@ def main():
         prev_last = np.concatenate([[b * run.L_R], m_out[:-1, -1]])
         m_in[:, 0] = np.minimum(L_in, prev_last + b * run.n_u)
         f_layer = (m_out / L_in[:, None]).mean(axis=0)
+        f_step = m_out.sum(axis=1) / (L_in * cfg.n_layers)          # drift of f over the run (fixed-tau mode)
         totals = {k: float(v.sum()) for k, v in kc.items() if len(v)}
         tot_all = sum(totals.values())
         per_class = {}
+        troof = {}     # sum over launches of max(bytes / BW, flops / P) per class
 
         def lm_cost(steps, n):
             """LM-head bytes / flops per launch: b x (masked rows of the active block at step t)."""
@@ -430,7 +477,6 @@ def main():
             base = k[5:] if full else k
             if full:
                 Mi = Mo = float(b * N)
-                Lt = np.full(len(v), float(b * N))
                 by, fl = algo_cost(base, cfg, run, Mi, Mo, b * N)
                 if by is None:
                     continue
@@ -451,6 +497,7 @@ def main():
                 bys, fls = np.broadcast_to(by, (n,)).astype(np.float64), np.broadcast_to(fl, (n,)).astype(np.float64)
                 v = v[:n]
             t_s = v.sum() / 1000.0
+            troof[k] = float(np.maximum(bys / (hbm * 1e9), fls / (tf_sus * 1e12)).sum()) / nsteps
             B, Fl = float(bys.sum()), float(fls.sum())
             bound = "hbm" if B / (hbm * 1e9) >= Fl / (tf_sus * 1e12) else "tensor"
             if bound == "hbm":
@@ -464,8 +511,15 @@ def main():
         roof = dict(per_class[dom])
         roof.update({"kernel": dom, "traffic": measured_traffic(dom, sparse_t, run),
                      "peak_source": src + (" sustained bf16" if roof["unit"] == "TFLOP/s" else " HBM copy")})
-        full_ms = sum(float(v.sum()) for k, v in kc.items() if k.startswith("full_")) / max(run.T_full * nsteps, 1)
-        full_tok_s = world * b * run.L_R / (T * full_ms / 1000.0) if full_ms > 0 else None
+        # ---- the generation against its roofline, and against full recompute
+        gen_s = ms / args.steps / 1000.0
+        troof_gen = sum(troof.values())
+        troof_full_step = sum(v for k, v in troof.items() if k.startswith("full_") and k != "full_lm_gemm") / max(run.T_full, 1)
+        troof_full_gen = T * troof_full_step + troof.get("lm_gemm", 0.0) + troof.get("full_lm_gemm", 0.0)
+        ffn_rows = float(m_out.sum()) + run.T_full * cfg.n_layers * b * N
+        full_rows = float(T * cfg.n_layers * b * N)
+        f_run = ffn_rows / full_rows
+        full_tok_s = world * b * run.L_R / (ms_full / 1000.0) if ms_full else None
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             cpu = cpu_oracle_sample(cfg, run, args.cpu_seconds, args.frac)
@@ -489,10 +543,20 @@ def main():
             "cpu_baseline": cpu,
             "salient_fraction": {"per_layer_mean": [round(float(x), 4) for x in f_layer],
                                  "run_mean": round(float(f_layer.mean()), 4),
+                                 "per_step_min_max": [round(float(f_step.min()), 4), round(float(f_step.max()), 4)],
+                                 "f_run": round(f_run, 4), "inv_f_run": round(1.0 / f_run, 2),
                                  "calibration": [[round(x, 4) for x in fr] for fr in cal_fracs]},
+            "salient_step_roofline": {
+                "model_s_per_generation": round(troof_gen, 4), "measured_s_per_generation": round(gen_s, 4),
+                "frac": round(troof_gen / gen_s, 4),
+                "note": "sum over the profiled generation's launches of max(alg bytes / HBM peak, alg flops / "
+                        "sustained bf16 peak) (SURVEY 8d.6), over the measured device time of one generation"},
             "kernels": per_class,
-            "full_recompute": {"ms_per_full_step": full_ms, "tokens_per_s_extrapolated": full_tok_s,
-                               "speedup": (value / full_tok_s) if full_tok_s else None},
+            "full_recompute": {"tokens_per_s": full_tok_s, "ms_per_generation": ms_full,
+                               "generations_timed": args.full_gens,
+                               "speedup_measured": (value / full_tok_s) if full_tok_s else None,
+                               "speedup_modelled": round(troof_full_gen / troof_gen, 2) if troof_gen else None,
+                               "inv_f_run": round(1.0 / f_run, 2)},
         }
         print(json.dumps(line, default=float), flush=True)
     if world > 1:
