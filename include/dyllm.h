@@ -50,13 +50,17 @@ typedef struct dyllm_cache dyllm_cache;
 
 /* Model shape (LLaDA / Dream style transformer, BASELINE.json configs).
  * Constraints: d_model % 64 == 0, head_dim in {16, 32, 64, 128}, n_heads % n_kv_heads == 0,
- * d_ff % 128 == 0, rope on all head_dim dims (rotate-half, D10). dtype must be 0 (bf16). */
+ * d_ff % 128 == 0, rope on all head_dim dims (rotate-half, D10). dtype 0 (bf16, the product
+ * path) or 1 (fp32-parity mode: fp32 caches / scratch / arithmetic, SIMT kernels, D12; a
+ * correctness mode at the north_star's 1e-4 bar, not a throughput path; no incremental softmax
+ * statistics, so DYLLM_STATS is unavailable). In fp32 mode every tensor the cache accessors hand
+ * out (K, V, Q, C, H) is fp32 instead of bf16; weights stay bf16 in both modes. */
 typedef struct {
   int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ff, vocab, mask_id;
   float rope_theta, rms_eps;
   int32_t qkv_bias;      /* 1: Q/K/V projections carry a bias (Dream / Qwen2.5) */
   int32_t residual_mode; /* 0: pre-norm residual block (D2 primary); 1: paper_literal Alg. 2/3 */
-  int32_t dtype;         /* 0: bf16 storage, fp32 accumulate (D12) */
+  int32_t dtype;         /* 0: bf16 storage, fp32 accumulate; 1: fp32-parity mode (D12) */
 } dyllm_model_cfg;
 
 /* Generation shape and schedule (Alg. 1). */

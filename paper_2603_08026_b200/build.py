@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libdyllm.so")
-SOURCES = ["dyllm.cu", "gemm.cu", "gemm_skinny.cu", "attn.cu", "attn_fused.cu", "kernels.cu"]
+SOURCES = ["dyllm.cu", "gemm.cu", "gemm_skinny.cu", "attn.cu", "attn_fused.cu", "kernels.cu", "fp32.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v"]

@@ -227,7 +227,10 @@ __device__ __forceinline__ void cp_async_8(void *smem, const void *gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// bar.sync is .aligned: every thread of the warp must execute it converged (compute-sanitizer
+// synccheck flagged a warp that had not reconverged after a lane-0 mbarrier arrive)
 __device__ __forceinline__ void fa_named_sync(int id, int n) {
+  __syncwarp();
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 

@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "fp32.h"
 #include "internal.h"
 #include "kernels.h"
 
@@ -133,6 +134,11 @@ struct dyllm_cache {
   float *sim;  // per-row similarity scratch (fraction mode)
   float2 *rope_cs;  // [N][head_dim/2] (cos, sin) table
   float2 *stats;    // [b*N][H] attention row statistics scratch
+  // fp32-parity mode (dtype 1): every cache / scratch row above is fp32 (element size es)
+  int es = 2;
+  float *gu32 = nullptr;      // [rows][2F] interleaved gate/up products
+  float *logits32 = nullptr;  // [b*block][vocab]
+  int *posmap = nullptr;      // [rows] index of a row in idx_in, -1 otherwise
   bool have_dec_prev = false;
   bool initialized = false;
   std::vector<void *> allocs;
@@ -170,7 +176,7 @@ static int validate_model(const dyllm_model_cfg *m) {
   }
   const int hd = m->head_dim;
   if (m->n_layers < 1 || m->d_model < 64 || m->n_heads < 1 || m->n_kv_heads < 1 || m->vocab < 2 ||
-      m->mask_id < 0 || m->mask_id >= m->vocab || m->dtype != 0) {
+      m->mask_id < 0 || m->mask_id >= m->vocab || m->dtype < 0 || m->dtype > 1) {
     set_error("model cfg out of range");
     return DYLLM_E_ARG;
   }
@@ -422,31 +428,48 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
       return rc;                        \
     }                                   \
   } while (0)
+  // activation rows: bf16, or fp32 in the fp32-parity mode (elements of es bytes)
+  const bool f32 = m.dtype == 1;
+  c->es = f32 ? 4 : 2;
+#define ALE(p, n)                                                                          \
+  do {                                                                                     \
+    rc = dalloc(A, reinterpret_cast<void **>(&(p)), static_cast<size_t>(n) * c->es);     \
+    if (rc) {                                                                              \
+      dyllm_cache_destroy(c);                                                              \
+      return rc;                                                                           \
+    }                                                                                      \
+  } while (0)
   c->L.resize(m.n_layers);
   for (auto &L : c->L) {
-    AL(L.K, rows * kw);
-    AL(L.V, rows * kw);
-    AL(L.Q, rows * qw);
-    AL(L.C, rows * qw);
-    AL(L.H, rows * d);
-    if (m.head_dim == 128) AL(L.st, rows * m.n_heads);
+    ALE(L.K, rows * kw);
+    ALE(L.V, rows * kw);
+    ALE(L.Q, rows * qw);
+    ALE(L.C, rows * qw);
+    ALE(L.H, rows * d);
+    if (m.head_dim == 128 && !f32) AL(L.st, rows * m.n_heads);
   }
-  AL(c->H0, rows * d);
-  AL(c->Xn, rows * d);
-  AL(c->qkv, rows * (qw + 2 * kw));
-  AL(c->dV, rows * kw);
-  AL(c->Qx, rows * qw);
-  AL(c->Kx, rows * kw);
-  AL(c->Kxo, rows * kw);
+  ALE(c->H0, rows * d);
+  ALE(c->Xn, rows * d);
+  ALE(c->qkv, rows * (qw + 2 * kw));
+  ALE(c->dV, rows * kw);
+  ALE(c->Qx, rows * qw);
+  ALE(c->Kx, rows * kw);
+  ALE(c->Kxo, rows * kw);
   AL(c->rowflag, rows);
-  AL(c->Cn, rows * qw);
-  AL(c->Cg, rows * qw);
-  AL(c->h, rows * d);
-  AL(c->hn, rows * d);
-  AL(c->act, rows * F);
-  AL(c->ffo, rows * d);
-  AL(c->Xf, lm_cap * d);
+  ALE(c->Cn, rows * qw);
+  ALE(c->Cg, rows * qw);
+  ALE(c->h, rows * d);
+  ALE(c->hn, rows * d);
+  ALE(c->act, rows * F);
+  ALE(c->ffo, rows * d);
+  ALE(c->Xf, lm_cap * d);
   AL(c->partials, lm_cap * gemm_lmhead_ntiles(m.vocab));
+  if (f32) {
+    AL(c->gu32, rows * 2 * F);
+    AL(c->logits32, lm_cap * m.vocab);
+    AL(c->posmap, rows);
+  }
+#undef ALE
   for (int i = 0; i < 2; ++i) {
     AL(c->lst[i], rows);
     AL(c->lst_off[i], r->batch + 1);
@@ -470,11 +493,11 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
   cudaStream_t st = ctx->stream;
   // compact scratch rows past the live count are read (with zero weight) by attention tiles:
   // start them finite
-  const bool ok = cudaMemsetAsync(c->dV, 0, rows * kw * 2, st) == cudaSuccess &&
-                  cudaMemsetAsync(c->Kx, 0, rows * kw * 2, st) == cudaSuccess &&
-                  cudaMemsetAsync(c->Kxo, 0, rows * kw * 2, st) == cudaSuccess &&
+  const bool ok = cudaMemsetAsync(c->dV, 0, rows * kw * c->es, st) == cudaSuccess &&
+                  cudaMemsetAsync(c->Kx, 0, rows * kw * c->es, st) == cudaSuccess &&
+                  cudaMemsetAsync(c->Kxo, 0, rows * kw * c->es, st) == cudaSuccess &&
                   cudaMemsetAsync(c->rowflag, 0, rows * sizeof(uint32_t), st) == cudaSuccess &&
-                  cudaMemsetAsync(c->Qx, 0, rows * qw * 2, st) == cudaSuccess &&
+                  cudaMemsetAsync(c->Qx, 0, rows * qw * c->es, st) == cudaSuccess &&
                   cudaMemsetAsync(c->zero_off, 0, (r->batch + 1) * sizeof(int), st) == cudaSuccess;
   if (!ok) {
     set_error("memset failed");
@@ -543,8 +566,141 @@ static int post_attention(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c
   return DYLLM_OK;
 }
 
+// ------------------------------------------------------------------ fp32-parity mode (dtype 1, D12)
+// The same step structure as the bf16 path below, on fp32 rows with the SIMT kernels of fp32.cu.
+static inline float *fp(void *p) { return static_cast<float *>(p); }
+
+static f32::GemmF32 g32(const int *M_ptr, int M_cap, int N, int K, const float *A, const bf16 *W, float *D, int ldd) {
+  f32::GemmF32 g;
+  g.M_ptr = M_ptr;
+  g.M_cap = M_cap;
+  g.N = N;
+  g.K = K;
+  g.A = A;
+  g.lda = K;
+  g.W = W;
+  g.D = D;
+  g.ldd = ldd;
+  return g;
+}
+
+// O-proj + FFN on the rows listed by (rows, M_ptr) (nullptr: all rows); A_c rows read at a_rows.
+static void post_attention_f32(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int l, const int *M_ptr,
+                               const float *A_c, const int *a_rows, const float *Hprev, const int *rows, float *out) {
+  const dyllm_model_cfg &m = c->m;
+  const int d = m.d_model, qw = m.n_heads * m.head_dim, F = m.d_ff, R = c->rows;
+  const LayerW &L = w->L[l];
+  cudaStream_t st = ctx->stream;
+  const bool res = m.residual_mode == 0;
+  f32::GemmF32 go = g32(M_ptr, R, d, qw, A_c, L.wo, fp(c->h), d);
+  go.a_rows = a_rows;
+  if (res) {  // h = x + C W_o
+    go.resid = Hprev;
+    go.ldr = d;
+    go.resid_rows = rows;
+  }
+  KL(O_GEMM, f32::gemm(go, st));
+  KL(OTHER, f32::gather_rmsnorm(fp(c->h), nullptr, M_ptr, R, L.g_ffn, m.rms_eps, fp(c->hn), d, st));
+  KL(GU_GEMM, f32::gemm(g32(M_ptr, R, 2 * F, d, fp(c->hn), L.wgu, c->gu32, 2 * F), st));
+  KL(OTHER, f32::swiglu(c->gu32, M_ptr, R, F, fp(c->act), st));
+  f32::GemmF32 gd = g32(M_ptr, R, d, F, fp(c->act), L.wd, out, d);
+  gd.out_rows = rows;  // scatter-back
+  if (res) {
+    gd.resid = fp(c->h);
+    gd.ldr = d;
+  }
+  KL(DOWN_GEMM, f32::gemm(gd, st));
+}
+
+static int full_step_f32(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, const int *d_tokens) {
+  const dyllm_model_cfg &m = c->m;
+  const int d = m.d_model, qw = m.n_heads * m.head_dim, kw = m.n_kv_heads * m.head_dim, rows = c->rows;
+  cudaStream_t st = ctx->stream;
+  ctx->cls_offset = DYLLM_KC_FULL;
+  KL(OTHER, f32::embed(d_tokens, nullptr, nullptr, rows, w->emb, fp(c->H0), d, st));
+  for (int l = 0; l < m.n_layers; ++l) {
+    const LayerW &L = w->L[l];
+    LayerC &C = c->L[l];
+    const float *Hprev = fp(l == 0 ? c->H0 : c->L[l - 1].H);
+    KL(GATHER, f32::gather_rmsnorm(Hprev, nullptr, nullptr, rows, L.g_attn, m.rms_eps, fp(c->Xn), d, st));
+    KL(QKV_GEMM, f32::gemm(g32(nullptr, rows, qw + 2 * kw, d, fp(c->Xn), L.wqkv, fp(c->qkv), qw + 2 * kw), st));
+    KL(QKV_POST, f32::qkv_post(fp(c->qkv), nullptr, nullptr, rows, L.bqkv, c->N, m.n_heads, m.n_kv_heads, m.head_dim,
+                               c->rope_cs, fp(C.Q), fp(C.K), fp(C.V), nullptr, 0, st));
+    f32::F32Attn a{};
+    a.batch = c->r.batch;
+    a.N = c->N;
+    a.H = m.n_heads;
+    a.KVH = m.n_kv_heads;
+    a.hd = m.head_dim;
+    a.row_lo = 0;
+    a.scale = 1.f / sqrtf(static_cast<float>(m.head_dim));
+    a.Q = fp(C.Q);
+    a.K = fp(C.K);
+    a.V = fp(C.V);
+    a.C_cache = fp(C.C);
+    a.C_out = fp(C.C);
+    a.all_exact = true;
+    KL(ATTN, f32::attention(a, st));
+    post_attention_f32(ctx, w, c, l, nullptr, fp(C.C), nullptr, Hprev, nullptr, fp(C.H));
+  }
+  ctx->cls_offset = 0;
+  c->carried_valid = false;
+  c->have_dec_prev = false;
+  c->initialized = true;
+  DY_CUDA(cudaGetLastError());
+  return DYLLM_OK;
+}
+
+static int layer_step_f32(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int l, int row_lo,
+                          const int *idx_in, const int *off_in, float tau, int *idx_out, int *off_out, float *sim,
+                          int *counts) {
+  const dyllm_model_cfg &m = c->m;
+  const int b = c->r.batch, N = c->N, rows = c->rows;
+  const int d = m.d_model, qw = m.n_heads * m.head_dim, kw = m.n_kv_heads * m.head_dim;
+  const LayerW &L = w->L[l];
+  LayerC &C = c->L[l];
+  const float *Hprev = fp(l == 0 ? c->H0 : c->L[l - 1].H);
+  cudaStream_t st = ctx->stream;
+  const int *M_in = off_in + b;
+  // a1-a3: RMSNorm(x[idx_in]) -> QKV -> RoPE, dV (before the overwrite), in-place K/V/Q rows
+  KL(GATHER, f32::gather_rmsnorm(Hprev, idx_in, M_in, rows, L.g_attn, m.rms_eps, fp(c->Xn), d, st));
+  KL(QKV_GEMM, f32::gemm(g32(M_in, rows, qw + 2 * kw, d, fp(c->Xn), L.wqkv, fp(c->qkv), qw + 2 * kw), st));
+  KL(QKV_POST, f32::qkv_post(fp(c->qkv), idx_in, M_in, rows, L.bqkv, N, m.n_heads, m.n_kv_heads, m.head_dim,
+                             c->rope_cs, fp(C.Q), fp(C.K), fp(C.V), fp(c->dV), 0, st));
+  // a4: exact rows (idx_in) and Alg. 4 rows, dense over the merged K
+  KL(OTHER, f32::posmap(idx_in, M_in, rows, c->posmap, st));
+  f32::F32Attn a{};
+  a.batch = b;
+  a.N = N;
+  a.H = m.n_heads;
+  a.KVH = m.n_kv_heads;
+  a.hd = m.head_dim;
+  a.row_lo = row_lo;
+  a.scale = 1.f / sqrtf(static_cast<float>(m.head_dim));
+  a.Q = fp(C.Q);
+  a.K = fp(C.K);
+  a.V = fp(C.V);
+  a.dV = fp(c->dV);
+  a.C_cache = fp(C.C);
+  a.C_out = fp(c->Cn);
+  a.sal_rows = idx_in;
+  a.sal_off = off_in;
+  a.posmap = c->posmap;
+  a.all_exact = false;
+  KL(ATTN, f32::attention(a, st));
+  // a5: cosine + threshold + compaction, C_cache <- C_new
+  const bool fmode = c->r.select_mode == 1;
+  KL(SELECT, f32::select(fp(c->Cn), fp(C.C), b, N, row_lo, qw, fmode ? 2.f : tau, c->r.cmp, fmode ? tau : -1.f,
+                         sim ? sim : c->sim, idx_out, off_out, counts, st));
+  // a6-a8 on idx_out, scattered into H_l
+  post_attention_f32(ctx, w, c, l, off_out + b, fp(C.C), idx_out, Hprev, idx_out, fp(C.H));
+  DY_CUDA(cudaGetLastError());
+  return DYLLM_OK;
+}
+
 // FullStep (Alg. 2): every row of every sequence, all caches rewritten.
 static int full_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, const int *d_tokens) {
+  if (c->m.dtype == 1) return full_step_f32(ctx, w, c, d_tokens);
   const dyllm_model_cfg &m = c->m;
   const int d = m.d_model, qw = m.n_heads * m.head_dim, kw = m.n_kv_heads * m.head_dim, rows = c->rows;
   cudaStream_t st = ctx->stream;
@@ -612,6 +768,7 @@ static int full_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c
 static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int l, int row_lo,
                            const int *idx_in, const int *off_in, float tau, int *idx_out, int *off_out, float *sim,
                            int *counts) {
+  if (c->m.dtype == 1) return layer_step_f32(ctx, w, c, l, row_lo, idx_in, off_in, tau, idx_out, off_out, sim, counts);
   const dyllm_model_cfg &m = c->m;
   const int b = c->r.batch, N = c->N, rows = c->rows;
   const int d = m.d_model, qw = m.n_heads * m.head_dim, kw = m.n_kv_heads * m.head_dim;
@@ -702,12 +859,22 @@ static int unmask_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, i
   const int lm_cap = r.batch * r.block;
   const bf16 *HL = c->L[m.n_layers - 1].H;
   KL(OTHER, launch_lm_candidates(d_tokens, r.batch, r.L_P, r.L_R, r.block, m.mask_id, c->lm_rows, c->lm_off, st));
+  if (m.dtype == 1) {  // fp32-parity mode: full logits rows, then one (max, sum exp, argmax) partial per row
+    const int *M_lm = c->lm_off + r.batch;
+    KL(GATHER, f32::gather_rmsnorm(fp(c->L[m.n_layers - 1].H), c->lm_rows, M_lm, lm_cap, w->g_final, m.rms_eps,
+                                   fp(c->Xf), m.d_model, st));
+    KL(LM_GEMM, f32::gemm(g32(M_lm, lm_cap, m.vocab, m.d_model, fp(c->Xf), w->lm_head, c->logits32, m.vocab), st));
+    KL(OTHER, f32::lm_reduce(c->logits32, M_lm, lm_cap, m.vocab, c->partials, st));
+    KL(OTHER, launch_lm_select_commit(c->partials, 1, c->lm_rows, c->lm_off, r.batch, r.n_u, d_tokens, c->dec_prev,
+                                      d_dec_tok, w->emb, nullptr, m.d_model, st, fp(c->H0)));
+  } else {
   KL(GATHER, launch_gather_rmsnorm(HL, c->lm_rows, c->lm_off + r.batch, lm_cap, w->g_final, m.rms_eps, c->Xf,
                                    m.d_model, st));
   KL(LM_GEMM, RET(gemm(ctx, c->lm_off + r.batch, lm_cap, m.vocab, m.d_model, c->Xf, w->lm_head, nullptr, 0, EPI_LMHEAD,
                        nullptr, 0, nullptr, nullptr, c->partials)));
   KL(OTHER, launch_lm_select_commit(c->partials, gemm_lmhead_ntiles(m.vocab), c->lm_rows, c->lm_off, r.batch, r.n_u,
                                     d_tokens, c->dec_prev, d_dec_tok, w->emb, c->H0, m.d_model, st));
+  }
   if (d_dec_pos)
     DY_CUDA(cudaMemcpyAsync(d_dec_pos, c->dec_prev, sizeof(int) * r.batch * r.n_u, cudaMemcpyDeviceToDevice, st));
   c->have_dec_prev = true;
@@ -775,11 +942,18 @@ int dyllm_denoise_step(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, i
       KL(OTHER, launch_build_list(2, c->carried_valid ? c->carried : nullptr, c->carried_off, c->dec_prev, r.n_u, 0,
                                   r.batch, c->N, row_lo, r.L_P, c->qx_rows, c->qx_off, st));
       const int *M_q = c->qx_off + r.batch;
+      if (m.dtype == 1) {
+        KL(GATHER, f32::gather_rmsnorm(fp(c->H0), c->qx_rows, M_q, c->rows, L0.g_attn, m.rms_eps, fp(c->Xn), d, st));
+        KL(QKV_GEMM, f32::gemm(g32(M_q, c->rows, qw + 2 * kw, d, fp(c->Xn), L0.wqkv, fp(c->qkv), qw + 2 * kw), st));
+        KL(QKV_POST, f32::qkv_post(fp(c->qkv), c->qx_rows, M_q, c->rows, L0.bqkv, c->N, m.n_heads, m.n_kv_heads,
+                                   m.head_dim, c->rope_cs, fp(c->L[0].Q), nullptr, nullptr, nullptr, 1, st));
+      } else {
       KL(GATHER, launch_gather_rmsnorm(c->H0, c->qx_rows, M_q, c->rows, L0.g_attn, m.rms_eps, c->Xn, d, st));
       KL(QKV_GEMM, RET(gemm(ctx, M_q, c->rows, qw + 2 * kw, d, c->Xn, L0.wqkv, c->qkv, qw + 2 * kw, EPI_BF16)));
       KL(QKV_POST, launch_qkv_post(c->qkv, c->qx_rows, M_q, c->rows, L0.bqkv, c->N, m.n_heads, m.n_kv_heads,
                                    m.head_dim, c->rope_cs, c->L[0].Q, nullptr, nullptr, nullptr, nullptr, nullptr,
                                    nullptr, nullptr, 0u, st, 1));
+      }
     }
     int cur = 0;
     for (int l = 0; l < c->m.n_layers; ++l) {
@@ -913,7 +1087,7 @@ static int tensor_ptr(const dyllm_cache *c, int layer, int which, void **d_ptr, 
   CHECK_ARG(c && d_ptr, "null argument");
   const int64_t rows = c->rows, d = c->m.d_model, qw = static_cast<int64_t>(c->m.n_heads) * c->m.head_dim,
                 kw = static_cast<int64_t>(c->m.n_kv_heads) * c->m.head_dim;
-  int eb = 2;
+  int eb = c->es;
   int64_t n = 0;
   if (which == DYLLM_H) {
     if (layer < 0 || layer > c->m.n_layers) {

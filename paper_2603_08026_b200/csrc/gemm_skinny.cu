@@ -101,6 +101,7 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t *bar) {
       : "memory");
 }
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
+  __syncwarp();  // bar.sync is .aligned: the warp must be converged
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 

@@ -704,7 +704,7 @@ __global__ void lm_select_commit_kernel(const float4 *__restrict__ partials, int
                                         const int *__restrict__ rows, const int *__restrict__ off, int n_u,
                                         int *__restrict__ tokens, int *__restrict__ dec_pos,
                                         int *__restrict__ dec_tok, const bf16 *__restrict__ emb,
-                                        bf16 *__restrict__ H0, int d) {
+                                        bf16 *__restrict__ H0, int d, float *__restrict__ H0f) {
   pdl_wait();
   __shared__ float conf[256];
   __shared__ int tok[256];
@@ -775,6 +775,10 @@ __global__ void lm_select_commit_kernel(const float4 *__restrict__ partials, int
   for (int j = warp; j < take; j += nw) {
     const int r = dec_pos[s * n_u + j];
     const int t = dec_tok[s * n_u + j];
+    if (H0f) {  // fp32-parity mode (dtype 1)
+      for (int c = lane; c < d; c += 32) H0f[static_cast<int64_t>(r) * d + c] = bf2f(emb[static_cast<int64_t>(t) * d + c]);
+      continue;
+    }
     const uint4 *src = reinterpret_cast<const uint4 *>(emb + static_cast<int64_t>(t) * d);
     uint4 *dst = reinterpret_cast<uint4 *>(H0 + static_cast<int64_t>(r) * d);
     for (int c = lane; c < d / 8; c += 32) dst[c] = src[c];
@@ -885,9 +889,9 @@ void launch_lm_candidates(const int *tokens, int batch, int L_P, int L_R, int bl
 }
 void launch_lm_select_commit(const float4 *partials, int n_tiles, const int *rows, const int *off, int batch, int n_u,
                              int *tokens, int *dec_pos, int *dec_tok, const bf16 *emb, bf16 *H0, int d,
-                             cudaStream_t st) {
+                             cudaStream_t st, float *H0f) {
   DY_CUDA_LAUNCH(launch_k(lm_select_commit_kernel, dim3(batch), dim3(256), 0, st, 1, partials, n_tiles, rows, off, n_u, tokens, dec_pos, dec_tok, emb, H0,
-                                                 d));
+                                                 d, H0f));
 }
 void launch_ih4_fill(bf16 *dst, int64_t rows, int cols, uint64_t keyA, uint64_t keyB, int il, float scale,
                      cudaStream_t st) {

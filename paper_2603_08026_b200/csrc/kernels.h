@@ -33,7 +33,7 @@ void launch_lm_candidates(const int *tokens, int batch, int L_P, int L_R, int bl
                           cudaStream_t st);
 void launch_lm_select_commit(const float4 *partials, int n_tiles, const int *rows, const int *off, int batch, int n_u,
                              int *tokens, int *dec_pos, int *dec_tok, const bf16 *emb, bf16 *H0, int d,
-                             cudaStream_t st);
+                             cudaStream_t st, float *H0f = nullptr);
 void launch_ih4_fill(bf16 *dst, int64_t rows, int cols, uint64_t keyA, uint64_t keyB, int il, float scale,
                      cudaStream_t st);
 void launch_fill_const(bf16 *dst, int64_t n, float v, cudaStream_t st);

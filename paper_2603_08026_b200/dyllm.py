@@ -35,7 +35,8 @@ class ModelCfg(C.Structure):
     @classmethod
     def from_py(cls, m):
         return cls(m.n_layers, m.d_model, m.n_heads, m.n_kv_heads, m.head_dim, m.d_ff, m.vocab,
-                   m.mask_id, m.rope_theta, m.rms_eps, int(m.qkv_bias), m.residual_mode, 0)
+                   m.mask_id, m.rope_theta, m.rms_eps, int(m.qkv_bias), m.residual_mode,
+                   int(getattr(m, "dtype", 0)))
 
 
 class RunCfg(C.Structure):
@@ -290,7 +291,8 @@ class Cache:
         _check(_lib.dyllm_cache_set_trace(self.ctx.h, self.h, _ptr(lists), _ptr(offs), _ptr(sims)))
 
     def tensor(self, layer, which) -> torch.Tensor:
-        """Zero-copy torch view of one cache tensor (bf16; H: layer 0 = embeddings; STATS: float32
+        """Zero-copy torch view of one cache tensor (bf16, fp32 in the fp32-parity mode; H: layer 0 =
+        embeddings; STATS: float32
         [b][N][H][2]). A writable view: K / Q / STATS views invalidate the incremental statistics."""
         p = C.c_void_p()
         n = C.c_int64()
@@ -300,6 +302,8 @@ class Cache:
         if which == STATS:
             arr = _CudaArray(p.value, (self.run.batch, self.N, width, 2), "<f4")
             return torch.as_tensor(arr, device=dev)
+        if getattr(self.cfg, "dtype", 0) == 1:      # fp32-parity mode
+            return torch.as_tensor(_CudaArray(p.value, (self.run.batch, self.N, width), "<f4"), device=dev)
         arr = _CudaArray(p.value, (self.run.batch, self.N, width), "<i2")
         return torch.as_tensor(arr, device=dev).view(torch.bfloat16)
 
@@ -312,7 +316,8 @@ class Cache:
         else:
             w = {K: self.cfg.kv_width, V: self.cfg.kv_width, Q: self.cfg.q_width, CTX: self.cfg.q_width,
                  H: self.cfg.d_model}[which]
-            out = torch.empty((b, N, w), dtype=torch.bfloat16, device=dev)
+            dt = torch.float32 if getattr(self.cfg, "dtype", 0) == 1 else torch.bfloat16
+            out = torch.empty((b, N, w), dtype=dt, device=dev)
         _check(_lib.dyllm_cache_copy(self.ctx.h, self.h, layer, which, _ptr(out), 1, 1))
         return out
 

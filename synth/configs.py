@@ -25,6 +25,7 @@ class ModelCfg:
     w_std: float = 0.02         # std of every projection / embedding / lm-head weight
     qk_std: float = 0.0         # std of W_q / W_k (0 -> w_std); the sigma_qk sharpness knob
     lm_std: float = 0.0         # std of the LM head (0 -> w_std); > w_std gives distinct confidences (tests)
+    dtype: int = 0              # 0 = bf16 storage (the product path); 1 = fp32-parity mode (DESIGN D12)
     name: str = ""
 
     @property

@@ -22,6 +22,20 @@ def to_dev_bf16(a: np.ndarray) -> torch.Tensor:
     return torch.tensor(np.asarray(a, dtype=np.float32)).to(torch.bfloat16).cuda()
 
 
+def f32_round(a: np.ndarray) -> np.ndarray:
+    return np.asarray(a, dtype=np.float64).astype(np.float32).astype(np.float64)
+
+
+def storage_round(dtype: int):
+    """The rounding of a value stored in the GPU caches: bf16 (product path) or fp32 (dtype 1)."""
+    return f32_round if dtype == 1 else bf16_round
+
+
+def to_dev(a: np.ndarray, dtype: int = 0) -> torch.Tensor:
+    t = torch.tensor(np.asarray(a, dtype=np.float32))
+    return (t if dtype == 1 else t.to(torch.bfloat16)).cuda()
+
+
 def from_dev(t: torch.Tensor) -> np.ndarray:
     return t.detach().float().cpu().numpy().astype(np.float64)
 
@@ -62,14 +76,15 @@ def oracle_states(m: Model, prompts, steps: int, tau=0.999):
     return states
 
 
-def round_states(states):
+def round_states(states, dtype: int = 0):
+    rnd = storage_round(dtype)
     out = []
     for st in states:
         s2 = copy.deepcopy(st)
         for lc in s2.caches:
-            lc.K, lc.V, lc.Q, lc.C, lc.H = (bf16_round(x) for x in (lc.K, lc.V, lc.Q, lc.C, lc.H))
+            lc.K, lc.V, lc.Q, lc.C, lc.H = (rnd(x) for x in (lc.K, lc.V, lc.Q, lc.C, lc.H))
         if s2.H0 is not None:
-            s2.H0 = bf16_round(s2.H0)
+            s2.H0 = rnd(s2.H0)
         out.append(s2)
     return out
 
@@ -81,8 +96,8 @@ def import_states(m: Model, cache, states):
     for l in range(m.cfg.n_layers):
         for which, f in fields:
             t = cache.tensor(l + 1 if which == dy.H else l, which)
-            t.copy_(to_dev_bf16(np.stack([getattr(st.caches[l], f) for st in states])))
-    cache.tensor(0, dy.H).copy_(to_dev_bf16(np.stack([st.H0 for st in states])))
+            t.copy_(to_dev(np.stack([getattr(st.caches[l], f) for st in states]), m.cfg.dtype))
+    cache.tensor(0, dy.H).copy_(to_dev(np.stack([st.H0 for st in states]), m.cfg.dtype))
     torch.cuda.synchronize()
     # mark initialised through the ABI import path
     buf = torch.empty_like(cache.tensor(0, dy.H))
