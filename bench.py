@@ -180,6 +180,18 @@ def cpu_oracle_sample(cfg, run, seconds: float, frac: float, seed: int = 0):
 
     timings["ro"] = sparse("ro")
     timings["fi"] = sparse("fi")
+    # BLAS threading: the vendor and thread count the oracle ran with, and the same
+    # response-only layer pinned to one core
+    blas = []
+    one_core = None
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+        blas = [f"{i.get('internal_api')} x{i.get('num_threads')}" for i in threadpool_info()
+                if i.get("user_api") == "blas"]
+        with threadpool_limits(limits=1, user_api="blas"):
+            one_core = sparse("ro")
+    except Exception:
+        pass
     t = time.time()
     if timings["ro"] + timings["fi"] < seconds:
         O.full_layer(x_all, W, cfg)
@@ -196,6 +208,14 @@ def cpu_oracle_sample(cfg, run, seconds: float, frac: float, seed: int = 0):
         cores = len(os.sched_getaffinity(0))
     except Exception:
         cores = os.cpu_count()
+    # measured outright at the tiny config (C1): one whole Alg. 1 generation of the oracle
+    from synth import configs as _cf
+    tcfg, trun = _cf.preset("tiny")
+    tW = gen.model_weights(tcfg, seed)
+    tprompts = gen.prompt_tokens(seed, trun.batch, trun.L_P, tcfg.mask_id)
+    t = time.time()
+    O.generate(tprompts, tW, tcfg, trun, 0.99)
+    tiny_tok_s = trun.batch * trun.L_R / (time.time() - t)
     return {
         "value": tok_s, "unit": UNIT, "cores": cores, "kind": "oracle",
         "sample": (f"oracle fp64 NumPy on one sequence: one RO sparse layer ({timings['ro']:.2f}s), one FI "
@@ -203,6 +223,10 @@ def cpu_oracle_sample(cfg, run, seconds: float, frac: float, seed: int = 0):
                    f"salient fraction {frac}; extrapolated x{cfg.n_layers} layers x ({n_full} full, {n_fi} FI, "
                    f"{n_ro} RO) steps, LM head excluded; setup {setup:.1f}s untimed"),
         "extrapolated": True,
+        "blas": blas,
+        "ro_layer_s_1core": one_core,
+        "ro_layer_s_all_cores": timings["ro"],
+        "tiny_e2e_tokens_per_s_measured": tiny_tok_s,
     }
 
 

@@ -253,8 +253,12 @@ uint64_t dyllm_launch_count(void);
  * keys on the 128 MMA rows, O^T = V^T P^T), so the tensor and exp work follows the row count
  * instead of a 128-row tile; 0 disables. The default build compiles those tiles out (measured
  * faster overall) and accepts the option without effect. */
+/* DYLLM_OPT_ATTN_PINC (default 1): in full-input steps, prompt tiles update their rows' softmax
+ * statistics by the keys changed since the previous full-input step (the list U: idx_in, then the
+ * keys written by the response-only steps since), instead of recomputing them over all N keys
+ * (SURVEY §8f1, D20). 0 = dense prompt tiles. */
 enum { DYLLM_OPT_SKINNY_GEMM = 1, DYLLM_OPT_SKINNY_SPLIT = 2, DYLLM_OPT_ATTN_FUSED = 3, DYLLM_OPT_SKINNY_ONE_CHUNK = 4,
-       DYLLM_OPT_PDL = 5, DYLLM_OPT_ATTN_INC = 6, DYLLM_OPT_ATTN_T4 = 7 };
+       DYLLM_OPT_PDL = 5, DYLLM_OPT_ATTN_INC = 6, DYLLM_OPT_ATTN_T4 = 7, DYLLM_OPT_ATTN_PINC = 8 };
 int dyllm_set_option(int option, int value);
 
 /* Debug hook: when d_buf != NULL, kernels of family `which` (0 = skinny GEMM) write %globaltimer

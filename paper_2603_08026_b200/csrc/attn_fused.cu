@@ -90,19 +90,30 @@ struct FaParams {
   int *fix;                   // [0] count, [1 ..] ids of incremental tiles whose update cancelled
   int fix_cap;
   int t4max;                  // exact-row items of <= t4max rows run transposed (type 4; 0: never)
+  // full-input steps with incremental prompt statistics (SURVEY §8f1 for the prompt rows): row
+  // tiles are split at resp_lo (MTp prompt tiles, then the response tiles), and a prompt tile
+  // updates its rows' statistics by the keys changed since they were last current (the list U of
+  // each sequence: its idx_in rows first, then the keys written by the response-only steps since,
+  // compact new keys Kun / snapshot keys Kuo at rows [s*N, s*N + ucnt[s]))
+  int MTp;
+  int pinc;                   // prompt statistics current up to U: incremental prompt tiles allowed
+  const int *ucnt;            // [b] |U| per sequence
 };
 
 struct FaItem {
   int s, h, kvh, nrows, q_row, off, nkP, xc;
+  int nkS;      // type 3: key count of its new / old key tiles (<= 2 tiles; first row s*N for U, else off)
   bool type2, passP;
-  bool inc;     // type 3: incremental statistics (response tile, <= 128 salient keys, current stats)
+  bool inc;     // type 3: incremental statistics (<= 128 salient keys, statistics current up to the
+                // changed keys: idx_in for response tiles, U for prompt tiles of full-input steps)
+  bool uk;      // type 3 over the U lists (prompt tile) instead of idx_in (Kx / Kxo)
   bool single;  // type 2 in one pass (online softmax); the fixup launch re-runs type 2 in two passes
   bool t4;      // type 2, single pass, <= 32 rows: computed transposed (keys on the MMA rows)
 };
 
 // Item decode from its index and the exact-row range (off, e) of its sequence (the producer reads
 // those once and passes them through the work queue, so no role stalls on global loads).
-__device__ __forceinline__ FaItem fa_item(const FaParams &p, int w, int off, int e) {
+__device__ __forceinline__ FaItem fa_item(const FaParams &p, int w, int off, int e, int nU) {
   FaItem it;
   const int per = p.MT + p.XT;
   const int t = w % per;
@@ -113,19 +124,34 @@ __device__ __forceinline__ FaItem fa_item(const FaParams &p, int w, int off, int
   it.s = sh / p.KVH;
   it.h = it.kvh * p.grp + g;
   it.off = off;
+  it.uk = false;
+  it.nkS = e;
   if (t < p.MT) {
     it.type2 = false;
     it.xc = 0;
-    it.q_row = it.s * p.N + p.row_lo + t * 128;
-    it.nrows = min(128, p.L - t * 128);
+    const bool prompt = t < p.MTp;
+    const int r0 = prompt ? p.row_lo + t * 128 : (p.MTp ? p.resp_lo : p.row_lo) + (t - p.MTp) * 128;
+    it.q_row = it.s * p.N + r0;
+    it.nrows = min(128, (prompt ? p.resp_lo : p.N) - r0);
     it.passP = e > 0 && p.mode != 2;
     it.nkP = e;
-    it.inc = p.inc && p.mode == 0 && e > 0 && e <= FA_BK && p.row_lo + t * 128 >= p.resp_lo;
     it.single = false;
     it.t4 = false;
-    // no salient key in the sequence: the keys did not change, so neither did the statistics
-    // (when current) nor the contexts: nothing to do
-    if (e == 0 && p.inc && p.mode == 0) it.nrows = 0;
+    if (prompt) {
+      // the prompt rows' statistics are current up to the keys of U: incremental when U fits in
+      // two key tiles (else dense); with no salient key there is no output, only the statistics
+      it.inc = p.pinc && p.mode == 0 && e <= FA_BK && nU <= 2 * FA_BK;
+      if (it.inc) {
+        it.uk = true;
+        it.nkS = nU;
+        if (nU == 0) it.nrows = 0;  // no key changed since the statistics: nothing to do
+      }
+    } else {
+      it.inc = p.inc && p.mode == 0 && e > 0 && e <= FA_BK && r0 >= p.resp_lo;
+      // no salient key in the sequence: the keys did not change, so neither did the statistics
+      // (when current) nor the contexts: nothing to do
+      if (e == 0 && p.inc && p.mode == 0) it.nrows = 0;
+    }
   } else {
     it.type2 = true;
     it.xc = t - p.MT;
@@ -262,8 +288,8 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     attn_fused_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQx,
                       const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                       const __grid_constant__ CUtensorMap tmKx, const __grid_constant__ CUtensorMap tmDV,
-                      const __grid_constant__ CUtensorMap tmKxo,
-                      const FaParams p) {
+                      const __grid_constant__ CUtensorMap tmKxo, const __grid_constant__ CUtensorMap tmKun,
+                      const __grid_constant__ CUtensorMap tmKuo, const FaParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t *sQ = smem;                                   // [2][32 KB]
@@ -397,7 +423,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         const int sq = fa_seq(p, w);
         off = p.ex_off[sq];
         e = p.ex_off[sq + 1] - off;
-        fi = fa_item(p, w, off, e);
+        fi = fa_item(p, w, off, e, p.pinc ? p.ucnt[sq] : 0);
         if (fi.nrows > 0) break;
       }
       const int slot = wn & 3;
@@ -446,11 +472,16 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       auto after_first = [&]() {
         if (warp == 0 && lane == 0 && wnext >= 0) load_q(inext, qi + 1);
       };
-      if (it.inc) {  // type 3: new salient keys, their old keys, dV
-        load_kv(&tmKx, it.off, it.kvh);
-        after_first();
-        load_kv(&tmKxo, it.off, it.kvh);
-        load_kv(&tmDV, it.off, it.kvh);
+      if (it.inc) {  // type 3: new keys, the same keys before (tile pairs), then dV
+        const CUtensorMap *mn = it.uk ? &tmKun : &tmKx, *mo = it.uk ? &tmKuo : &tmKxo;
+        const int nt = (it.nkS + FA_BK - 1) / FA_BK;
+        const int kbase = it.uk ? seq0 : it.off;
+        for (int j = 0; j < nt; ++j) {
+          load_kv(mn, kbase + j * FA_BK, it.kvh);
+          if (j == 0) after_first();
+          load_kv(mo, kbase + j * FA_BK, it.kvh);
+        }
+        if (it.passP) load_kv(&tmDV, it.off, it.kvh);
         ++qi;
         continue;
       }
@@ -502,7 +533,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         mbar_arrive(&wq_empty[slot]);
         ++wn1;
         if (qw0 < 0) break;
-        ev(it.inc ? 3 : it.type2 ? 2 : 1);
+        ev(it.inc ? (it.uk ? 4 : 3) : it.type2 ? 2 : 1);
         const int qb = qi & 1;
         fa_wait(&q_full[qb], (qi >> 1) & 1);
         ev(9);
@@ -550,11 +581,16 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           ++g;
           ++pc;
         };
-        if (it.inc) {  // type 3: S_new, S_old, then P dV
-          qk();
-          qk();
-          pv(0, 1);
-          ++ai;
+        if (it.inc) {  // type 3: (S_new, S_old) per key tile, then P dV (P from the first new tile)
+          const int nt = (it.nkS + FA_BK - 1) / FA_BK;
+          for (int j = 0; j < nt; ++j) {
+            qk();
+            qk();
+          }
+          if (it.passP) {
+            pv(0, 1);
+            ++ai;
+          }
           umma_commit(&q_empty[qb]);
           continue;
         }
@@ -695,7 +731,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         return p.stats != nullptr && rvalid && hh == 0 && (it.type2 || p.mode == 2 || rp->rf != p.tag);
       };
       auto srow = [&]() { return static_cast<int64_t>(rp->orow) * p.H + it.h; };
-      ev(it.inc ? 3 : it.type2 ? 2 : 1);
+      ev(it.inc ? (it.uk ? 4 : 3) : it.type2 ? 2 : 1);
       float acc[FA_CW];
       float oscale = 1.f;
       if (DYLLM_FA_T4 && it.t4) {
@@ -802,33 +838,66 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           if (pos < p.fix_cap) p.fix[1 + pos] = w;
         }
       } else if (it.inc) {
-        // ---- type 3, incremental statistics (exact up to rounding): only the salient
-        // keys changed since this row's statistics (m_old, l_old) were computed, so
+        // ---- type 3, incremental statistics (exact up to rounding): only the keys in
+        // the item's changed-key list (idx_in for response tiles, U for prompt tiles) differ from
+        // the keys this row's statistics (m_old, l_old) were computed with, so
         //   l_new = l_old 2^(m_old - m) - sum_j 2^(s_old_j c - m) + sum_j 2^(s_new_j c - m),
-        // with m = max(m_old, max_j s_new_j c); P = 2^(s_new c - m) feeds P dV as in pass P. All
-        // exps on MUFU (no polynomial: the removed and added terms must carry no systematic error).
-        // A row whose l_new cancels below 2^-14 of l_old (the changed keys held nearly all its
-        // attention) sends its tile to the dense fixup launch.
+        // with m = max(m_old, max over the first new tile of s_new c); P = 2^(s_new c - m) over the
+        // salient keys (the first it.nkP columns of the first new tile) feeds P dV. All exps on MUFU
+        // (the removed and added terms must carry no systematic error). A row whose l_new cancels
+        // below 2^-14 of l_old (the changed keys held nearly all its attention), or whose later new
+        // keys score 2^64 above m, sends its tile to the dense fixup launch.
         float2 so = make_float2(0.f, 1.f);
-        // this warp's 32 key columns hold salient keys (else: no exps, P = 0 — the MUFU work
-        // follows the salient key count, not the 128-key tile)
-        const bool kact = !DYLLM_FA_KACT || hh * FA_CW < it.nkP;
+        const int nt = (it.nkS + FA_BK - 1) / FA_BK;
         float part = 0.f, mref = 0.f;
-        {
+        bool over = false;
+        // the old keys of a tile: their terms leave the normaliser
+        auto old_tile = [&](int nvalid) {
+          const int sb = sc & 1;
+          fa_wait(&s_full[sb], (sc >> 1) & 1);
+          ev(43);
+          ++sc;
+          if (wact && nvalid > 0) {
+            tc_fence_after();
+            float v[FA_CW];
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch) tmem_ld32(trow + sb * FA_BK + hh * FA_CW + ch * 32, v + ch * 32);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[sb]);
+            float sub = 0.f;
+#pragma unroll
+            for (int t = 0; t < FA_CW; ++t) sub += ex2f(t < nvalid ? fmaf(v[t], c, -mref) : -INFINITY);
+            part -= sub;
+          } else {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[sb]);
+          }
+        };
+        {  // ---- tile 0: the new keys (m, P of the salient keys), then the same keys before
+          // this warp's valid key columns (the MUFU work follows the changed-key count, not the
+          // 128-key tile: warps without one skip their exps)
+          const int nvalid = min(FA_CW, it.nkS - hh * FA_CW);
+          const bool kact = !DYLLM_FA_KACT || nvalid > 0;
           const int sb = sc & 1;
           ev(40);
           fa_wait(&s_full[sb], (sc >> 1) & 1);
           ev(41);
           ++sc;
-          const int pb = pc & 1;
-          ++pc;
+          int pb = 0;
+          if (it.passP) {
+            pb = pc & 1;
+            ++pc;
+          }
           if (!wact) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_empty[sb]);
-            fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&p_full[pb]);
-          } else if (!kact) {  // no salient key in this warp's columns: P = 0, no exps
+            if (it.passP) {
+              fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1);
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&p_full[pb]);
+            }
+          } else if (!kact) {  // no changed key in this warp's columns: no exps, P = 0
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_empty[sb]);
             xch[hh * 128 + r].x = -INFINITY;
@@ -839,17 +908,19 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             fa_named_sync(1 + quad, 32 * FA_NG);
             if (rvalid) so = rp->so;
             mref = fmaxf(so.x, mn * c);
-            fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1);
-            tc_fence_after();
-            uint32_t pk[16];
+            if (it.passP) {
+              fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1);
+              tc_fence_after();
+              uint32_t pk[16];
 #pragma unroll
-            for (int t = 0; t < 16; ++t) pk[t] = 0u;
+              for (int t = 0; t < 16; ++t) pk[t] = 0u;
 #pragma unroll
-            for (int ch = 0; ch < NCH; ++ch) tmem_st16(trow + FA_P_COL + pb * 64 + hh * (FA_CW / 2) + ch * 16, pk);
-            tmem_st_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&p_full[pb]);
+              for (int ch = 0; ch < NCH; ++ch) tmem_st16(trow + FA_P_COL + pb * 64 + hh * (FA_CW / 2) + ch * 16, pk);
+              tmem_st_wait();
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&p_full[pb]);
+            }
           } else {
             tc_fence_after();
             float v[FA_CW];
@@ -861,7 +932,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             float tmax = -INFINITY;
 #pragma unroll
             for (int t = 0; t < FA_CW; ++t) {
-              if (hh * FA_CW + t >= it.nkP) v[t] = -INFINITY;
+              if (t >= nvalid) v[t] = -INFINITY;
               tmax = fmaxf(tmax, v[t]);
             }
             xch[hh * 128 + r].x = tmax;
@@ -872,54 +943,63 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             fa_named_sync(1 + quad, 32 * FA_NG);
             if (rvalid) so = rp->so;
             mref = fmaxf(so.x, mn * c);
-            fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1);
-            tc_fence_after();
-#pragma unroll
-            for (int ch = 0; ch < NCH; ++ch) {
-              uint32_t pk[16];
-#pragma unroll
-              for (int t = 0; t < 16; ++t) {
-                const float p0 = ex2f(fmaf(v[ch * 32 + 2 * t], c, -mref));
-                const float p1 = ex2f(fmaf(v[ch * 32 + 2 * t + 1], c, -mref));
-                part += p0 + p1;
-                pk[t] = pack2(p0, p1);
-              }
-              tmem_st16(trow + FA_P_COL + pb * 64 + hh * (FA_CW / 2) + ch * 16, pk);
-            }
-            tmem_st_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&p_full[pb]);
-          }
-          ev(42);
-        }
-        {  // the same keys before this step's overwrite
-          const int sb = sc & 1;
-          fa_wait(&s_full[sb], (sc >> 1) & 1);
-          ev(43);
-          ++sc;
-          if (!wact) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&s_empty[sb]);
-          } else {
-            float sub = 0.f;
-            if (kact) {
+            if (it.passP) {
+              // P over the salient keys (columns < nkP), bf16x2-packed into the P buffer; every
+              // valid column's term (masked keys: 2^-inf = 0) enters the normaliser
+              const int npv = it.nkP - hh * FA_CW;
+              fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1);
               tc_fence_after();
-              float v[FA_CW];
 #pragma unroll
-              for (int ch = 0; ch < NCH; ++ch) tmem_ld32(trow + sb * FA_BK + hh * FA_CW + ch * 32, v + ch * 32);
+              for (int ch = 0; ch < NCH; ++ch) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int t = 0; t < 16; ++t) {
+                  const int t0 = ch * 32 + 2 * t;
+                  const float p0 = ex2f(fmaf(v[t0], c, -mref)), p1 = ex2f(fmaf(v[t0 + 1], c, -mref));
+                  part += p0 + p1;
+                  pk[t] = pack2(t0 < npv ? p0 : 0.f, t0 + 1 < npv ? p1 : 0.f);
+                }
+                tmem_st16(trow + FA_P_COL + pb * 64 + hh * (FA_CW / 2) + ch * 16, pk);
+              }
+              tmem_st_wait();
               tc_fence_before();
               __syncwarp();
-              if (lane == 0) mbar_arrive(&s_empty[sb]);
-#pragma unroll
-              for (int t = 0; t < FA_CW; ++t)
-                sub += hh * FA_CW + t < it.nkP ? ex2f(fmaf(v[t], c, -mref)) : 0.f;
+              if (lane == 0) mbar_arrive(&p_full[pb]);
             } else {
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&s_empty[sb]);
+#pragma unroll
+              for (int t = 0; t < FA_CW; ++t) part += ex2f(fmaf(v[t], c, -mref));
             }
-            part -= sub;
           }
+          ev(42);
+          old_tile(nvalid);
+        }
+        for (int jt = 1; jt < nt; ++jt) {  // ---- further tiles of U (prompt tiles): sums only
+          const int nvalid = min(FA_CW, it.nkS - (jt * FA_BK + hh * FA_CW));
+          const int sb = sc & 1;
+          fa_wait(&s_full[sb], (sc >> 1) & 1);
+          ++sc;
+          if (wact && nvalid > 0) {
+            tc_fence_after();
+            float v[FA_CW];
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch) tmem_ld32(trow + sb * FA_BK + hh * FA_CW + ch * 32, v + ch * 32);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[sb]);
+            float add = 0.f, tmax = -INFINITY;
+#pragma unroll
+            for (int t = 0; t < FA_CW; ++t) {
+              const float x = t < nvalid ? fmaf(v[t], c, -mref) : -INFINITY;
+              tmax = fmaxf(tmax, x);
+              add += ex2f(x);
+            }
+            over = over || tmax > 64.f;
+            part += add;
+          } else {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[sb]);
+          }
+          old_tile(nvalid);
         }
         float Lnew = 1.f;
         bool bad = false;
@@ -932,27 +1012,30 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           fa_named_sync(1 + quad, 32 * FA_NG);
           const float base = so.y * ex2f(so.x - mref);
           Lnew = base + tot;
-          bad = !(so.y > 0.f) || !(Lnew > base * 0x1p-14f) || !(Lnew < INFINITY);
+          bad = over || !(so.y > 0.f) || !(Lnew > base * 0x1p-14f) || !(Lnew < INFINITY);
           if (own_stats() && !bad) p.stats[srow()] = make_float2(mref, Lnew);
         }
         // a tile with a cancelled row is recomputed densely by the fixup launch (duplicates of a
-        // tile id are harmless: the dense recomputation is deterministic)
-        if (__ballot_sync(0xffffffffu, bad && write_row()) != 0u && lane == 0) {
+        // tile id are harmless: the dense recomputation is deterministic); `over` is per column
+        // group, so every warp's rows vote
+        if (__ballot_sync(0xffffffffu, bad && rvalid && (it.type2 || rp->rf != p.tag)) != 0u && lane == 0) {
           const int pos = atomicAdd(&p.fix[0], 1);
           if (pos < p.fix_cap) p.fix[1 + pos] = w;
         }
         ev(50);
-        fa_wait(acc_full, ai & 1);
-        ev(51);
-        ++ai;
-        if (wact) {
-          tc_fence_after();
+        if (it.passP) {
+          fa_wait(acc_full, ai & 1);
+          ev(51);
+          ++ai;
+          if (wact) {
+            tc_fence_after();
 #pragma unroll
-          for (int ch = 0; ch < NCH; ++ch) tmem_ld32(trow + FA_ACC_COL + hh * FA_CW + ch * 32, acc + ch * 32);
-          tc_fence_before();
+            for (int ch = 0; ch < NCH; ++ch) tmem_ld32(trow + FA_ACC_COL + hh * FA_CW + ch * 32, acc + ch * 32);
+            tc_fence_before();
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(acc_empty);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(acc_empty);
         oscale = 1.f / Lnew;
       } else if (it.single) {
         // ---- exact rows: one pass over the N keys. P = 2^((s - ref) c) with ONE reference per
@@ -1269,7 +1352,7 @@ int attention_fused_launch(const AttnArgs &a, cudaStream_t st) {
   }
   const int rows_total = a.batch * a.N;
   const int qw = a.H * 128, kw = a.KVH * 128;
-  CUtensorMap tq, tqx, tk, tv, tkx, tdv, tkxo;
+  CUtensorMap tq, tqx, tk, tv, tkx, tdv, tkxo, tkun, tkuo;
   int rc;
   if ((rc = make_tmap3(&tq, a.Q, rows_total, qw, 128, 2))) return rc;
   if ((rc = make_tmap3(&tqx, a.Qx ? a.Qx : a.Q, rows_total, qw, 128, 2))) return rc;
@@ -1278,6 +1361,9 @@ int attention_fused_launch(const AttnArgs &a, cudaStream_t st) {
   if ((rc = make_tmap3(&tkx, a.Kx ? a.Kx : a.K, rows_total, kw, FA_BK, 2))) return rc;
   if ((rc = make_tmap3(&tdv, a.dV ? a.dV : a.V, rows_total, kw, FA_BK, 2))) return rc;
   if ((rc = make_tmap3(&tkxo, a.Kxo ? a.Kxo : a.K, rows_total, kw, FA_BK, 2))) return rc;
+  const bool pinc = a.pinc && a.Kun && a.Kuo && a.ucnt && a.stats_cache && a.mode == 0;
+  if ((rc = make_tmap3(&tkun, pinc ? a.Kun : a.K, rows_total, kw, FA_BK, 2))) return rc;
+  if ((rc = make_tmap3(&tkuo, pinc ? a.Kuo : a.K, rows_total, kw, FA_BK, 2))) return rc;
   FaParams p;
   p.N = a.N;
   p.row_lo = a.row_lo;
@@ -1285,7 +1371,13 @@ int attention_fused_launch(const AttnArgs &a, cudaStream_t st) {
   p.H = a.H;
   p.KVH = a.KVH;
   p.grp = a.H / a.KVH;
-  p.MT = a.full_only ? 0 : (p.L + 127) / 128;
+  // row tiles: prompt tiles and response tiles never mix (their statistics are current up to
+  // different key sets), so a full-input launch splits its rows at resp_lo
+  const bool split = !a.full_only && a.row_lo < a.resp_lo && a.resp_lo < a.N;
+  p.MTp = split ? (a.resp_lo - a.row_lo + 127) / 128 : 0;
+  p.MT = a.full_only ? 0 : split ? p.MTp + (a.N - a.resp_lo + 127) / 128 : (p.L + 127) / 128;
+  p.pinc = pinc ? 1 : 0;
+  p.ucnt = a.ucnt;
   p.XT = (a.max_rows_per_seq + 127) / 128;
   p.items = a.batch * a.H * (p.MT + p.XT);
   p.qw = qw;
@@ -1317,7 +1409,7 @@ int attention_fused_launch(const AttnArgs &a, cudaStream_t st) {
   // fixup launch: a few CTAs claim the (rare, device-counted) listed tiles
   const int grid = p.mode == 1 ? 16 : (p.items < a.num_sms ? p.items : a.num_sms);
   DY_CUDA(launch_k(attn_fused_kernel, dim3(grid), dim3(FA_THREADS), FA_SMEM, st, 1, tq, tqx, tk, tv, tkx, tdv, tkxo,
-                   p));
+                   tkun, tkuo, p));
   DY_CUDA(cudaGetLastError());
   return DYLLM_OK;
 }

@@ -95,7 +95,8 @@ struct KScope {
   } while (0)
 static constexpr int64_t kMaskCap = 1 << 20;
 static constexpr int kFixCap = 1 << 16;
-static bool g_attn_inc_enabled = true;  // test hook: incremental attention statistics  // fused attention: tiles re-run densely after a cancelled update
+static bool g_attn_inc_enabled = true;   // test hook: incremental attention statistics (response tiles)
+static bool g_attn_pinc_enabled = true;  // test hook: incremental prompt statistics in full-input steps
 
 struct LayerW {
   bf16 *g_attn, *wqkv, *bqkv, *wo, *g_ffn, *wgu, *wd;
@@ -111,6 +112,13 @@ struct LayerC {
   float2 *st = nullptr;  // [rows][H] softmax statistics (m c, l) of the fused attention (head_dim 128)
   mutable bool st_ok = false;  // statistics of the response rows are current (incremental tiles
                                // allowed); cleared whenever K or Q may be written from outside
+  // incremental prompt statistics of full-input steps: the prompt rows' statistics are
+  // current as of the start of `epoch` (every full-input attention, FullStep or refresh begins a new
+  // one); a key row written since then has dtag == epoch and its key at the epoch start in Kfi
+  bf16 *Kfi = nullptr;
+  uint32_t *dtag = nullptr;
+  uint32_t epoch = 1;
+  mutable bool pst_ok = false;
 };
 struct dyllm_cache {
   dyllm_model_cfg m;
@@ -129,6 +137,8 @@ struct dyllm_cache {
   int *ap_rows, *ap_off, *all_rows, *all_off, *zero_off, *lm_rows, *lm_off;
   int *dec_prev;
   int *qx_rows, *qx_off;  // layer1_policy 0: decoded rows outside idx_in (Q-only refresh, D6)
+  int *urows = nullptr, *ucnt = nullptr;  // changed-key lists U of a full-input step ([b][N], [b])
+  bf16 *Kun = nullptr, *Kuo = nullptr;    // their keys now / at the statistics epoch (compact per sequence)
   int32_t *tr_lists = nullptr, *tr_offs = nullptr;  // dyllm_cache_set_trace (caller-owned)
   float *tr_sims = nullptr;
   float *sim;  // per-row similarity scratch (fraction mode)
@@ -446,7 +456,17 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
     ALE(L.Q, rows * qw);
     ALE(L.C, rows * qw);
     ALE(L.H, rows * d);
-    if (m.head_dim == 128 && !f32) AL(L.st, rows * m.n_heads);
+    if (m.head_dim == 128 && !f32) {
+      AL(L.st, rows * m.n_heads);
+      AL(L.Kfi, rows * kw);
+      AL(L.dtag, rows);
+    }
+  }
+  if (m.head_dim == 128 && !f32) {
+    AL(c->urows, rows);
+    AL(c->ucnt, r->batch);
+    AL(c->Kun, rows * kw);
+    AL(c->Kuo, rows * kw);
   }
   ALE(c->H0, rows * d);
   ALE(c->Xn, rows * d);
@@ -499,7 +519,13 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
                   cudaMemsetAsync(c->rowflag, 0, rows * sizeof(uint32_t), st) == cudaSuccess &&
                   cudaMemsetAsync(c->Qx, 0, rows * qw * c->es, st) == cudaSuccess &&
                   cudaMemsetAsync(c->zero_off, 0, (r->batch + 1) * sizeof(int), st) == cudaSuccess;
-  if (!ok) {
+  bool ok2 = ok;
+  for (auto &L : c->L)
+    if (L.dtag) ok2 = ok2 && cudaMemsetAsync(L.dtag, 0, rows * sizeof(uint32_t), st) == cudaSuccess;
+  if (c->Kun)
+    ok2 = ok2 && cudaMemsetAsync(c->Kun, 0, rows * kw * 2, st) == cudaSuccess &&
+          cudaMemsetAsync(c->Kuo, 0, rows * kw * 2, st) == cudaSuccess;
+  if (!ok2) {
     set_error("memset failed");
     dyllm_cache_destroy(c);
     return DYLLM_E_CUDA;
@@ -750,6 +776,8 @@ static int full_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c
       KL(OTHER, RET(attention_launch(f, st)));
     }
     C.st_ok = fused;
+    C.pst_ok = fused;  // every row's statistics were just computed: a new epoch
+    ++C.epoch;
     int prc = post_attention(ctx, w, c, l, nullptr, C.C, Hprev, nullptr, C.H);
     if (prc) {
       ctx->cls_offset = 0;
@@ -792,7 +820,13 @@ static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *
   const bool inc = fused && g_attn_inc_enabled && C.st_ok && !(l == 0 && c->r.layer1_policy == 0);
   KL(QKV_POST, launch_qkv_post(c->qkv, idx_in, M_in, rows, L.bqkv, N, m.n_heads, m.n_kv_heads, m.head_dim,
                                c->rope_cs, C.Q, C.K, C.V, c->dV, c->Qx, c->Kx, inc ? c->Kxo : nullptr,
-                               fused ? c->rowflag : nullptr, tag, st));
+                               fused ? c->rowflag : nullptr, tag, st, 0, fused ? C.Kfi : nullptr, C.dtag, C.epoch));
+  // full-input step with current prompt statistics: the keys changed since they were current
+  const bool full_in = row_lo < c->r.L_P;
+  const bool pinc = fused && full_in && g_attn_inc_enabled && g_attn_pinc_enabled && C.pst_ok;
+  if (pinc)
+    KL(OTHER, launch_build_u(idx_in, off_in, c->rowflag, tag, C.dtag, C.epoch, C.K, C.Kfi, b, N, kw, c->urows, c->Kun,
+                             c->Kuo, c->ucnt, st));
   // a4: exact rows + approximate rows (Alg. 4) -> Cn
   AttnArgs a{};
   a.batch = b;
@@ -828,14 +862,23 @@ static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *
   a.resp_lo = c->r.L_P;
   a.fix = ctx->attn_fix;
   a.fix_cap = kFixCap;
+  a.Kun = c->Kun;
+  a.Kuo = c->Kuo;
+  a.ucnt = c->ucnt;
+  a.pinc = pinc;
   KL(ATTN, RET(attention_launch(a, st)));
   if (fused) {  // tiles whose incremental update cancelled or whose single pass could overflow (rare)
     AttnArgs f = a;
     f.mode = 1;
     KL(OTHER, RET(attention_launch(f, st)));  // not an attention pass of its own (roofline accounting)
   }
-  // every input row's statistics are now current (dense tiles, incremental tiles, exact rows)
+  // every input row's statistics are now current (dense tiles, incremental tiles, exact rows);
+  // after a full-input step that includes the prompt rows: a new epoch
   C.st_ok = fused;
+  if (fused && full_in) {
+    C.pst_ok = true;
+    ++C.epoch;
+  }
   // a5: cosine similarity + threshold + compaction; C_cache <- Cn for the input rows
   const bool fmode = c->r.select_mode == 1;
   const bool delta = attention_writes_delta(m.head_dim);  // fused kernel: Cn = dC for approximate rows
@@ -1050,6 +1093,11 @@ int dyllm_set_option(int option, int value) {
     g_attn_inc_enabled = value != 0;
     return prev;
   }
+  if (option == DYLLM_OPT_ATTN_PINC) {
+    const int prev = g_attn_pinc_enabled ? 1 : 0;
+    g_attn_pinc_enabled = value != 0;
+    return prev;
+  }
   if (option == DYLLM_OPT_ATTN_T4) {
     const int prev = g_attn_t4_rows;
     g_attn_t4_rows = value < 0 ? 0 : (value > 32 ? 32 : value);
@@ -1127,7 +1175,7 @@ int dyllm_cache_tensor(const dyllm_cache *c, int layer, int which, void **d_ptr,
   RET(tensor_ptr(c, layer, which, d_ptr, n_elems, nullptr));
   // K / Q / statistics handed out writable: the incremental softmax statistics of that layer can
   // no longer be trusted until the next dense pass (a denoising step, or dyllm_cache_refresh_stats)
-  if (which == DYLLM_K || which == DYLLM_Q || which == DYLLM_STATS) c->L[layer].st_ok = false;
+  if (which == DYLLM_K || which == DYLLM_Q || which == DYLLM_STATS) c->L[layer].st_ok = c->L[layer].pst_ok = false;
   return DYLLM_OK;
 }
 
@@ -1147,8 +1195,11 @@ int dyllm_cache_copy(dyllm_ctx *ctx, dyllm_cache *c, int layer, int which, void 
   c->initialized = true;
   // imported K / Q invalidate the statistics; imported statistics are the caller's claim that
   // they belong to the current K and Q
-  if (which == DYLLM_K || which == DYLLM_Q) c->L[layer].st_ok = false;
-  if (which == DYLLM_STATS) c->L[layer].st_ok = true;
+  if (which == DYLLM_K || which == DYLLM_Q) c->L[layer].st_ok = c->L[layer].pst_ok = false;
+  if (which == DYLLM_STATS) {  // every row's statistics, current for the present K: a new epoch
+    c->L[layer].st_ok = c->L[layer].pst_ok = true;
+    ++c->L[layer].epoch;
+  }
   return DYLLM_OK;
 }
 
@@ -1223,7 +1274,8 @@ int dyllm_cache_refresh_stats(dyllm_ctx *ctx, dyllm_cache *c, int layer) {
   a.fix_cap = kFixCap;
   a.mode = 2;
   KL(ATTN, RET(attention_launch(a, ctx->stream)));
-  C.st_ok = true;
+  C.st_ok = C.pst_ok = true;
+  ++C.epoch;
   DY_CUDA(cudaGetLastError());
   return DYLLM_OK;
 }

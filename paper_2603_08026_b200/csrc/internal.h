@@ -135,6 +135,12 @@ struct AttnArgs {
   int mode = 0;                   // 0 step, 1 fixup list, 2 statistics refresh
   int *fix = nullptr;             // [1 + fix_cap] fixup list (ctx-owned, count zero between steps)
   int fix_cap = 0;
+  // incremental statistics of the prompt rows in full-input steps: the keys changed since those
+  // statistics were current (U: idx_in first, then the keys written since), compact per sequence
+  // at rows [s*N, s*N + ucnt[s]): new values Kun, values at the statistics' time Kuo
+  const bf16 *Kun = nullptr, *Kuo = nullptr;
+  const int *ucnt = nullptr;
+  bool pinc = false;
 };
 int attention_launch(const AttnArgs &a, cudaStream_t st);
 int attention_fused_launch(const AttnArgs &a, cudaStream_t st);  // attn_fused.cu

@@ -144,7 +144,8 @@ __global__ void qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restr
                                 int H, int KVH, int hd, const float2 *__restrict__ rope_cs, bf16 *__restrict__ Qc,
                                 bf16 *__restrict__ Kc, bf16 *__restrict__ Vc, bf16 *__restrict__ dV,
                                 bf16 *__restrict__ Qx, bf16 *__restrict__ Kx, bf16 *__restrict__ Kxo,
-                                uint32_t *__restrict__ rowflag, uint32_t tag, int q_only) {
+                                uint32_t *__restrict__ rowflag, uint32_t tag, int q_only,
+                                bf16 *__restrict__ Kfi, uint32_t *__restrict__ dtag, uint32_t epoch) {
   pdl_wait();
   const int M = M_ptr ? *M_ptr : M_cap;
   const int qw = H * hd, kw = KVH * hd, W = qw + 2 * kw;
@@ -158,6 +159,15 @@ __global__ void qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restr
     const bf16 *src = qkv + static_cast<int64_t>(i) * W;
     if (rowflag && !q_only && threadIdx.x == 0) rowflag[r] = tag;  // exact row of this layer step (fused attention)
     const float2 *cs = rope_cs + static_cast<int64_t>(pos) * half;
+    // statistics epochs (incremental prompt statistics): the first write of a key row
+    // since its layer's epoch began keeps the overwritten key in Kfi (the key the prompt rows'
+    // statistics were computed with) and marks the row changed
+    bool snap = false;
+    if (Kfi && !q_only) {
+      snap = dtag[r] != epoch;
+      __syncthreads();  // every thread has read the tag before it changes
+      if (snap && threadIdx.x == 0) dtag[r] = epoch;
+    }
     for (int rd = 0; rd < rounds; ++rd) {
       const int v = rd * blockDim.x + threadIdx.x;
       const bool has_qk = v < nqk, has_v = v < nvv;
@@ -178,7 +188,7 @@ __global__ void qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restr
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) c4[j] = reinterpret_cast<const float4 *>(cs + k0)[j];
-        if (Kxo && col >= qw) {  // the key row this step overwrites (incremental statistics)
+        if ((Kxo || snap) && col >= qw) {  // the key row this step overwrites (incremental statistics)
           const bf16 *ko = Kc + static_cast<int64_t>(r) * kw + (col - qw);
           uk1 = *reinterpret_cast<const uint4 *>(ko);
           uk2 = *reinterpret_cast<const uint4 *>(ko + half);
@@ -230,6 +240,11 @@ __global__ void qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restr
           bf16 *xo = Kxo + static_cast<int64_t>(i) * kw + (col - qw);
           *reinterpret_cast<uint4 *>(xo) = uk1;
           *reinterpret_cast<uint4 *>(xo + half) = uk2;
+        }
+        if (snap && col >= qw) {
+          bf16 *xf = Kfi + static_cast<int64_t>(r) * kw + (col - qw);
+          *reinterpret_cast<uint4 *>(xf) = uk1;
+          *reinterpret_cast<uint4 *>(xf + half) = uk2;
         }
       }
       // v: dV = v_new - V_cache (read before the overwrite), then V_cache <- v_new
@@ -371,6 +386,62 @@ __global__ void build_list_kernel(int mode, const int *__restrict__ carried, con
       __syncthreads();
     }
     if (threadIdx.x == 0) out_off[s + 1] = base;
+  }
+}
+
+// Changed-key list U of each sequence for the incremental prompt statistics of a full-input step
+// (SURVEY §8f1): its idx_in rows in list order (their new keys are the salient keys of the P pass),
+// then the other rows whose key was written since the layer's statistics epoch began (ascending).
+// One CTA per sequence; row ids at urows[s*N ..), count ucnt[s]; the first kUcap entries' keys
+// are gathered compact: Kun = current K, Kuo = the key at the epoch start (Kfi).
+constexpr int kUcap = 256;  // two key tiles: larger lists take the dense path
+__global__ void build_u_kernel(const int *__restrict__ idx_in, const int *__restrict__ off_in,
+                               const uint32_t *__restrict__ rowflag, uint32_t tag, const uint32_t *__restrict__ dtag,
+                               uint32_t epoch, const bf16 *__restrict__ K, const bf16 *__restrict__ Kfi, int N, int kw,
+                               int *__restrict__ urows, bf16 *__restrict__ Kun, bf16 *__restrict__ Kuo,
+                               int *__restrict__ ucnt) {
+  pdl_wait();
+  __shared__ int warp_cnt[32];
+  __shared__ int total;
+  const int s = blockIdx.x;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  const int b0 = off_in[s], e = off_in[s + 1] - b0;
+  int *u = urows + static_cast<int64_t>(s) * N;
+  for (int j = threadIdx.x; j < e; j += blockDim.x) u[j] = idx_in[b0 + j];
+  int base = e;
+  for (int p0 = 0; p0 < N; p0 += blockDim.x) {
+    const int p = p0 + threadIdx.x;
+    const int64_t r = static_cast<int64_t>(s) * N + p;
+    const bool keep = p < N && dtag[r] == epoch && rowflag[r] != tag;
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) warp_cnt[warp] = __popc(m);
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int w = 0; w < nw; ++w) {
+      before += (w < warp) ? warp_cnt[w] : 0;
+      tot += warp_cnt[w];
+    }
+    if (keep) u[base + before + __popc(m & ((1u << lane) - 1))] = static_cast<int>(r);
+    base += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    ucnt[s] = base;
+    total = base;
+  }
+  __syncthreads();
+  const int n = min(total, kUcap), nv = kw / 8;
+  for (int i = warp; i < n; i += nw) {
+    const int64_t r = u[i];
+    const uint4 *kn = reinterpret_cast<const uint4 *>(K + r * kw);
+    const uint4 *ko = reinterpret_cast<const uint4 *>(Kfi + r * kw);
+    uint4 *dn = reinterpret_cast<uint4 *>(Kun + (static_cast<int64_t>(s) * N + i) * kw);
+    uint4 *dd = reinterpret_cast<uint4 *>(Kuo + (static_cast<int64_t>(s) * N + i) * kw);
+    for (int c = lane; c < nv; c += 32) {
+      const uint4 a = kn[c], b = ko[c];
+      dn[c] = a;
+      dd[c] = b;
+    }
   }
 }
 
@@ -856,12 +927,19 @@ void launch_rmsnorm_rows(const bf16 *src, const int *M_ptr, int M_cap, const bf1
 }
 void launch_qkv_post(const bf16 *qkv, const int *idx, const int *M_ptr, int M_cap, const bf16 *bias, int N, int H,
                      int KVH, int hd, const float2 *rope_cs, bf16 *Qc, bf16 *Kc, bf16 *Vc, bf16 *dV, bf16 *Qx,
-                     bf16 *Kx, bf16 *Kxo, uint32_t *rowflag, uint32_t tag, cudaStream_t st, int q_only) {
+                     bf16 *Kx, bf16 *Kxo, uint32_t *rowflag, uint32_t tag, cudaStream_t st, int q_only, bf16 *Kfi,
+                     uint32_t *dtag, uint32_t epoch) {
   const int g = M_cap < 148 * 4 ? M_cap : 148 * 4;  // one row per CTA per pass; capped like grid_for
   const int work = std::max((H + KVH) * (hd / 16), KVH * hd / 8);  // vectors per row of each part
   const int threads = std::min(1024, std::max(32, (work + 31) / 32 * 32));
   DY_CUDA_LAUNCH(launch_k(qkv_post_kernel, dim3(g > 0 ? g : 1), dim3(threads), 0, st, 1, qkv, idx, M_ptr, M_cap, bias, N, H, KVH, hd, rope_cs, Qc, Kc, Vc,
-                                                 dV, Qx, Kx, Kxo, rowflag, tag, q_only));
+                                                 dV, Qx, Kx, Kxo, rowflag, tag, q_only, Kfi, dtag, epoch));
+}
+void launch_build_u(const int *idx_in, const int *off_in, const uint32_t *rowflag, uint32_t tag, const uint32_t *dtag,
+                    uint32_t epoch, const bf16 *K, const bf16 *Kfi, int batch, int N, int kw, int *urows, bf16 *Kun,
+                    bf16 *Kuo, int *ucnt, cudaStream_t st) {
+  DY_CUDA_LAUNCH(launch_k(build_u_kernel, dim3(batch), dim3(512), 0, st, 1, idx_in, off_in, rowflag, tag, dtag, epoch, K,
+                          Kfi, N, kw, urows, Kun, Kuo, ucnt));
 }
 void launch_rope_table(float2 *cs, int N, int hd, double theta, cudaStream_t st) {
   DY_CUDA_LAUNCH(launch_k(rope_table_kernel, dim3(148), dim3(256), 0, st, 1, cs, N, hd, theta));

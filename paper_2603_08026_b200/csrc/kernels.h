@@ -20,7 +20,11 @@ void launch_rmsnorm_rows(const bf16 *src, const int *M_ptr, int M_cap, const bf1
 void launch_qkv_post(const bf16 *qkv, const int *idx, const int *M_ptr, int M_cap, const bf16 *bias, int N, int H,
                      int KVH, int hd, const float2 *rope_cs, bf16 *Qc, bf16 *Kc, bf16 *Vc, bf16 *dV, bf16 *Qx,
                      bf16 *Kx, bf16 *Kxo, uint32_t *rowflag, uint32_t tag,
-                     cudaStream_t st, int q_only = 0);
+                     cudaStream_t st, int q_only = 0, bf16 *Kfi = nullptr, uint32_t *dtag = nullptr,
+                     uint32_t epoch = 0);
+void launch_build_u(const int *idx_in, const int *off_in, const uint32_t *rowflag, uint32_t tag, const uint32_t *dtag,
+                    uint32_t epoch, const bf16 *K, const bf16 *Kfi, int batch, int N, int kw, int *urows, bf16 *Kun,
+                    bf16 *Kuo, int *ucnt, cudaStream_t st);
 void launch_rope_table(float2 *cs, int N, int hd, double theta, cudaStream_t st);
 void launch_approx_rows(const int *idx_in, const int *off_in, int batch, int N, int row_lo, int *ap_rows,
                         int *ap_off, cudaStream_t st);

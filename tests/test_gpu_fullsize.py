@@ -179,10 +179,12 @@ def test_incremental_statistics_drift_full_size():
     """Incremental softmax statistics over a whole LLaDA-8B-shape generation
     prefix (batch 16, N = 956, 4 FullSteps + 64 denoising steps, f = 0.1): after every step, the
     statistics the attention kept incrementally for each layer are compared with a dense
-    recomputation from the same K and Q caches (dyllm_cache_refresh_stats), then restored so the
-    incremental state keeps accumulating. log2 of Alg. 4's normaliser (m + log2 l, DYLLM_STATS)
-    must agree within 1e-3 on every row whose statistics are current (response rows after every
-    step; all rows after full-input steps)."""
+    recomputation from the same K and Q caches (copied into a second cache and refreshed there with
+    dyllm_cache_refresh_stats, so the generation's own incremental state — statistics, epochs and
+    changed-key snapshots — keeps accumulating untouched). log2 of Alg. 4's normaliser
+    (m + log2 l, DYLLM_STATS) must agree within 1e-3 on every row whose statistics are current
+    (response rows after every step; all rows after full-input steps, whose prompt rows are updated
+    by the keys changed since the previous full-input step)."""
     from paper_2603_08026_b200 import dyllm as dy
     cfg, run = configs.preset("llada8b")
     cfg = replace(cfg, n_layers=2)
@@ -193,6 +195,8 @@ def test_incremental_statistics_drift_full_size():
     prompts = torch.tensor(gen.prompt_tokens(SEED, run.batch, run.L_P, cfg.mask_id), dtype=torch.int32)
     eng.load_prompts(prompts.cuda())
     taus = np.full(cfg.n_layers, 0.1, np.float32)
+    ref = dy.Cache(ctx, w, run)     # dense reference: same K / Q, statistics recomputed
+    ref.init(eng.tokens)
     worst = 0.0
     for t in range(run.T_full + 64):
         eng.cache.denoise_step(t, taus, eng.tokens, eng.dec_pos, eng.dec_tok)
@@ -201,9 +205,10 @@ def test_incremental_statistics_drift_full_size():
         lo = 0 if t % run.full_period == 0 else run.L_P
         for l in range(cfg.n_layers):
             inc = eng.cache.export(l, dy.STATS)
-            eng.cache.refresh_stats(l)
-            dense = eng.cache.export(l, dy.STATS)
-            eng.cache.import_(l, dy.STATS, inc)
+            for which in (dy.K, dy.Q):
+                ref.import_(l, which, eng.cache.export(l, which))
+            ref.refresh_stats(l)
+            dense = ref.export(l, dy.STATS)
             torch.cuda.synchronize()
             lse = lambda s: (s[..., 0].double() + torch.log2(s[..., 1].double()))[:, lo:]
             err = (lse(inc) - lse(dense)).abs().max().item()

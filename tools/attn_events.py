@@ -4,7 +4,7 @@ per-role event logs of CTAs 0-1 for the last layer of one denoising step of the 
     DYLLM_NVCC_FLAGS=-DDYLLM_ATTN_EVENTS=1 python -m paper_2603_08026_b200.build --force
     python tools/attn_events.py --mode ro|fi|full [--items 3]
 
-Codes: MMA 1/2/3 item (type 1/2/3), 9 Q ready, 10 QK begin, 11 S buffer free, 12 K tile ready, 13 QK issued,
+Codes: MMA 1/2/3/4 item (type 1/2/3, 4 = type 3 over the prompt U lists), 9 Q ready, 10 QK begin, 11 S buffer free, 12 K tile ready, 13 QK issued,
 20 PV begin, 21 P ready, 22 V/acc ready, 23 PV issued. Softmax (warp 2) 1/2 item, 30 S wait,
 31 S ready, 32 S read (buffer released), 33 S tile done, 40 P-pass S wait, 41 ready, 42 P stored,
 50 acc wait, 51 acc ready, 52 epilogue done. Producer 60 K slot wait, 61 K issued, 62/63 claim begin/end, 64/65 Q slot wait begin/end. V 70, 71.
@@ -89,9 +89,9 @@ for role in range(4):
             print(f"   {name:18s} total {sums[name]:8.1f} us  n={cnt[name]:5d}  mean {sums[name] / cnt[name] * 1e3:7.0f} ns")
     if role in (0, 1):
         # per-item durations
-        starts = [(t, code) for code, t in ev if code in (1, 2, 3)]
+        starts = [(t, code) for code, t in ev if code in (1, 2, 3, 4)]
         durs = [((starts[i + 1][0] - starts[i][0]) * cyc, starts[i][1]) for i in range(len(starts) - 1)]
-        for kind in (1, 2, 3):
+        for kind in (1, 2, 3, 4):
             d = [x for x, k in durs if k == kind]
             if d:
                 print(f"   items type {kind}: n={len(d)} mean {np.mean(d):.2f} us  min {np.min(d):.2f}  max {np.max(d):.2f}")
@@ -108,7 +108,7 @@ if a.kind:
 n_items = 0
 print("== timeline (first items): time_us role code")
 for t, r, c in merged:
-    if r == "M" and c in (1, 2, 3):
+    if r == "M" and c in (1, 2, 3, 4):
         n_items += 1
         if n_items > a.items:
             break

@@ -1,0 +1,5 @@
+# round 2: incremental prompt statistics in full-input steps (U lists) — GPU tests + bench
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.smoke(); print('SMOKE OK')" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; tail -8 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench.log 2>&1; tail -c 600 gpurun_out/bench.log
