@@ -258,7 +258,14 @@ uint64_t dyllm_launch_count(void);
  * keys written by the response-only steps since), instead of recomputing them over all N keys
  * (SURVEY §8f1, D20). 0 = dense prompt tiles. */
 enum { DYLLM_OPT_SKINNY_GEMM = 1, DYLLM_OPT_SKINNY_SPLIT = 2, DYLLM_OPT_ATTN_FUSED = 3, DYLLM_OPT_SKINNY_ONE_CHUNK = 4,
-       DYLLM_OPT_PDL = 5, DYLLM_OPT_ATTN_INC = 6, DYLLM_OPT_ATTN_T4 = 7, DYLLM_OPT_ATTN_PINC = 8 };
+       DYLLM_OPT_PDL = 5, DYLLM_OPT_ATTN_INC = 6, DYLLM_OPT_ATTN_T4 = 7, DYLLM_OPT_ATTN_PINC = 8,
+       DYLLM_OPT_ATTN_COS = 9, DYLLM_OPT_SKINNY_CHUNK = 10 };
+/* DYLLM_OPT_SKINNY_CHUNK (default 0 = 256): largest number of activation rows per chunk of the
+ * skinny GEMM when the rows are chunked (tuning hook). */
+/* DYLLM_OPT_ATTN_COS (default 0, measured slower): head_dim-128 sparse steps form C_new, commit it to the C cache and
+ * compute the per-(row, head) cosine partials in the attention epilogue; the
+ * selection kernel then reads 16 bytes per (row, head) instead of both context rows. 0 = the
+ * attention writes dC / C rows to scratch and the selection kernel forms, compares and commits. */
 int dyllm_set_option(int option, int value);
 
 /* Debug hook: when d_buf != NULL, kernels of family `which` (0 = skinny GEMM) write %globaltimer

@@ -98,7 +98,16 @@ struct FaParams {
   int MTp;
   int pinc;                   // prompt statistics current up to U: incremental prompt tiles allowed
   const int *ucnt;            // [b] |U| per sequence
+  // similarity partials fused into the epilogue: when set, the epilogue reads the
+  // cached context C_old of each written row, commits C_new = C_old + dC (approximate rows) or C
+  // (exact rows) into C_cache (= C_out) in place, and writes per (row, head) the partial sums
+  // (<C_new, C_old>, |C_new|^2, |C_old|^2) over the head's dims, which the selection kernel adds
+  // over the heads: the rows are read and written once, by the kernel that produces them
+  float4 *cos_part;           // [b*N][H] or nullptr
 };
+// statistics entry of a row whose tile was handed to the fixup launch (its output was not written;
+// the fixup launch recomputes exactly the rows carrying it)
+constexpr float FA_PENDING = -1.f;
 
 struct FaItem {
   int s, h, kvh, nrows, q_row, off, nkP, xc;
@@ -284,6 +293,9 @@ struct FaEv {
 #endif
 };
 
+// COS: the fused similarity-partials epilogue is compiled in (a separate instance,
+// so its registers do not weigh on the default kernel)
+template <bool COS>
 __global__ void __launch_bounds__(FA_THREADS, 1)
     attn_fused_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQx,
                       const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
@@ -296,6 +308,11 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   uint8_t *sKV = sQ + FA_QST * FA_Q_BYTES;              // [4][32 KB] K, V or dV tiles
   uint8_t *sPT = sKV + FA_KVST * FA_KV_BYTES;           // [2][8 KB] type-4 P^T tiles (1024-aligned)
   float2 *xch = reinterpret_cast<float2 *>(sPT + FA_PT);  // [column group][128 rows]
+  // similarity partial exchange [item parity][column group][128 rows] (the type-4 P^T tiles' space:
+  // type 4 and the fused partials are never built together)
+  float4 *cpx = reinterpret_cast<float4 *>(sPT);
+  static_assert(DYLLM_FA_T4 == 0 || true, "");
+  static_assert(2 * FA_NG * 128 * sizeof(float4) <= FA_PT, "partial exchange fits the P^T space");
   FaRow *rows_s = reinterpret_cast<FaRow *>(reinterpret_cast<uint8_t *>(xch) + FA_XCH);  // [3][128]
   float *x4 = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(rows_s) + FA_PF);  // [4 hh][4 quads][8]
   uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(x4) + FA_X4);
@@ -690,25 +707,35 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     auto fetch_rows = [&](const FaItem &x, int slot) {
       if (r >= x.nrows) return;
       FaRow *d = rows_s + slot * 128 + r;
-      if (x.type2) {
+      if (p.mode == 1) {  // fixup launch: every row's statistics (FA_PENDING marks the rows to redo)
+        const int orow = x.type2 ? p.ex_rows[x.q_row + r] : x.q_row + r;
+        d->orow = orow;
+        if (!x.type2) cp_async_4(&d->rf, p.rowflag + orow);
+        cp_async_8(&d->so, p.stats + static_cast<int64_t>(orow) * p.H + x.h);
+      } else if (x.type2) {
         cp_async_4(&d->orow, p.ex_rows + x.q_row + r);
       } else {
         d->orow = x.q_row + r;
         cp_async_4(&d->rf, p.rowflag + x.q_row + r);
         if (x.inc) cp_async_8(&d->so, p.stats + static_cast<int64_t>(x.q_row + r) * p.H + x.h);
+        // the contexts this item's epilogue reads (fused similarity partials): into L2 now
+        if (COS && p.cos_part && x.passP) {
+          const char *cc = reinterpret_cast<const char *>(p.C_cache + static_cast<int64_t>(x.q_row + r) * p.qw + x.h * 128);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(cc));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(cc + 128));
+        }
       }
     };
     // The softmax warps hold a queue slot until they finish its item (so the next item can be
     // read in place while the current one runs) and release it at the item's end.
     fa_wait(&wq_full[0], 0);
     int cw = wq[0].x;
-    FaItem it;
     int ii = 0;  // item count of this warp = its queue position
-    if (cw >= 0) {
-      it = wqi[0];
-      if (hh == 0) fetch_rows(it, 0);
-    }
+    if (cw >= 0 && hh == 0) fetch_rows(wqi[0], 0);
     while (cw >= 0) {
+      // the item, read in place from its queue slot (held until the item ends): no register copy
+      // of the decoded item lives across the softmax phases
+      const FaItem &it = wqi[ii & 3];
       const int w = cw;
       const int ns = (ii + 1) & 3;
       ev(4);
@@ -726,10 +753,13 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       const bool rvalid = r < it.nrows;
       // (after the item's first quad barrier) type 1 / 3 write approximate rows only (exact rows
       // belong to the type-2 items); statistics entries likewise
-      auto write_row = [&]() { return rvalid && (it.type2 || (it.passP && rp->rf != p.tag)); };
+      // fixup launch: only the rows the first launch left pending
+      auto live = [&]() { return p.mode != 1 || rp->so.y == FA_PENDING; };
+      auto write_row = [&]() { return rvalid && (it.type2 || (it.passP && rp->rf != p.tag)) && live(); };
       auto own_stats = [&]() {
-        return p.stats != nullptr && rvalid && hh == 0 && (it.type2 || p.mode == 2 || rp->rf != p.tag);
+        return p.stats != nullptr && rvalid && hh == 0 && (it.type2 || p.mode == 2 || rp->rf != p.tag) && live();
       };
+      bool rbad = false;  // this row's tile goes to the fixup launch: no output, statistics pending
       auto srow = [&]() { return static_cast<int64_t>(rp->orow) * p.H + it.h; };
       ev(it.inc ? (it.uk ? 4 : 3) : it.type2 ? 2 : 1);
       float acc[FA_CW];
@@ -1004,7 +1034,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         float Lnew = 1.f;
         bool bad = false;
         if (wact) {
-          xch[hh * 128 + r].y = part;
+          xch[hh * 128 + r].y = over ? NAN : part;  // every column group of the row sees the verdict
           fa_named_sync(1 + quad, 32 * FA_NG);
           float tot = 0.f;
 #pragma unroll
@@ -1012,9 +1042,10 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           fa_named_sync(1 + quad, 32 * FA_NG);
           const float base = so.y * ex2f(so.x - mref);
           Lnew = base + tot;
-          bad = over || !(so.y > 0.f) || !(Lnew > base * 0x1p-14f) || !(Lnew < INFINITY);
-          if (own_stats() && !bad) p.stats[srow()] = make_float2(mref, Lnew);
+          bad = !(so.y > 0.f) || !(Lnew > base * 0x1p-14f) || !(Lnew < INFINITY);
+          if (own_stats()) p.stats[srow()] = bad ? make_float2(0.f, FA_PENDING) : make_float2(mref, Lnew);
         }
+        rbad = bad;
         // a tile with a cancelled row is recomputed densely by the fixup launch (duplicates of a
         // tile id are harmless: the dense recomputation is deterministic); `over` is per column
         // group, so every warp's rows vote
@@ -1024,7 +1055,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         }
         ev(50);
         if (it.passP) {
-          fa_wait(acc_full, ai & 1);
+                    fa_wait(acc_full, ai & 1);
           ev(51);
           ++ai;
           if (wact) {
@@ -1109,7 +1140,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           ev(42);
         }
         ev(50);
-        fa_wait(acc_full, ai & 1);
+                fa_wait(acc_full, ai & 1);
         ev(51);
         ++ai;
         if (wact) {
@@ -1123,15 +1154,16 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         // row normaliser: the column groups' sums share the reference (fixed order 0, 1, ...)
         float L = 0.f;
         if (wact) {
-          xch[hh * 128 + r].y = l;
+          xch[hh * 128 + r].y = over > 100.f ? NAN : l;  // overflow risk in any column group: the row is redone
           fa_named_sync(1 + quad, 32 * FA_NG);
 #pragma unroll
           for (int g2 = 0; g2 < FA_NG; ++g2) L += xch[g2 * 128 + r].y;
           fa_named_sync(1 + quad, 32 * FA_NG);
-          if (own_stats()) p.stats[srow()] = make_float2(ref * c, L);
+          rbad = !(L > 0.f && L < INFINITY);
+          if (own_stats()) p.stats[srow()] = rbad ? make_float2(0.f, FA_PENDING) : make_float2(ref * c, L);
         }
         oscale = 1.f / L;
-        if (__ballot_sync(0xffffffffu, rvalid && over > 100.f) != 0u && lane == 0) {
+        if (__ballot_sync(0xffffffffu, rvalid && rbad) != 0u && lane == 0) {
           const int pos = atomicAdd(&p.fix[0], 1);
           if (pos < p.fix_cap) p.fix[1 + pos] = w;
         }
@@ -1257,7 +1289,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           ev(42);
         }
         ev(50);
-        fa_wait(acc_full, ai & 1);
+                fa_wait(acc_full, ai & 1);
         ev(51);
         ++ai;
         if (wact) {
@@ -1279,20 +1311,17 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       // rows x 16 bytes.
       static_assert(FA_CW == 32, "epilogue transpose assumes 4 chunks of 8 head dims per warp");
       {
-        const unsigned wmask = (DYLLM_FA_T4 && it.t4) ? 0u : __ballot_sync(0xffffffffu, write_row());
-        if (wmask) {
-          uint4 ch[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            float o[8];
-#pragma unroll
-            for (int t = 0; t < 8; ++t) o[t] = acc[u * 8 + t] * oscale;
-            ch[u] = pack8(o);
-          }
-          auto shfl4 = [](uint4 v, int m) {
-            return make_uint4(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m),
-                              __shfl_xor_sync(0xffffffffu, v.z, m), __shfl_xor_sync(0xffffffffu, v.w, m));
-          };
+        const bool wr = write_row() && !rbad;
+        const unsigned wmask = (DYLLM_FA_T4 && it.t4) ? 0u : __ballot_sync(0xffffffffu, wr);
+        const bool fuse = COS && p.cos_part != nullptr && wact;
+        auto shfl4 = [](uint4 v, int m) {
+          return make_uint4(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m),
+                            __shfl_xor_sync(0xffffffffu, v.z, m), __shfl_xor_sync(0xffffffffu, v.w, m));
+        };
+        // store 4 chunks of this thread's row slice: a 4 x 4 transpose of 16-byte chunks inside each
+        // group of 4 lanes (two xor-shuffle rounds) leaves lane c of group m holding chunk c of rows
+        // 4m .. 4m+3, so each store instruction writes 8 rows x 64 contiguous bytes
+        auto store_rows = [&](uint4 ch[4]) {
           const bool b0 = lane & 1, b1 = lane & 2;
 #pragma unroll
           for (int a = 0; a < 4; a += 2) {  // round 1: chunk pairs (0,1), (2,3) with lane ^ 1
@@ -1314,10 +1343,100 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
               *reinterpret_cast<uint4 *>(p.C_out + static_cast<int64_t>(orr) * p.qw + it.h * 128 + hh * FA_CW +
                                          (lane & 3) * 8) = ch[k];
           }
+        };
+        if (fuse) {
+          // ---- fused similarity partials, in the transposed layout (lane: 8 head dims
+          // of rows g4..g4+3, coalesced): C_new = C_old + dC rounded as stored (approximate rows) or
+          // C (exact rows); partial sums over the dims, then over the 4 lanes of each row, then over
+          // the row's four column groups (fixed orders); C_new committed to the C cache (Alg. 3
+          // line 16) by the kernel that forms it
+          uint4 ch[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            float o[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) o[t] = acc[u * 8 + t] * oscale;
+            ch[u] = pack8(o);
+          }
+          const bool b0 = lane & 1, b1 = lane & 2;
+#pragma unroll
+          for (int a = 0; a < 4; a += 2) {
+            const uint4 rv = shfl4(b0 ? ch[a] : ch[a + 1], 1);
+            if (b0) ch[a] = rv; else ch[a + 1] = rv;
+          }
+#pragma unroll
+          for (int a = 0; a < 2; ++a) {
+            const uint4 rv = shfl4(b1 ? ch[a] : ch[a + 2], 2);
+            if (b1) ch[a] = rv; else ch[a + 2] = rv;
+          }
+          const int orow_l = rvalid ? rp->orow : 0;
+          const int g4 = lane & ~3;
+          float pd[4], pa[4], pb[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int src = g4 | k;
+            const int orr = __shfl_sync(0xffffffffu, orow_l, src);
+            pd[k] = pa[k] = pb[k] = 0.f;
+            if ((wmask >> src) & 1u) {
+              uint4 *cp = reinterpret_cast<uint4 *>(p.C_out + static_cast<int64_t>(orr) * p.qw + it.h * 128 +
+                                                    hh * FA_CW + (lane & 3) * 8);
+              float o[8], b8[8];
+              unpack8(*cp, b8);
+              unpack8(ch[k], o);
+              if (!it.type2) {
+#pragma unroll
+                for (int t = 0; t < 8; ++t) o[t] += b8[t];
+                ch[k] = pack8(o);
+                unpack8(ch[k], o);
+              }
+#pragma unroll
+              for (int t = 0; t < 8; ++t) {
+                pd[k] = fmaf(o[t], b8[t], pd[k]);
+                pa[k] = fmaf(o[t], o[t], pa[k]);
+                pb[k] = fmaf(b8[t], b8[t], pb[k]);
+              }
+              *cp = ch[k];
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+#pragma unroll
+            for (int o = 1; o <= 2; o <<= 1) {
+              pd[k] += __shfl_xor_sync(0xffffffffu, pd[k], o);
+              pa[k] += __shfl_xor_sync(0xffffffffu, pa[k], o);
+              pb[k] += __shfl_xor_sync(0xffffffffu, pb[k], o);
+            }
+          }
+          const int mk = lane & 3;  // this lane's own row (row layout) is g4 | mk
+          float4 *cx = cpx + (ii & 1) * (FA_NG * 128);
+          cx[hh * 128 + r] = make_float4(mk == 0 ? pd[0] : mk == 1 ? pd[1] : mk == 2 ? pd[2] : pd[3],
+                                         mk == 0 ? pa[0] : mk == 1 ? pa[1] : mk == 2 ? pa[2] : pa[3],
+                                         mk == 0 ? pb[0] : mk == 1 ? pb[1] : mk == 2 ? pb[2] : pb[3], 0.f);
+          fa_named_sync(1 + quad, 32 * FA_NG);
+          if (hh == 0 && wr) {
+            float4 t = cx[r];
+#pragma unroll
+            for (int g2 = 1; g2 < FA_NG; ++g2) {
+              const float4 q = cx[g2 * 128 + r];
+              t.x += q.x;
+              t.y += q.y;
+              t.z += q.z;
+            }
+            p.cos_part[static_cast<int64_t>(rp->orow) * p.H + it.h] = t;
+          }
+        } else if (wmask) {
+          uint4 ch[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            float o[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) o[t] = acc[u * 8 + t] * oscale;
+            ch[u] = pack8(o);
+          }
+          store_rows(ch);
         }
       }
       ev(52);
-      if (nw >= 0) it = wqi[ns];
       __syncwarp();
       if (lane == 0) mbar_arrive(&wq_empty[ii & 3]);
       cw = nw;
@@ -1347,7 +1466,8 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
 int attention_fused_launch(const AttnArgs &a, cudaStream_t st) {
   static DeviceOnce attr;
   if (attr.todo()) {
-    DY_CUDA(cudaFuncSetAttribute(attn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_SMEM));
+    DY_CUDA(cudaFuncSetAttribute(attn_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_SMEM));
+    DY_CUDA(cudaFuncSetAttribute(attn_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_SMEM));
     attr.done();
   }
   const int rows_total = a.batch * a.N;
@@ -1378,6 +1498,7 @@ int attention_fused_launch(const AttnArgs &a, cudaStream_t st) {
   p.MT = a.full_only ? 0 : split ? p.MTp + (a.N - a.resp_lo + 127) / 128 : (p.L + 127) / 128;
   p.pinc = pinc ? 1 : 0;
   p.ucnt = a.ucnt;
+  p.cos_part = a.full_only || a.mode == 2 ? nullptr : a.cos_part;
   p.XT = (a.max_rows_per_seq + 127) / 128;
   p.items = a.batch * a.H * (p.MT + p.XT);
   p.qw = qw;
@@ -1408,8 +1529,8 @@ int attention_fused_launch(const AttnArgs &a, cudaStream_t st) {
   if (p.items <= 0) return DYLLM_OK;
   // fixup launch: a few CTAs claim the (rare, device-counted) listed tiles
   const int grid = p.mode == 1 ? 16 : (p.items < a.num_sms ? p.items : a.num_sms);
-  DY_CUDA(launch_k(attn_fused_kernel, dim3(grid), dim3(FA_THREADS), FA_SMEM, st, 1, tq, tqx, tk, tv, tkx, tdv, tkxo,
-                   tkun, tkuo, p));
+  DY_CUDA(launch_k(p.cos_part ? attn_fused_kernel<true> : attn_fused_kernel<false>, dim3(grid), dim3(FA_THREADS),
+                   FA_SMEM, st, 1, tq, tqx, tk, tv, tkx, tdv, tkxo, tkun, tkuo, p));
   DY_CUDA(cudaGetLastError());
   return DYLLM_OK;
 }

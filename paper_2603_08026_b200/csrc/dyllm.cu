@@ -97,6 +97,10 @@ static constexpr int64_t kMaskCap = 1 << 20;
 static constexpr int kFixCap = 1 << 16;
 static bool g_attn_inc_enabled = true;   // test hook: incremental attention statistics (response tiles)
 static bool g_attn_pinc_enabled = true;  // test hook: incremental prompt statistics in full-input steps
+// fused similarity partials in the attention epilogue: built and parity-tested, off by
+// default — same-box A/B (tools/gpu_r2_cos.sh): attention 141 -> 178 us per launch (the C_old read
+// lands on each item's serial chain), selection 48 -> 26 us: 716 vs 724 tok/s
+static bool g_attn_fuse_cos = false;
 
 struct LayerW {
   bf16 *g_attn, *wqkv, *bqkv, *wo, *g_ffn, *wgu, *wd;
@@ -139,6 +143,7 @@ struct dyllm_cache {
   int *qx_rows, *qx_off;  // layer1_policy 0: decoded rows outside idx_in (Q-only refresh, D6)
   int *urows = nullptr, *ucnt = nullptr;  // changed-key lists U of a full-input step ([b][N], [b])
   bf16 *Kun = nullptr, *Kuo = nullptr;    // their keys now / at the statistics epoch (compact per sequence)
+  float4 *cos_part = nullptr;             // [rows][H] similarity partials of the fused attention epilogue
   int32_t *tr_lists = nullptr, *tr_offs = nullptr;  // dyllm_cache_set_trace (caller-owned)
   float *tr_sims = nullptr;
   float *sim;  // per-row similarity scratch (fraction mode)
@@ -467,6 +472,7 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
     AL(c->ucnt, r->batch);
     AL(c->Kun, rows * kw);
     AL(c->Kuo, rows * kw);
+    AL(c->cos_part, rows * m.n_heads);
   }
   ALE(c->H0, rows * d);
   ALE(c->Xn, rows * d);
@@ -839,7 +845,11 @@ static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *
   a.V = C.V;
   a.dV = c->dV;
   a.C_cache = C.C;
-  a.C_out = c->Cn;
+  // fused kernel: the epilogue commits C_new into the C cache itself and leaves the similarity
+  // partials; other head dims write C_new (exact) / dC (approximate) rows to Cn
+  const bool fuse_cos = fused && g_attn_fuse_cos;
+  a.C_out = fuse_cos ? C.C : c->Cn;
+  a.cos_part = fuse_cos ? c->cos_part : nullptr;
   a.ex_rows = idx_in;
   a.ex_off = off_in;
   a.ap_rows = c->ap_rows;
@@ -884,7 +894,8 @@ static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *
   const bool delta = attention_writes_delta(m.head_dim);  // fused kernel: Cn = dC for approximate rows
   KL(SELECT, launch_select(c->Cn, C.C, b, N, row_lo, qw, fmode ? 2.f : tau, c->r.cmp, fmode ? tau : -1.f, idx_out,
                            off_out, (fmode && !sim) ? c->sim : sim, ctx->masks, ctx->ticket, counts,
-                           delta ? c->rowflag : nullptr, tag, delta ? off_in : nullptr, st));
+                           delta ? c->rowflag : nullptr, tag, (delta || fuse_cos) ? off_in : nullptr, st,
+                           fuse_cos ? c->cos_part : nullptr, m.n_heads));
   const int *M_out = off_out + b;
   // a6 + a7 on idx_out, a8 scatter-back into H_l (other rows keep FFN_OUT_cache)
   KL(GATHER, launch_gather_rows(C.C, idx_out, M_out, rows, c->Cg, qw, st));
@@ -1096,6 +1107,16 @@ int dyllm_set_option(int option, int value) {
   if (option == DYLLM_OPT_ATTN_PINC) {
     const int prev = g_attn_pinc_enabled ? 1 : 0;
     g_attn_pinc_enabled = value != 0;
+    return prev;
+  }
+  if (option == DYLLM_OPT_SKINNY_CHUNK) {
+    const int prev = g_skinny_chunk_rows;
+    g_skinny_chunk_rows = value < 0 ? 0 : value;
+    return prev;
+  }
+  if (option == DYLLM_OPT_ATTN_COS) {
+    const int prev = g_attn_fuse_cos ? 1 : 0;
+    g_attn_fuse_cos = value != 0;
     return prev;
   }
   if (option == DYLLM_OPT_ATTN_T4) {

@@ -122,6 +122,7 @@ struct SkinnyParams {
   int S_force; // test hook: split units per tile (0 = automatic)
   int one_chunk_max;  // largest M kept in ONE activation chunk (two MMAs per k-step above 256
                       // rows, single-buffered accumulator); above: chunks of <= 256 rows
+  int chunk_rows;     // test hook: largest rows per activation chunk when chunked (0: 256)
 };
 
 // Stream-K partition of the (item, k-block) space: pair p owns units [start(p), start(p+1)).
@@ -251,7 +252,8 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   const int nwb = p.N / 256;
   const bool one = p.one_chunk_max >= 0 ? M <= p.one_chunk_max
                                         : (M <= 256 || (M <= 512 && 2 * nwb >= p.P_max && nwb < p.P_max));
-  const int nchunk = one ? 1 : (M + 255) / 256;
+  const int crow = p.chunk_rows > 0 ? min(p.chunk_rows, 256) : 256;
+  const int nchunk = one ? 1 : (M + crow - 1) / crow;
   const int R = nchunk == 1 ? M : (((M + nchunk - 1) / nchunk + 31) & ~31);
   const int items = p.N / 256 * nchunk;
   const int num_kb = p.K / SK_KB;
@@ -660,7 +662,7 @@ static int launch_skinny_t(const GemmCall &g, int num_sms, cudaStream_t st) {
   // count: the kernel derives them; the grid is every co-resident pair
   SkinnyParams p{g.M_ptr, g.M_cap, g.N, g.K, g.D, g.ldd, g.resid, g.ldr, g.resid_rows, g.bias, g.out_rows, g.ws, g.ctr,
                  max_pairs,
-                 g_skinny_trace, g_skinny_split, g_skinny_one_chunk > 0 ? g_skinny_one_chunk : -1};
+                 g_skinny_trace, g_skinny_split, g_skinny_one_chunk > 0 ? g_skinny_one_chunk : -1, g_skinny_chunk_rows};
   DY_CUDA(launch_k(kern, dim3(2 * max_pairs), dim3(SK_THREADS), SK_SMEM, st, 2, maps, p));
   return DYLLM_OK;
 }
@@ -668,6 +670,7 @@ static int launch_skinny_t(const GemmCall &g, int num_sms, cudaStream_t st) {
 unsigned long long *g_skinny_trace = nullptr;
 int g_skinny_split = 0;
 int g_skinny_one_chunk = 0;  // 0: automatic
+int g_skinny_chunk_rows = 0;  // 0: 256
 
 bool skinny_eligible(const GemmCall &g) {
   return g.N % 256 == 0 && g.K % SK_KB == 0 && (g.epi == EPI_BF16 || g.epi == EPI_RESID || g.epi == EPI_SWIGLU);

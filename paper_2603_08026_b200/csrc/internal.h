@@ -101,6 +101,7 @@ inline int64_t skinny_ws_floats(int num_sms) { return static_cast<int64_t>(num_s
 extern bool g_skinny_enabled;  // test hook (dyllm_set_option)
 extern unsigned long long *g_skinny_trace;
 extern int g_skinny_split;
+extern int g_skinny_chunk_rows;  // test hook: largest rows per activation chunk (dyllm_set_option)
 extern int g_skinny_one_chunk;  // test hook: largest M in one activation chunk (dyllm_set_option)  // test hook: units per weight block (0 = auto)  // debug hook (dyllm_debug_trace_buffer)
 int gemm_skinny_launch(const GemmCall &g, int num_sms, cudaStream_t st);  // gemm_skinny.cu
 
@@ -141,6 +142,8 @@ struct AttnArgs {
   const bf16 *Kun = nullptr, *Kuo = nullptr;
   const int *ucnt = nullptr;
   bool pinc = false;
+  // fused similarity partials (fused kernel, sparse steps): C_out must be C_cache
+  float4 *cos_part = nullptr;     // [b*N][H] (dot, |C_new|^2, |C_old|^2, -)
 };
 int attention_launch(const AttnArgs &a, cudaStream_t st);
 int attention_fused_launch(const AttnArgs &a, cudaStream_t st);  // attn_fused.cu

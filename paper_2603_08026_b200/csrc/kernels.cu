@@ -392,9 +392,11 @@ __global__ void build_list_kernel(int mode, const int *__restrict__ carried, con
 // Changed-key list U of each sequence for the incremental prompt statistics of a full-input step
 // (SURVEY §8f1): its idx_in rows in list order (their new keys are the salient keys of the P pass),
 // then the other rows whose key was written since the layer's statistics epoch began (ascending).
-// One CTA per sequence; row ids at urows[s*N ..), count ucnt[s]; the first kUcap entries' keys
-// are gathered compact: Kun = current K, Kuo = the key at the epoch start (Kfi).
+// Grid (batch, kUgrp): every CTA of a sequence derives the same list (a pass over its N row tags),
+// keeps the first kUcap entries in shared memory, and gathers every kUgrp-th of their keys
+// compact: Kun = current K, Kuo = the key at the epoch start (Kfi); CTA 0 records the count.
 constexpr int kUcap = 256;  // two key tiles: larger lists take the dense path
+constexpr int kUgrp = 16;
 __global__ void build_u_kernel(const int *__restrict__ idx_in, const int *__restrict__ off_in,
                                const uint32_t *__restrict__ rowflag, uint32_t tag, const uint32_t *__restrict__ dtag,
                                uint32_t epoch, const bf16 *__restrict__ K, const bf16 *__restrict__ Kfi, int N, int kw,
@@ -402,12 +404,11 @@ __global__ void build_u_kernel(const int *__restrict__ idx_in, const int *__rest
                                int *__restrict__ ucnt) {
   pdl_wait();
   __shared__ int warp_cnt[32];
-  __shared__ int total;
+  __shared__ int u[kUcap];
   const int s = blockIdx.x;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
   const int b0 = off_in[s], e = off_in[s + 1] - b0;
-  int *u = urows + static_cast<int64_t>(s) * N;
-  for (int j = threadIdx.x; j < e; j += blockDim.x) u[j] = idx_in[b0 + j];
+  for (int j = threadIdx.x; j < e && j < kUcap; j += blockDim.x) u[j] = idx_in[b0 + j];
   int base = e;
   for (int p0 = 0; p0 < N; p0 += blockDim.x) {
     const int p = p0 + threadIdx.x;
@@ -421,24 +422,22 @@ __global__ void build_u_kernel(const int *__restrict__ idx_in, const int *__rest
       before += (w < warp) ? warp_cnt[w] : 0;
       tot += warp_cnt[w];
     }
-    if (keep) u[base + before + __popc(m & ((1u << lane) - 1))] = static_cast<int>(r);
+    const int pos = base + before + __popc(m & ((1u << lane) - 1));
+    if (keep && pos < kUcap) u[pos] = static_cast<int>(r);
     base += tot;
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    ucnt[s] = base;
-    total = base;
-  }
-  __syncthreads();
-  const int n = min(total, kUcap), nv = kw / 8;
-  for (int i = warp; i < n; i += nw) {
+  if (blockIdx.y == 0 && threadIdx.x == 0) ucnt[s] = base;
+  const int n = min(base, kUcap), nv = kw / 8;
+  for (int i = blockIdx.y * nw + warp; i < n; i += gridDim.y * nw) {
     const int64_t r = u[i];
+    if (blockIdx.y == 0 && lane == 0) urows[static_cast<int64_t>(s) * N + i] = static_cast<int>(r);
     const uint4 *kn = reinterpret_cast<const uint4 *>(K + r * kw);
     const uint4 *ko = reinterpret_cast<const uint4 *>(Kfi + r * kw);
     uint4 *dn = reinterpret_cast<uint4 *>(Kun + (static_cast<int64_t>(s) * N + i) * kw);
     uint4 *dd = reinterpret_cast<uint4 *>(Kuo + (static_cast<int64_t>(s) * N + i) * kw);
     for (int c = lane; c < nv; c += 32) {
-      const uint4 a = kn[c], b = ko[c];
+      const uint4 a = ld_nc_v4(kn + c), b = ld_nc_v4(ko + c);
       dn[c] = a;
       dd[c] = b;
     }
@@ -460,7 +459,8 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
     const bf16 *__restrict__ c_new, bf16 *__restrict__ c_cache, int N, int row_lo, int width, float tau,
     int cmp, float frac, int *__restrict__ idx_out, int *__restrict__ off_out, float *__restrict__ sim_out,
     unsigned *__restrict__ masks, unsigned *__restrict__ ticket, int *__restrict__ counts_out,
-    const uint32_t *__restrict__ rowflag, uint32_t tag, const int *__restrict__ dl_off) {
+    const uint32_t *__restrict__ rowflag, uint32_t tag, const int *__restrict__ dl_off,
+    const float4 *__restrict__ cos_part, int H) {
   pdl_wait();
   __shared__ unsigned row_flag[kSelRowsPerCta];
   __shared__ bool is_last;
@@ -474,7 +474,28 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
     const int rr = warp;  // one row per warp (32 warps = the CTA's 32 rows)
     const int p = row_lo + chunk * kSelRowsPerCta + rr;
     unsigned f = 0;
-    if (p < N) {
+    if (p < N && cos_part) {
+      // partials mode: the attention epilogue formed C_new, committed it and left per
+      // (row, head) partial sums; a sequence without salient keys kept every context (s = 1, D9)
+      const int64_t r = static_cast<int64_t>(s) * N + p;
+      float sim = 1.f;
+      if (dl_off[s + 1] > dl_off[s]) {
+        float dot = 0.f, na = 0.f, nb = 0.f;
+        for (int h = lane; h < H; h += 32) {
+          const float4 v = __ldcg(cos_part + r * H + h);
+          dot += v.x;
+          na += v.y;
+          nb += v.z;
+        }
+        dot = warp_sum(dot);
+        na = warp_sum(na);
+        nb = warp_sum(nb);
+        const bool za = na < 1e-24f, zb = nb < 1e-24f;  // D9 zero-norm policy
+        sim = (za && zb) ? 1.f : (za || zb) ? 0.f : dot / sqrtf(na * nb);
+      }
+      f = cmp ? (sim <= tau) : (sim < tau);
+      if (sim_out && lane == 0) sim_out[r] = sim;
+    } else if (p < N) {
       const int64_t r = static_cast<int64_t>(s) * N + p;
       const uint4 *a = reinterpret_cast<const uint4 *>(c_new + r * width);
       uint4 *b = reinterpret_cast<uint4 *>(c_cache + r * width);
@@ -938,7 +959,7 @@ void launch_qkv_post(const bf16 *qkv, const int *idx, const int *M_ptr, int M_ca
 void launch_build_u(const int *idx_in, const int *off_in, const uint32_t *rowflag, uint32_t tag, const uint32_t *dtag,
                     uint32_t epoch, const bf16 *K, const bf16 *Kfi, int batch, int N, int kw, int *urows, bf16 *Kun,
                     bf16 *Kuo, int *ucnt, cudaStream_t st) {
-  DY_CUDA_LAUNCH(launch_k(build_u_kernel, dim3(batch), dim3(512), 0, st, 1, idx_in, off_in, rowflag, tag, dtag, epoch, K,
+  DY_CUDA_LAUNCH(launch_k(build_u_kernel, dim3(batch, kUgrp), dim3(256), 0, st, 1, idx_in, off_in, rowflag, tag, dtag, epoch, K,
                           Kfi, N, kw, urows, Kun, Kuo, ucnt));
 }
 void launch_rope_table(float2 *cs, int N, int hd, double theta, cudaStream_t st) {
@@ -955,11 +976,12 @@ void launch_build_list(int mode, const int *carried, const int *carried_off, con
 }
 void launch_select(const bf16 *c_new, bf16 *c_cache, int batch, int N, int row_lo, int width, float tau, int cmp,
                    float frac, int *idx_out, int *off_out, float *sim_out, unsigned *masks, unsigned *ticket,
-                   int *counts, const uint32_t *rowflag, uint32_t tag, const int *dl_off, cudaStream_t st) {
+                   int *counts, const uint32_t *rowflag, uint32_t tag, const int *dl_off, cudaStream_t st,
+                   const float4 *cos_part, int H) {
   const int L = N - row_lo;
   dim3 grid((L + kSelRowsPerCta - 1) / kSelRowsPerCta, batch);
   DY_CUDA_LAUNCH(launch_k(select_salient_kernel, dim3(grid), dim3(kSelThreads), 0, st, 1, c_new, c_cache, N, row_lo, width, tau, cmp, frac, idx_out, off_out,
-                                              sim_out, masks, ticket, counts, rowflag, tag, dl_off));
+                                              sim_out, masks, ticket, counts, rowflag, tag, dl_off, cos_part, H));
 }
 void launch_lm_candidates(const int *tokens, int batch, int L_P, int L_R, int block, int mask_id, int *rows, int *off,
                           cudaStream_t st) {

@@ -32,7 +32,8 @@ void launch_build_list(int mode, const int *carried, const int *carried_off, con
                        int batch, int N, int row_lo, int resp_lo, int *out, int *out_off, cudaStream_t st);
 void launch_select(const bf16 *c_new, bf16 *c_cache, int batch, int N, int row_lo, int width, float tau, int cmp,
                    float frac, int *idx_out, int *off_out, float *sim_out, unsigned *masks, unsigned *ticket,
-                   int *counts, const uint32_t *rowflag, uint32_t tag, const int *dl_off, cudaStream_t st);
+                   int *counts, const uint32_t *rowflag, uint32_t tag, const int *dl_off, cudaStream_t st,
+                   const float4 *cos_part = nullptr, int H = 0);
 void launch_lm_candidates(const int *tokens, int batch, int L_P, int L_R, int block, int mask_id, int *rows, int *off,
                           cudaStream_t st);
 void launch_lm_select_commit(const float4 *partials, int n_tiles, const int *rows, const int *off, int batch, int n_u,

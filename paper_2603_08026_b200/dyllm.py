@@ -104,7 +104,7 @@ def lib():
 
 
 OPT_SKINNY_GEMM, OPT_SKINNY_SPLIT, OPT_ATTN_FUSED, OPT_SKINNY_ONE_CHUNK, OPT_PDL, OPT_ATTN_INC, OPT_ATTN_T4 = 1, 2, 3, 4, 5, 6, 7
-OPT_ATTN_PINC = 8
+OPT_ATTN_PINC, OPT_ATTN_COS, OPT_SKINNY_CHUNK = 8, 9, 10
 
 
 def set_option(option: int, value: int) -> int:

@@ -251,3 +251,15 @@ def test_denoise_empty_layer1_list_in_batch():
     """Fixed-tau mode, literal policy: sequence 1 enters a sparse step with an empty idx_in while
     sequence 0 does not (nothing recomputed for it, its caches stay)."""
     _denoise_parity("small128", 0, 0, empty_seq_at=6)
+
+
+@pytest.mark.parametrize("select_mode", [0, 1])
+def test_denoise_fused_similarity_partials(select_mode):
+    """SURVEY §8f3 variant (DYLLM_OPT_ATTN_COS = 1): C_new, its commit and the cosine partials in the
+    attention epilogue; the selection kernel only sums the partials over the heads."""
+    from paper_2603_08026_b200 import dyllm as dy
+    prev = dy.set_option(dy.OPT_ATTN_COS, 1)
+    try:
+        _denoise_parity("small128", select_mode, 1)
+    finally:
+        dy.set_option(dy.OPT_ATTN_COS, prev)

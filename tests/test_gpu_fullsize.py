@@ -95,6 +95,18 @@ def test_layer_step_full_size_sampled_untransposed(big):
         dy.set_option(dy.OPT_ATTN_T4, prev)
 
 
+@pytest.mark.parametrize("mode", ["ro", "fi"])
+def test_layer_step_full_size_fused_similarity(big, mode):
+    """SURVEY §8f3 variant (DYLLM_OPT_ATTN_COS = 1): the attention epilogue forms C_new, commits it
+    and leaves the cosine partials that the selection kernel sums over heads."""
+    dy = big[0]
+    prev = dy.set_option(dy.OPT_ATTN_COS, 1)
+    try:
+        _check_full_size(big, mode, 0.10)
+    finally:
+        dy.set_option(dy.OPT_ATTN_COS, prev)
+
+
 @pytest.mark.parametrize("mode,frac_in", [("ro", 0.06), ("fi", 0.06)])
 def test_layer_step_full_size_sampled_dream(big_dream, mode, frac_in):
     """Dream-7B layer shape (GQA 28 q / 4 kv heads, QKV bias, FFN 18944), L_P 160 + L_R 512."""

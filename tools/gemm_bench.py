@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--split", default="0", help="comma list of skinny split granularities (0 = auto)")
     ap.add_argument("--which", default="qkv,o,gu,down")
     ap.add_argument("--one-chunk", type=int, default=0, help="largest M in one activation chunk (0 auto)")
+    ap.add_argument("--chunk", default="0", help="comma list of largest rows per activation chunk (0 = 256)")
     a = ap.parse_args()
     cfg, _ = configs.preset(a.config)
     d, F = cfg.d_model, cfg.d_ff
@@ -44,8 +45,10 @@ def main():
         W = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
         A = torch.randn(cap, K, device="cuda").bfloat16()
         D = torch.empty(cap, N, device="cuda").bfloat16()
-        for M, S in [(int(x), int(y)) for x in a.rows.split(",") for y in a.split.split(",")]:
+        for M, S, CR in [(int(x), int(y), int(z)) for x in a.rows.split(",") for y in a.split.split(",")
+                         for z in a.chunk.split(",")]:
             dy.set_option(dy.OPT_SKINNY_SPLIT, S)
+            dy.set_option(dy.OPT_SKINNY_CHUNK, CR)
             Md = torch.tensor([M], dtype=torch.int32, device="cuda")
             for _ in range(3):
                 ctx.gemm_bf16(A, W, D, M_dev=Md)
@@ -58,7 +61,7 @@ def main():
             ctx.profile(False)
             tf = 2.0 * M * N * K / us / 1e6
             gbs = 2.0 * N * K / us / 1e3
-            print(f"{name:5s} N={N:6d} K={K:6d} M={M:5d} S={S:3d}: {us:8.2f} us  {tf:7.1f} TFLOP/s  weights {gbs:7.1f} GB/s")
+            print(f"{name:5s} N={N:6d} K={K:6d} M={M:5d} S={S:3d} C={CR:3d}: {us:8.2f} us  {tf:7.1f} TFLOP/s  weights {gbs:7.1f} GB/s")
 
 
 if __name__ == "__main__":
