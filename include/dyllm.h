@@ -47,6 +47,7 @@ enum {
 typedef struct dyllm_ctx dyllm_ctx;
 typedef struct dyllm_weights dyllm_weights;
 typedef struct dyllm_cache dyllm_cache;
+typedef struct dyllm_tp dyllm_tp;
 
 /* Model shape (LLaDA / Dream style transformer, BASELINE.json configs).
  * Constraints: d_model % 64 == 0, head_dim in {16, 32, 64, 128}, n_heads % n_kv_heads == 0,
@@ -217,6 +218,40 @@ int dyllm_select_salient(dyllm_ctx *ctx, int batch, int N, int row_lo, int width
  * K % 64 == 0, N % 8 == 0. Asynchronous. */
 int dyllm_gemm_bf16(dyllm_ctx *ctx, const int32_t *d_M, int M_cap, int N, int K, const void *d_A,
                     const void *d_W, void *d_D, const void *d_resid, const void *d_bias);
+
+/* ------------------------------------------------------------------ tensor parallelism */
+/* Megatron-style tensor parallelism over attention heads and FFN channels. Shard g of a group of
+ * `world` holds heads [g*H/world, (g+1)*H/world) (query and kv heads, so n_heads and n_kv_heads must
+ * both divide by world) and FFN channels [g*F/world, ...): its weights are a dyllm_weights built
+ * for the LOCAL model cfg (n_heads/world, n_kv_heads/world, d_ff/world; wq/wk/wv/bias rows and wo
+ * columns of its heads, gate/up rows and down columns of its channels; embeddings, gains and the
+ * LM head whole), its K/V/Q/C caches hold its heads, and hidden states H_l are replicated. Per
+ * sparse layer three all-reduces (sums over the shards in shard order): the per-row similarity
+ * partials (<C_new, C_old>, |C_new|^2, |C_old|^2 over the shard's heads; every shard thresholds the
+ * same sums, so the salient lists agree), the O projection (shard 0 adds the residual)
+ * and the FFN down projection (shard 0 adds h), whose rows are then scattered into H_l.
+ * Two backends:
+ *  - loopback (nccl_unique_id == NULL): the group's `world` shards live in THIS process on the
+ *    ctx's device and run one after another; the all-reduce is one kernel over the shards'
+ *    buffers (row counts read on the device, no host synchronisation). This is the one-device
+ *    test harness of the TP math.
+ *  - NCCL (one process per GPU, `rank` of `world`): ncclAllReduce on the ctx stream; the row count
+ *    of a device-side list is read back before each hidden-state all-reduce (one synchronisation
+ *    per collective). NCCL is loaded at run time (dlopen "libnccl.so.2"); DYLLM_E_NCCL if absent.
+ * bf16 (dtype 0) only. */
+int dyllm_tp_unique_id(void *h_out, int n_bytes);  /* NCCL unique id (n_bytes >= 128); synchronous */
+int dyllm_tp_create(dyllm_ctx *ctx, int world, int rank, const void *nccl_unique_id, dyllm_tp **out);
+/* Register cache `c` (created from shard `shard`'s weights) as that shard (loopback: every shard
+ * in [0, world); NCCL: shard == rank). Shapes are checked against the group. */
+int dyllm_tp_attach(dyllm_tp *tp, int shard, dyllm_cache *c);
+/* FullStep (Alg. 2) on every local shard; w[i] = weights of the i-th attached local shard. */
+int dyllm_tp_cache_init(dyllm_tp *tp, const dyllm_weights *const *w, const int32_t *d_tokens);
+/* dyllm_denoise_step over the group (same arguments; d_sal_counts nullable). Loopback: the
+ * caller's d_tokens / d_dec_pos / d_dec_tok belong to shard 0; the other shards decide on private
+ * copies of the same tokens (identical decisions: H_L is bit-identical on every shard). */
+int dyllm_tp_denoise_step(dyllm_tp *tp, const dyllm_weights *const *w, int t, const float *h_tau,
+                          int32_t *d_tokens, int32_t *d_dec_pos, int32_t *d_dec_tok, int32_t *d_sal_counts);
+void dyllm_tp_destroy(dyllm_tp *tp);
 
 /* ------------------------------------------------------------------ instrumentation */
 /* Kernel classes timed by the profiler (CUDA events on the ctx stream around each launch). */

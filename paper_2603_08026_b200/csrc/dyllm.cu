@@ -2,7 +2,9 @@
 // FullStep (Alg. 2), the per-layer SparseStep (Alg. 3 with Alg. 4 folded into the attention
 // kernel), the denoise step (Alg. 1 body) and the unmasking rule. No host synchronisation
 // inside a step: every kernel reads its row counts from device memory.
+#include <dlfcn.h>
 #include <math.h>
+#include <nccl.h>
 
 #include <atomic>
 #include <cstring>
@@ -144,6 +146,11 @@ struct dyllm_cache {
   int *urows = nullptr, *ucnt = nullptr;  // changed-key lists U of a full-input step ([b][N], [b])
   bf16 *Kun = nullptr, *Kuo = nullptr;    // their keys now / at the statistics epoch (compact per sequence)
   float4 *cos_part = nullptr;             // [rows][H] similarity partials of the fused attention epilogue
+  // tensor parallelism: this cache is shard tp_shard of a group (local heads / FFN)
+  dyllm_tp *tp = nullptr;
+  int tp_shard = 0;
+  float4 *tp_part = nullptr;              // [rows] this shard's similarity partial sums, then the group's
+  int32_t *tp_tokens = nullptr;           // loopback shards > 0: private copy of the step's tokens
   int32_t *tr_lists = nullptr, *tr_offs = nullptr;  // dyllm_cache_set_trace (caller-owned)
   float *tr_sims = nullptr;
   float *sim;  // per-row similarity scratch (fraction mode)
@@ -731,17 +738,14 @@ static int layer_step_f32(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c
 }
 
 // FullStep (Alg. 2): every row of every sequence, all caches rewritten.
-static int full_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, const int *d_tokens) {
-  if (c->m.dtype == 1) return full_step_f32(ctx, w, c, d_tokens);
+// FullStep layer, phase 1 (Alg. 2 lines 3-5): every row's Q/K/V and exact context
+static int full_attn_phase(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int l) {
   const dyllm_model_cfg &m = c->m;
   const int d = m.d_model, qw = m.n_heads * m.head_dim, kw = m.n_kv_heads * m.head_dim, rows = c->rows;
   cudaStream_t st = ctx->stream;
-  ctx->cls_offset = DYLLM_KC_FULL;
-  KL(OTHER, launch_embed_rows(d_tokens, nullptr, nullptr, rows, w->emb, c->H0, d, st));
-  for (int l = 0; l < m.n_layers; ++l) {
-    const LayerW &L = w->L[l];
-    LayerC &C = c->L[l];
-    const bf16 *Hprev = l == 0 ? c->H0 : c->L[l - 1].H;
+  const LayerW &L = w->L[l];
+  LayerC &C = c->L[l];
+  const bf16 *Hprev = l == 0 ? c->H0 : c->L[l - 1].H;
     KL(GATHER, launch_gather_rmsnorm(Hprev, nullptr, nullptr, rows, L.g_attn, m.rms_eps, c->Xn, d, st));
     KL(QKV_GEMM, RET(gemm(ctx, nullptr, rows, qw + 2 * kw, d, c->Xn, L.wqkv, c->qkv, qw + 2 * kw, EPI_BF16)));
     KL(QKV_POST, launch_qkv_post(c->qkv, nullptr, nullptr, rows, L.bqkv, c->N, m.n_heads, m.n_kv_heads, m.head_dim,
@@ -784,6 +788,21 @@ static int full_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c
     C.st_ok = fused;
     C.pst_ok = fused;  // every row's statistics were just computed: a new epoch
     ++C.epoch;
+  return DYLLM_OK;
+}
+
+static int full_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, const int *d_tokens) {
+  if (c->m.dtype == 1) return full_step_f32(ctx, w, c, d_tokens);
+  const dyllm_model_cfg &m = c->m;
+  const int d = m.d_model, qw = m.n_heads * m.head_dim, kw = m.n_kv_heads * m.head_dim, rows = c->rows;
+  cudaStream_t st = ctx->stream;
+  ctx->cls_offset = DYLLM_KC_FULL;
+  KL(OTHER, launch_embed_rows(d_tokens, nullptr, nullptr, rows, w->emb, c->H0, d, st));
+  for (int l = 0; l < m.n_layers; ++l) {
+    const LayerW &L = w->L[l];
+    LayerC &C = c->L[l];
+    const bf16 *Hprev = l == 0 ? c->H0 : c->L[l - 1].H;
+    RET(full_attn_phase(ctx, w, c, l));
     int prc = post_attention(ctx, w, c, l, nullptr, C.C, Hprev, nullptr, C.H);
     if (prc) {
       ctx->cls_offset = 0;
@@ -798,11 +817,10 @@ static int full_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c
   return DYLLM_OK;
 }
 
-// One layer of SparseStep (Alg. 3 lines 3-16) on internal lists.
-static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int l, int row_lo,
-                           const int *idx_in, const int *off_in, float tau, int *idx_out, int *off_out, float *sim,
-                           int *counts) {
-  if (c->m.dtype == 1) return layer_step_f32(ctx, w, c, l, row_lo, idx_in, off_in, tau, idx_out, off_out, sim, counts);
+// Phase 1 of a sparse layer step (Alg. 3 lines 3-11): a1-a4 up to the new contexts. Returns the
+// layer step's row tag and whether the attention epilogue already formed the similarity partials.
+static int attn_phase(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int l, int row_lo, const int *idx_in,
+                      const int *off_in, uint32_t *tag_out, bool *fuse_cos_out) {
   const dyllm_model_cfg &m = c->m;
   const int b = c->r.batch, N = c->N, rows = c->rows;
   const int d = m.d_model, qw = m.n_heads * m.head_dim, kw = m.n_kv_heads * m.head_dim;
@@ -847,7 +865,7 @@ static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *
   a.C_cache = C.C;
   // fused kernel: the epilogue commits C_new into the C cache itself and leaves the similarity
   // partials; other head dims write C_new (exact) / dC (approximate) rows to Cn
-  const bool fuse_cos = fused && g_attn_fuse_cos;
+  const bool fuse_cos = fused && g_attn_fuse_cos && !c->tp;  // tensor parallel: partials over shards
   a.C_out = fuse_cos ? C.C : c->Cn;
   a.cos_part = fuse_cos ? c->cos_part : nullptr;
   a.ex_rows = idx_in;
@@ -889,6 +907,25 @@ static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *
     C.pst_ok = true;
     ++C.epoch;
   }
+  *tag_out = tag;
+  *fuse_cos_out = fuse_cos;
+  return DYLLM_OK;
+}
+
+// One layer of SparseStep (Alg. 3 lines 3-16) on internal lists.
+static int layer_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int l, int row_lo,
+                           const int *idx_in, const int *off_in, float tau, int *idx_out, int *off_out, float *sim,
+                           int *counts) {
+  if (c->m.dtype == 1) return layer_step_f32(ctx, w, c, l, row_lo, idx_in, off_in, tau, idx_out, off_out, sim, counts);
+  const dyllm_model_cfg &m = c->m;
+  const int b = c->r.batch, N = c->N, rows = c->rows;
+  const int qw = m.n_heads * m.head_dim;
+  const LayerC &C = c->L[l];
+  const bf16 *Hprev = l == 0 ? c->H0 : c->L[l - 1].H;
+  cudaStream_t st = ctx->stream;
+  uint32_t tag = 0;
+  bool fuse_cos = false;
+  RET(attn_phase(ctx, w, c, l, row_lo, idx_in, off_in, &tag, &fuse_cos));
   // a5: cosine similarity + threshold + compaction; C_cache <- Cn for the input rows
   const bool fmode = c->r.select_mode == 1;
   const bool delta = attention_writes_delta(m.head_dim);  // fused kernel: Cn = dC for approximate rows
@@ -961,6 +998,45 @@ int dyllm_layer_step(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int
   return layer_step_impl(ctx, w, c, layer, row_lo, d_idx_in, d_off_in, tau, d_idx_out, d_off_out, d_sim_out, nullptr);
 }
 
+}  // extern "C"
+
+// Layer-1 list of a sparse step (Alg. 1, D5) into lst[0], and under the literal layer-1
+// policy the Q-only refresh of rows decoded at t-1 (D6)
+static int layer1_prepare(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int row_lo) {
+  const dyllm_run_cfg &r = c->r;
+  cudaStream_t st = ctx->stream;
+  // layer-1 idx_in: carried (or response rows when None) [∪ decoded rows, D5], ∩ input rows
+  KL(OTHER, launch_build_list(1, c->carried_valid ? c->carried : nullptr, c->carried_off,
+                              c->have_dec_prev ? c->dec_prev : nullptr, r.n_u, r.layer1_policy, r.batch, c->N, row_lo,
+                              r.L_P, c->lst[0], c->lst_off[0], st));
+  if (r.layer1_policy == 0 && c->have_dec_prev) {
+    // literal Alg. 1: rows decoded at t-1 stay out of layer-1 idx_in unless carried, but their
+    // embedding changed, so their query does too (Alg. 3 line 4 recomputes Q for every input
+    // row; D6 keeps a Q cache): refresh Q alone for decoded rows outside idx_in
+    const dyllm_model_cfg &m = c->m;
+    const int d = m.d_model, qw = m.n_heads * m.head_dim, kw = m.n_kv_heads * m.head_dim;
+    const LayerW &L0 = w->L[0];
+    KL(OTHER, launch_build_list(2, c->carried_valid ? c->carried : nullptr, c->carried_off, c->dec_prev, r.n_u, 0,
+                                r.batch, c->N, row_lo, r.L_P, c->qx_rows, c->qx_off, st));
+    const int *M_q = c->qx_off + r.batch;
+    if (m.dtype == 1) {
+      KL(GATHER, f32::gather_rmsnorm(fp(c->H0), c->qx_rows, M_q, c->rows, L0.g_attn, m.rms_eps, fp(c->Xn), d, st));
+      KL(QKV_GEMM, f32::gemm(g32(M_q, c->rows, qw + 2 * kw, d, fp(c->Xn), L0.wqkv, fp(c->qkv), qw + 2 * kw), st));
+      KL(QKV_POST, f32::qkv_post(fp(c->qkv), c->qx_rows, M_q, c->rows, L0.bqkv, c->N, m.n_heads, m.n_kv_heads,
+                                 m.head_dim, c->rope_cs, fp(c->L[0].Q), nullptr, nullptr, nullptr, 1, st));
+    } else {
+    KL(GATHER, launch_gather_rmsnorm(c->H0, c->qx_rows, M_q, c->rows, L0.g_attn, m.rms_eps, c->Xn, d, st));
+    KL(QKV_GEMM, RET(gemm(ctx, M_q, c->rows, qw + 2 * kw, d, c->Xn, L0.wqkv, c->qkv, qw + 2 * kw, EPI_BF16)));
+    KL(QKV_POST, launch_qkv_post(c->qkv, c->qx_rows, M_q, c->rows, L0.bqkv, c->N, m.n_heads, m.n_kv_heads,
+                                 m.head_dim, c->rope_cs, c->L[0].Q, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                 nullptr, nullptr, 0u, st, 1));
+    }
+  }
+  return DYLLM_OK;
+}
+
+extern "C" {
+
 int dyllm_denoise_step(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int t, const float *h_tau,
                        int32_t *d_tokens, int32_t *d_dec_pos, int32_t *d_dec_tok, int32_t *d_sal_counts) {
   CHECK_ARG(ctx && w && c && d_tokens && d_dec_tok, "null argument");
@@ -982,33 +1058,7 @@ int dyllm_denoise_step(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, i
       return DYLLM_E_STATE;
     }
     const int row_lo = (t % r.full_period == 0) ? 0 : r.L_P;
-    // layer-1 idx_in: carried (or response rows when None) [∪ decoded rows, D5], ∩ input rows
-    KL(OTHER, launch_build_list(1, c->carried_valid ? c->carried : nullptr, c->carried_off,
-                                c->have_dec_prev ? c->dec_prev : nullptr, r.n_u, r.layer1_policy, r.batch, c->N, row_lo,
-                                r.L_P, c->lst[0], c->lst_off[0], st));
-    if (r.layer1_policy == 0 && c->have_dec_prev) {
-      // literal Alg. 1: rows decoded at t-1 stay out of layer-1 idx_in unless carried, but their
-      // embedding changed, so their query does too (Alg. 3 line 4 recomputes Q for every input
-      // row; D6 keeps a Q cache): refresh Q alone for decoded rows outside idx_in
-      const dyllm_model_cfg &m = c->m;
-      const int d = m.d_model, qw = m.n_heads * m.head_dim, kw = m.n_kv_heads * m.head_dim;
-      const LayerW &L0 = w->L[0];
-      KL(OTHER, launch_build_list(2, c->carried_valid ? c->carried : nullptr, c->carried_off, c->dec_prev, r.n_u, 0,
-                                  r.batch, c->N, row_lo, r.L_P, c->qx_rows, c->qx_off, st));
-      const int *M_q = c->qx_off + r.batch;
-      if (m.dtype == 1) {
-        KL(GATHER, f32::gather_rmsnorm(fp(c->H0), c->qx_rows, M_q, c->rows, L0.g_attn, m.rms_eps, fp(c->Xn), d, st));
-        KL(QKV_GEMM, f32::gemm(g32(M_q, c->rows, qw + 2 * kw, d, fp(c->Xn), L0.wqkv, fp(c->qkv), qw + 2 * kw), st));
-        KL(QKV_POST, f32::qkv_post(fp(c->qkv), c->qx_rows, M_q, c->rows, L0.bqkv, c->N, m.n_heads, m.n_kv_heads,
-                                   m.head_dim, c->rope_cs, fp(c->L[0].Q), nullptr, nullptr, nullptr, 1, st));
-      } else {
-      KL(GATHER, launch_gather_rmsnorm(c->H0, c->qx_rows, M_q, c->rows, L0.g_attn, m.rms_eps, c->Xn, d, st));
-      KL(QKV_GEMM, RET(gemm(ctx, M_q, c->rows, qw + 2 * kw, d, c->Xn, L0.wqkv, c->qkv, qw + 2 * kw, EPI_BF16)));
-      KL(QKV_POST, launch_qkv_post(c->qkv, c->qx_rows, M_q, c->rows, L0.bqkv, c->N, m.n_heads, m.n_kv_heads,
-                                   m.head_dim, c->rope_cs, c->L[0].Q, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                   nullptr, nullptr, 0u, st, 1));
-      }
-    }
+    RET(layer1_prepare(ctx, w, c, row_lo));
     int cur = 0;
     for (int l = 0; l < c->m.n_layers; ++l) {
       float *sim_tr = c->tr_sims ? c->tr_sims + static_cast<int64_t>(l) * c->rows : nullptr;
@@ -1046,6 +1096,349 @@ int dyllm_unmask(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int32_t
   }
   RET(sticky(ctx));
   return unmask_impl(ctx, w, c, d_tokens, d_dec_pos, d_dec_tok);
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ tensor parallelism
+// NCCL is resolved at run time (the loopback backend needs none; the torch process usually has it)
+struct NcclApi {
+  bool ok = false;
+  decltype(&ncclGetUniqueId) get_id = nullptr;
+  decltype(&ncclCommInitRank) init_rank = nullptr;
+  decltype(&ncclAllReduce) all_reduce = nullptr;
+  decltype(&ncclCommDestroy) destroy = nullptr;
+};
+static NcclApi &nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.get_id = reinterpret_cast<decltype(api.get_id)>(dlsym(h, "ncclGetUniqueId"));
+      api.init_rank = reinterpret_cast<decltype(api.init_rank)>(dlsym(h, "ncclCommInitRank"));
+      api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+      api.destroy = reinterpret_cast<decltype(api.destroy)>(dlsym(h, "ncclCommDestroy"));
+      api.ok = api.get_id && api.init_rank && api.all_reduce && api.destroy;
+    }
+  }
+  return api;
+}
+
+struct dyllm_tp {
+  dyllm_ctx *ctx = nullptr;
+  int world = 1, rank = 0;
+  bool loopback = true;
+  ncclComm_t comm = nullptr;
+  std::vector<dyllm_cache *> shard;  // loopback: world shards; NCCL: this rank's
+  int *h_cnt = nullptr;              // pinned: device row counts read back for NCCL
+};
+
+// Sum of a per-shard buffer over the group, in shard order, left in every shard's buffer.
+// buf_of(c): the shard's buffer; M_ptr (nullable): shard 0's device row count; width: elements per row.
+template <typename F>
+static int tp_reduce(dyllm_tp *tp, F buf_of, const int *M_ptr, int M_cap, int width, bool f32) {
+  dyllm_ctx *ctx = tp->ctx;
+  cudaStream_t st = ctx->stream;
+  if (tp->loopback) {
+    TpPtrs p{};
+    for (int g = 0; g < tp->world; ++g) p.p[g] = buf_of(tp->shard[g]);
+    KL(OTHER, launch_tp_reduce(p, tp->world, M_ptr, M_cap, width, f32 ? 1 : 0, st));
+    DY_CUDA(cudaGetLastError());
+    return DYLLM_OK;
+  }
+  int M = M_cap;
+  if (M_ptr) {  // the list length lives on the device: read it back (one synchronisation)
+    DY_CUDA(cudaMemcpyAsync(tp->h_cnt, M_ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
+    DY_CUDA(cudaStreamSynchronize(st));
+    M = std::min(*tp->h_cnt, M_cap);
+  }
+  if (M <= 0) return DYLLM_OK;
+  void *b = buf_of(tp->shard[0]);
+  if (nccl_api().all_reduce(b, b, static_cast<size_t>(M) * width, f32 ? ncclFloat32 : ncclBfloat16, ncclSum, tp->comm,
+                            st) != ncclSuccess) {
+    set_error("ncclAllReduce failed");
+    return DYLLM_E_NCCL;
+  }
+  return DYLLM_OK;
+}
+
+// O projection + FFN of a shard on the rows (rows, M_ptr) (nullptr: all rows), with the group's
+// all-reduces: h = x + sum_g C_g W_o,g (shard 0 adds x), out = h + sum_g FFN_g(RMSNorm(h)) (shard 0
+// adds h); residual_mode 1 (paper_literal): h = RMSNorm(sum_g C_g W_o,g), out = sum_g FFN_g(h).
+// A_c(c): the shard's context rows (contiguous, aligned with rows); out rows land in H_l at `rows`.
+// rows_of(c) -> RowList{row ids, device count}: the shard's list (ignored when all_rows)
+struct RowList {
+  const int *rows;
+  const int *count;
+};
+template <typename FA, typename FR>
+static int tp_post_attention(dyllm_tp *tp, const dyllm_weights *const *W, int l, FA A_c, FR rows_of, bool all_rows) {
+  const int G = static_cast<int>(tp->shard.size());
+  dyllm_ctx *ctx = tp->ctx;
+  cudaStream_t st = ctx->stream;
+  dyllm_cache *c0 = tp->shard[0];
+  const dyllm_model_cfg &m0 = c0->m;
+  const int d = m0.d_model, R = c0->rows, b = c0->r.batch;
+  const bool res = m0.residual_mode == 0;
+  for (int i = 0; i < G; ++i) {
+    dyllm_cache *c = tp->shard[i];
+    const dyllm_model_cfg &m = c->m;
+    const int qw = m.n_heads * m.head_dim;
+    const bool first = (tp->loopback ? i : tp->rank) == 0;
+    const RowList rl = rows_of(c);
+    const int *rows = all_rows ? nullptr : rl.rows;
+    const int *M_ptr = all_rows ? nullptr : rl.count;
+    const bf16 *Hprev = l == 0 ? c->H0 : c->L[l - 1].H;
+    KL(O_GEMM, RET(gemm(ctx, M_ptr, R, d, qw, A_c(c), W[i]->L[l].wo, c->h, d, (res && first) ? EPI_RESID : EPI_BF16,
+                        Hprev, d, rows)));
+  }
+  RET(tp_reduce(tp, [](dyllm_cache *c) { return static_cast<void *>(c->h); },
+                all_rows ? nullptr : rows_of(c0).count, R, d, false));
+  for (int i = 0; i < G; ++i) {
+    dyllm_cache *c = tp->shard[i];
+    const dyllm_model_cfg &m = c->m;
+    const int F = m.d_ff;
+    const bool first = (tp->loopback ? i : tp->rank) == 0;
+    const int *M_ptr = all_rows ? nullptr : rows_of(c).count;
+    const LayerW &L = W[i]->L[l];
+    KL(OTHER, launch_rmsnorm_rows(c->h, M_ptr, R, L.g_ffn, m.rms_eps, c->hn, d, st));
+    KL(GU_GEMM, RET(gemm(ctx, M_ptr, R, 2 * F, d, c->hn, L.wgu, c->act, F, EPI_SWIGLU)));
+    bf16 *out = all_rows ? c->L[l].H : c->ffo;
+    KL(DOWN_GEMM, RET(gemm(ctx, M_ptr, R, d, F, c->act, L.wd, out, d, (res && first) ? EPI_RESID : EPI_BF16, c->h, d)));
+  }
+  RET(tp_reduce(tp, [l, all_rows](dyllm_cache *c) { return static_cast<void *>(all_rows ? c->L[l].H : c->ffo); },
+                all_rows ? nullptr : rows_of(c0).count, R, d, false));
+  if (!all_rows)  // scatter-back of the summed rows: rows outside the list keep their output
+    for (int i = 0; i < G; ++i) {
+      dyllm_cache *c = tp->shard[i];
+      const RowList rl = rows_of(c);
+      KL(OTHER, launch_scatter_rows(c->ffo, rl.rows, rl.count, R, c->L[l].H, d, st));
+    }
+  (void)b;
+  return DYLLM_OK;
+}
+
+static int tp_full_step(dyllm_tp *tp, const dyllm_weights *const *W, const int *d_tokens) {
+  const int G = static_cast<int>(tp->shard.size());
+  dyllm_ctx *ctx = tp->ctx;
+  const int nl = tp->shard[0]->m.n_layers;
+  ctx->cls_offset = DYLLM_KC_FULL;
+  for (int i = 0; i < G; ++i) {
+    dyllm_cache *c = tp->shard[i];
+    KL(OTHER, launch_embed_rows(d_tokens, nullptr, nullptr, c->rows, W[i]->emb, c->H0, c->m.d_model, ctx->stream));
+  }
+  int rc = DYLLM_OK;
+  for (int l = 0; l < nl && rc == DYLLM_OK; ++l) {
+    for (int i = 0; i < G && rc == DYLLM_OK; ++i) rc = full_attn_phase(ctx, W[i], tp->shard[i], l);
+    if (rc == DYLLM_OK)
+      rc = tp_post_attention(tp, W, l, [l](dyllm_cache *c) { return static_cast<const bf16 *>(c->L[l].C); },
+                             [](dyllm_cache *) { return RowList{nullptr, nullptr}; }, true);
+  }
+  ctx->cls_offset = 0;
+  RET(rc);
+  for (dyllm_cache *c : tp->shard) {
+    c->carried_valid = false;
+    c->have_dec_prev = false;
+    c->initialized = true;
+  }
+  DY_CUDA(cudaGetLastError());
+  return DYLLM_OK;
+}
+
+// One sparse layer of the group: a1-a4 per shard, similarity partials summed over the shards,
+// the same threshold / compaction on every shard, then O projection and FFN with their all-reduces.
+static int tp_layer_step(dyllm_tp *tp, const dyllm_weights *const *W, int l, int row_lo, int cur, float tau,
+                         int *counts) {
+  const int G = static_cast<int>(tp->shard.size());
+  dyllm_ctx *ctx = tp->ctx;
+  cudaStream_t st = ctx->stream;
+  dyllm_cache *c0 = tp->shard[0];
+  const int b = c0->r.batch, N = c0->N, R = c0->rows;
+  const bool fmode = c0->r.select_mode == 1;
+  std::vector<uint32_t> tags(G);
+  for (int i = 0; i < G; ++i) {
+    dyllm_cache *c = tp->shard[i];
+    const dyllm_model_cfg &m = c->m;
+    bool fc = false;
+    RET(attn_phase(ctx, W[i], c, l, row_lo, c->lst[cur], c->lst_off[cur], &tags[i], &fc));
+    const bool delta = attention_writes_delta(m.head_dim);
+    // this shard's partial sums (dot, |C_new|^2, |C_old|^2) per input row; C_cache <- C_new
+    KL(SELECT, launch_select(c->Cn, c->L[l].C, b, N, row_lo, m.n_heads * m.head_dim, 2.f, c->r.cmp, -1.f, nullptr,
+                             nullptr, nullptr, ctx->masks, ctx->ticket, nullptr, delta ? c->rowflag : nullptr, tags[i],
+                             delta ? c->lst_off[cur] : nullptr, st, nullptr, 0, c->tp_part));
+  }
+  RET(tp_reduce(tp, [](dyllm_cache *c) { return static_cast<void *>(c->tp_part); }, nullptr, R, 4, true));
+  for (int i = 0; i < G; ++i) {
+    dyllm_cache *c = tp->shard[i];
+    float *sim_tr = c->tr_sims ? c->tr_sims + static_cast<int64_t>(l) * c->rows : nullptr;
+    // identical sums on every shard: identical similarities, thresholds and lists
+    KL(SELECT, launch_select(nullptr, nullptr, b, N, row_lo, 8, fmode ? 2.f : tau, c->r.cmp, fmode ? tau : -1.f,
+                             c->lst[cur ^ 1], c->lst_off[cur ^ 1], (fmode && !sim_tr) ? c->sim : sim_tr, ctx->masks,
+                             ctx->ticket, i == 0 ? counts : nullptr, nullptr, 0u, c->lst_off[cur], st, c->tp_part, 1));
+    const dyllm_model_cfg &m = c->m;
+    KL(GATHER, launch_gather_rows(c->L[l].C, c->lst[cur ^ 1], c->lst_off[cur ^ 1] + b, R, c->Cg,
+                                  m.n_heads * m.head_dim, st));
+  }
+  return tp_post_attention(tp, W, l, [](dyllm_cache *c) { return static_cast<const bf16 *>(c->Cg); },
+                           [cur](dyllm_cache *c) { return RowList{c->lst[cur ^ 1], c->lst_off[cur ^ 1] + c->r.batch}; }, false);
+}
+
+extern "C" {
+
+int dyllm_tp_unique_id(void *h_out, int n_bytes) {
+  CHECK_ARG(h_out && n_bytes >= static_cast<int>(sizeof(ncclUniqueId)), "need a 128-byte buffer");
+  NcclApi &api = nccl_api();
+  if (!api.ok) {
+    set_error("libnccl.so.2 not found");
+    return DYLLM_E_NCCL;
+  }
+  ncclUniqueId id;
+  if (api.get_id(&id) != ncclSuccess) {
+    set_error("ncclGetUniqueId failed");
+    return DYLLM_E_NCCL;
+  }
+  std::memcpy(h_out, &id, sizeof(id));
+  return DYLLM_OK;
+}
+
+int dyllm_tp_create(dyllm_ctx *ctx, int world, int rank, const void *nccl_unique_id, dyllm_tp **out) {
+  CHECK_ARG(ctx && out, "null argument");
+  CHECK_ARG(world >= 1 && world <= kTpMax, "world out of range (1..8)");
+  dyllm_tp *tp = new dyllm_tp();
+  tp->ctx = ctx;
+  tp->world = world;
+  tp->loopback = nccl_unique_id == nullptr;
+  tp->rank = tp->loopback ? 0 : rank;
+  if (!tp->loopback) {
+    if (rank < 0 || rank >= world) {
+      delete tp;
+      set_error("rank out of range");
+      return DYLLM_E_ARG;
+    }
+    NcclApi &api = nccl_api();
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof(id));
+    if (!api.ok || api.init_rank(&tp->comm, world, id, rank) != ncclSuccess) {
+      delete tp;
+      set_error(api.ok ? "ncclCommInitRank failed" : "libnccl.so.2 not found");
+      return DYLLM_E_NCCL;
+    }
+    if (cudaMallocHost(&tp->h_cnt, sizeof(int)) != cudaSuccess) {
+      api.destroy(tp->comm);
+      delete tp;
+      set_error("cudaMallocHost failed");
+      return DYLLM_E_NOMEM;
+    }
+  }
+  tp->shard.assign(tp->loopback ? world : 1, nullptr);
+  *out = tp;
+  return DYLLM_OK;
+}
+
+int dyllm_tp_attach(dyllm_tp *tp, int shard, dyllm_cache *c) {
+  CHECK_ARG(tp && c, "null argument");
+  const int slot = tp->loopback ? shard : 0;
+  if (shard < 0 || shard >= tp->world || (!tp->loopback && shard != tp->rank)) {
+    set_error("shard out of range (NCCL: shard must be the rank)");
+    return DYLLM_E_INDEX;
+  }
+  if (c->m.dtype != 0) {
+    set_error("tensor parallelism: bf16 caches only");
+    return DYLLM_E_ARG;
+  }
+  for (dyllm_cache *o : tp->shard)
+    if (o && (o->m.d_model != c->m.d_model || o->m.n_layers != c->m.n_layers || o->m.n_heads != c->m.n_heads ||
+              o->m.n_kv_heads != c->m.n_kv_heads || o->m.d_ff != c->m.d_ff || o->N != c->N ||
+              o->r.batch != c->r.batch || o->m.residual_mode != c->m.residual_mode)) {
+      set_error("tensor parallelism: shard shapes differ");
+      return DYLLM_E_SHAPE;
+    }
+  if (!c->tp_part) {
+    RET(dalloc_t(c->allocs, &c->tp_part, c->rows));
+    RET(dalloc_t(c->allocs, &c->tp_tokens, c->rows + static_cast<int64_t>(c->r.batch) * c->r.n_u));
+  }
+  c->tp = tp;
+  c->tp_shard = shard;
+  tp->shard[slot] = c;
+  return DYLLM_OK;
+}
+
+static int tp_check(dyllm_tp *tp, const dyllm_weights *const *w) {
+  CHECK_ARG(tp && w, "null argument");
+  for (size_t i = 0; i < tp->shard.size(); ++i) {
+    if (!tp->shard[i] || !w[i]) {
+      set_error("tensor parallelism: every local shard needs a cache and weights");
+      return DYLLM_E_STATE;
+    }
+  }
+  return sticky(tp->ctx);
+}
+
+int dyllm_tp_cache_init(dyllm_tp *tp, const dyllm_weights *const *w, const int32_t *d_tokens) {
+  CHECK_ARG(d_tokens, "null tokens");
+  RET(tp_check(tp, w));
+  return tp_full_step(tp, w, d_tokens);
+}
+
+int dyllm_tp_denoise_step(dyllm_tp *tp, const dyllm_weights *const *w, int t, const float *h_tau, int32_t *d_tokens,
+                          int32_t *d_dec_pos, int32_t *d_dec_tok, int32_t *d_sal_counts) {
+  CHECK_ARG(d_tokens && d_dec_tok, "null argument");
+  RET(tp_check(tp, w));
+  dyllm_ctx *ctx = tp->ctx;
+  cudaStream_t st = ctx->stream;
+  const int G = static_cast<int>(tp->shard.size());
+  dyllm_cache *c0 = tp->shard[0];
+  const dyllm_run_cfg &r = c0->r;
+  const int T_total = (r.L_R + r.n_u - 1) / r.n_u;
+  if (t < 0) {
+    set_error("t < 0");
+    return DYLLM_E_INDEX;
+  }
+  if (t >= T_total) return DYLLM_DONE;
+  if (t < r.T_full) {
+    RET(tp_full_step(tp, w, d_tokens));
+  } else {
+    CHECK_ARG(h_tau, "null tau");
+    for (dyllm_cache *c : tp->shard)
+      if (!c->initialized) {
+        set_error("sparse step before any FullStep");
+        return DYLLM_E_STATE;
+      }
+    const int row_lo = (t % r.full_period == 0) ? 0 : r.L_P;
+    for (int i = 0; i < G; ++i) RET(layer1_prepare(ctx, w[i], tp->shard[i], row_lo));
+    int cur = 0;
+    for (int l = 0; l < c0->m.n_layers; ++l) {
+      RET(tp_layer_step(tp, w, l, row_lo, cur, h_tau[l], d_sal_counts ? d_sal_counts + l * r.batch : nullptr));
+      cur ^= 1;
+    }
+    for (dyllm_cache *c : tp->shard) {
+      DY_CUDA(cudaMemcpyAsync(c->carried, c->lst[cur], sizeof(int) * c->rows, cudaMemcpyDeviceToDevice, st));
+      DY_CUDA(cudaMemcpyAsync(c->carried_off, c->lst_off[cur], sizeof(int) * (r.batch + 1), cudaMemcpyDeviceToDevice,
+                              st));
+      c->carried_valid = true;
+    }
+  }
+  // unmasking: every shard decides on the same (bit-identical) H_L and the same tokens
+  for (int i = 1; i < G; ++i)
+    DY_CUDA(cudaMemcpyAsync(tp->shard[i]->tp_tokens, d_tokens, sizeof(int32_t) * c0->rows, cudaMemcpyDeviceToDevice,
+                            st));
+  RET(unmask_impl(ctx, w[0], c0, d_tokens, d_dec_pos, d_dec_tok));
+  for (int i = 1; i < G; ++i) {
+    dyllm_cache *c = tp->shard[i];
+    RET(unmask_impl(ctx, w[i], c, c->tp_tokens, nullptr, c->tp_tokens + c->rows));
+  }
+  return DYLLM_OK;
+}
+
+void dyllm_tp_destroy(dyllm_tp *tp) {
+  if (!tp) return;
+  for (dyllm_cache *c : tp->shard)
+    if (c) c->tp = nullptr;
+  if (tp->comm) nccl_api().destroy(tp->comm);
+  if (tp->h_cnt) cudaFreeHost(tp->h_cnt);
+  delete tp;
 }
 
 // ------------------------------------------------------------------ ABI: instrumentation

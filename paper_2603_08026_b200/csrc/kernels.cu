@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
     int cmp, float frac, int *__restrict__ idx_out, int *__restrict__ off_out, float *__restrict__ sim_out,
     unsigned *__restrict__ masks, unsigned *__restrict__ ticket, int *__restrict__ counts_out,
     const uint32_t *__restrict__ rowflag, uint32_t tag, const int *__restrict__ dl_off,
-    const float4 *__restrict__ cos_part, int H) {
+    const float4 *__restrict__ cos_part, int H, float4 *__restrict__ part_out) {
   pdl_wait();
   __shared__ unsigned row_flag[kSelRowsPerCta];
   __shared__ bool is_last;
@@ -556,6 +556,7 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
       dot = warp_sum(dot);
       na = warp_sum(na);
       nb = warp_sum(nb);
+      if (part_out && lane == 0) part_out[r] = make_float4(dot, na, nb, 0.f);
       float sim;
       const bool za = na < 1e-24f, zb = nb < 1e-24f;   // D9 zero-norm policy
       if (za && zb) sim = 1.f;
@@ -566,6 +567,9 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
     }
     if (lane == 0) row_flag[rr] = f;
   }
+  // tensor-parallel shard: only the partial sums over this shard's heads; the threshold
+  // and compaction run after the all-reduce (cos_part mode, H = 1), identically on every shard
+  if (part_out) return;
   __syncthreads();
   if (threadIdx.x < 32) {
     const unsigned m = __ballot_sync(0xffffffffu, row_flag[threadIdx.x] != 0);
@@ -735,6 +739,28 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
   }
   (void)nwords;
   if (threadIdx.x == 0) *ticket = 0u;  // re-arm for the next launch (stream-ordered)
+}
+
+// ============================================================================ TP: loopback all-reduce
+// Sum over the G shards of a group driven by one process on one device: element e
+// of every shard's buffer becomes sum_g buf_g[e], added in shard order 0..G-1 (fp32, one rounding
+// for bf16 buffers), so every shard holds bit-identical results. Rows from a device count.
+__global__ void tp_reduce_kernel(TpPtrs ptrs, int G, const int *__restrict__ M_ptr, int M_cap, int width, int f32) {
+  pdl_wait();
+  const int M = M_ptr ? min(*M_ptr, M_cap) : M_cap;
+  const int64_t n = static_cast<int64_t>(M) * width;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float acc = 0.f;
+    if (f32) {
+      for (int g = 0; g < G; ++g) acc += static_cast<const float *>(ptrs.p[g])[e];
+      for (int g = 0; g < G; ++g) static_cast<float *>(ptrs.p[g])[e] = acc;
+    } else {
+      for (int g = 0; g < G; ++g) acc += bf2f(static_cast<const bf16 *>(ptrs.p[g])[e]);
+      const bf16 v = f2bf(acc);
+      for (int g = 0; g < G; ++g) static_cast<bf16 *>(ptrs.p[g])[e] = v;
+    }
+  }
 }
 
 // ============================================================================ a9: unmasking
@@ -977,11 +1003,11 @@ void launch_build_list(int mode, const int *carried, const int *carried_off, con
 void launch_select(const bf16 *c_new, bf16 *c_cache, int batch, int N, int row_lo, int width, float tau, int cmp,
                    float frac, int *idx_out, int *off_out, float *sim_out, unsigned *masks, unsigned *ticket,
                    int *counts, const uint32_t *rowflag, uint32_t tag, const int *dl_off, cudaStream_t st,
-                   const float4 *cos_part, int H) {
+                   const float4 *cos_part, int H, float4 *part_out) {
   const int L = N - row_lo;
   dim3 grid((L + kSelRowsPerCta - 1) / kSelRowsPerCta, batch);
   DY_CUDA_LAUNCH(launch_k(select_salient_kernel, dim3(grid), dim3(kSelThreads), 0, st, 1, c_new, c_cache, N, row_lo, width, tau, cmp, frac, idx_out, off_out,
-                                              sim_out, masks, ticket, counts, rowflag, tag, dl_off, cos_part, H));
+                                              sim_out, masks, ticket, counts, rowflag, tag, dl_off, cos_part, H, part_out));
 }
 void launch_lm_candidates(const int *tokens, int batch, int L_P, int L_R, int block, int mask_id, int *rows, int *off,
                           cudaStream_t st) {
@@ -992,6 +1018,9 @@ void launch_lm_select_commit(const float4 *partials, int n_tiles, const int *row
                              cudaStream_t st, float *H0f) {
   DY_CUDA_LAUNCH(launch_k(lm_select_commit_kernel, dim3(batch), dim3(256), 0, st, 1, partials, n_tiles, rows, off, n_u, tokens, dec_pos, dec_tok, emb, H0,
                                                  d, H0f));
+}
+void launch_tp_reduce(const TpPtrs &ptrs, int G, const int *M_ptr, int M_cap, int width, int f32, cudaStream_t st) {
+  DY_CUDA_LAUNCH(launch_k(tp_reduce_kernel, dim3(148 * 4), dim3(256), 0, st, 1, ptrs, G, M_ptr, M_cap, width, f32));
 }
 void launch_ih4_fill(bf16 *dst, int64_t rows, int cols, uint64_t keyA, uint64_t keyB, int il, float scale,
                      cudaStream_t st) {

@@ -33,7 +33,12 @@ void launch_build_list(int mode, const int *carried, const int *carried_off, con
 void launch_select(const bf16 *c_new, bf16 *c_cache, int batch, int N, int row_lo, int width, float tau, int cmp,
                    float frac, int *idx_out, int *off_out, float *sim_out, unsigned *masks, unsigned *ticket,
                    int *counts, const uint32_t *rowflag, uint32_t tag, const int *dl_off, cudaStream_t st,
-                   const float4 *cos_part = nullptr, int H = 0);
+                   const float4 *cos_part = nullptr, int H = 0, float4 *part_out = nullptr);
+constexpr int kTpMax = 8;
+struct TpPtrs {
+  void *p[kTpMax];
+};
+void launch_tp_reduce(const TpPtrs &ptrs, int G, const int *M_ptr, int M_cap, int width, int f32, cudaStream_t st);
 void launch_lm_candidates(const int *tokens, int batch, int L_P, int L_R, int block, int mask_id, int *rows, int *off,
                           cudaStream_t st);
 void launch_lm_select_commit(const float4 *partials, int n_tiles, const int *rows, const int *off, int batch, int n_u,

@@ -1,7 +1,8 @@
-"""Batch-parallel multi-GPU plumbing: one process per GPU, every rank owns a
+"""Multi-GPU plumbing. Batch parallelism: one process per GPU, every rank owns a
 contiguous shard of the sequences and runs the whole DyLLM step on its own GPU with no per-step
 collective. Only the bench timing (max over ranks) and the final token gather cross ranks.
-torch.distributed (NCCL on GPUs, gloo in the CPU tests) is the transport."""
+torch.distributed (NCCL on GPUs, gloo in the CPU tests) is the transport. Tensor parallelism
+(include/dyllm.h dyllm_tp_*): shard_weights slices a model's weights into the head / FFN shards."""
 from __future__ import annotations
 
 import os
@@ -42,3 +43,26 @@ def gather_tokens(tokens: torch.Tensor, global_batch: int):
     out = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(out, pad)
     return torch.cat([o[: hi - lo] for o, (lo, hi) in zip(out, sizes)], dim=0)
+
+
+def shard_weights(cfg, W, world: int, shard: int):
+    """Tensor-parallel shard `shard` of `world` (include/dyllm.h): the local model cfg and the
+    oracle-layout weights of its heads and FFN channels (embeddings, gains and LM head whole)."""
+    from dataclasses import replace
+    hd = cfg.head_dim
+    Hl, KVl, Fl = cfg.n_heads // world, cfg.n_kv_heads // world, cfg.d_ff // world
+    if Hl * world != cfg.n_heads or KVl * world != cfg.n_kv_heads or Fl * world != cfg.d_ff:
+        raise ValueError("n_heads, n_kv_heads and d_ff must divide by the TP world size")
+    lcfg = replace(cfg, n_heads=Hl, n_kv_heads=KVl, d_ff=Fl)
+    q = slice(shard * Hl * hd, (shard + 1) * Hl * hd)
+    kv = slice(shard * KVl * hd, (shard + 1) * KVl * hd)
+    f = slice(shard * Fl, (shard + 1) * Fl)
+    layers = []
+    for lw in W["layers"]:
+        sl = {"g_attn": lw["g_attn"], "wq": lw["wq"][q], "wk": lw["wk"][kv], "wv": lw["wv"][kv],
+              "wo": lw["wo"][:, q], "g_ffn": lw["g_ffn"], "w_gate": lw["w_gate"][f], "w_up": lw["w_up"][f],
+              "w_down": lw["w_down"][:, f]}
+        if cfg.qkv_bias:
+            sl.update(bq=lw["bq"][q], bk=lw["bk"][kv], bv=lw["bv"][kv])
+        layers.append(sl)
+    return lcfg, {"emb": W["emb"], "g_final": W["g_final"], "lm_head": W["lm_head"], "layers": layers}

@@ -87,6 +87,12 @@ def _load():
         "dyllm_launch_count": (U64, []),
         "dyllm_set_option": (I, [I, I]),
         "dyllm_debug_trace_buffer": (I, [I, P]),
+        "dyllm_tp_unique_id": (I, [P, I]),
+        "dyllm_tp_create": (I, [P, I, I, P, PP]),
+        "dyllm_tp_attach": (I, [P, I, P]),
+        "dyllm_tp_cache_init": (I, [P, P, P]),
+        "dyllm_tp_denoise_step": (I, [P, P, I, P, P, P, P, P]),
+        "dyllm_tp_destroy": (None, [P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -324,6 +330,57 @@ class Cache:
 
     def import_(self, layer, which, src: torch.Tensor):
         _check(_lib.dyllm_cache_copy(self.ctx.h, self.h, layer, which, _ptr(src.contiguous()), 1, 0))
+
+
+from .dist import shard_weights  # noqa: E402,F401  (tensor-parallel shard slicing, host logic)
+
+
+class TensorParallel:
+    """A tensor-parallel group (dyllm_tp_*): loopback (every shard in this process, nccl_id None)
+    or NCCL (this process is `rank` of `world`)."""
+
+    def __init__(self, ctx: Context, world: int, rank: int = 0, nccl_id: bytes | None = None):
+        self.ctx, self.world = ctx, world
+        h = C.c_void_p()
+        buf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        _check(_lib.dyllm_tp_create(ctx.h, world, rank, buf, C.byref(h)))
+        self.h = h
+        self.caches = []
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(_lib.dyllm_tp_unique_id(buf, 128))
+        return buf.raw
+
+    def attach(self, shard: int, cache: "Cache"):
+        _check(_lib.dyllm_tp_attach(self.h, shard, cache.h))
+        self.caches.append(cache)
+
+    @staticmethod
+    def _warr(weights):
+        arr = (C.c_void_p * len(weights))(*[w.h.value for w in weights])
+        return arr
+
+    def init(self, weights, tokens):
+        _check(_lib.dyllm_tp_cache_init(self.h, self._warr(weights), _ptr(tokens)))
+
+    def denoise_step(self, weights, t, tau, tokens, dec_pos, dec_tok, sal_counts=None):
+        n_layers = weights[0].cfg.n_layers
+        taus = np.broadcast_to(np.asarray(tau, dtype=np.float32), (n_layers,)).copy()
+        return _check(_lib.dyllm_tp_denoise_step(self.h, self._warr(weights), t, taus.ctypes.data_as(C.c_void_p),
+                                                 _ptr(tokens), _ptr(dec_pos), _ptr(dec_tok), _ptr(sal_counts)))
+
+    def close(self):
+        if self.h:
+            _lib.dyllm_tp_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Engine:
