@@ -235,8 +235,9 @@ int dyllm_ctx_create(int device, void *cuda_stream, dyllm_ctx **out) {
     return DYLLM_E_ARG;
   }
   DY_CUDA(cudaMalloc(&c->masks, kMaskCap * sizeof(unsigned)));
-  DY_CUDA(cudaMalloc(&c->ticket, sizeof(unsigned)));
-  DY_CUDA(cudaMemset(c->ticket, 0, sizeof(unsigned)));
+  // K1 tickets: [0] global last-CTA ticket, [1 + s] per-sequence tickets (fraction mode, batch <= 1024)
+  DY_CUDA(cudaMalloc(&c->ticket, 1025 * sizeof(unsigned)));
+  DY_CUDA(cudaMemset(c->ticket, 0, 1025 * sizeof(unsigned)));
   DY_CUDA(cudaMalloc(&c->sk_ws, skinny_ws_floats(c->num_sms) * sizeof(float)));
   DY_CUDA(cudaMalloc(&c->sk_ctr, kSkinnyCtrCap * sizeof(int)));
   DY_CUDA(cudaMemset(c->sk_ctr, 0, kSkinnyCtrCap * sizeof(int)));
@@ -1280,6 +1281,12 @@ static int tp_layer_step(dyllm_tp *tp, const dyllm_weights *const *W, int l, int
     const dyllm_model_cfg &m = c->m;
     KL(GATHER, launch_gather_rows(c->L[l].C, c->lst[cur ^ 1], c->lst_off[cur ^ 1] + b, R, c->Cg,
                                   m.n_heads * m.head_dim, st));
+    if (c->tr_lists) {  // dyllm_cache_set_trace on a shard: its per-layer lists
+      DY_CUDA(cudaMemcpyAsync(c->tr_lists + static_cast<int64_t>(l) * c->rows, c->lst[cur ^ 1], sizeof(int) * c->rows,
+                              cudaMemcpyDeviceToDevice, st));
+      DY_CUDA(cudaMemcpyAsync(c->tr_offs + static_cast<int64_t>(l) * (b + 1), c->lst_off[cur ^ 1], sizeof(int) * (b + 1),
+                              cudaMemcpyDeviceToDevice, st));
+    }
   }
   return tp_post_attention(tp, W, l, [](dyllm_cache *c) { return static_cast<const bf16 *>(c->Cg); },
                            [cur](dyllm_cache *c) { return RowList{c->lst[cur ^ 1], c->lst_off[cur ^ 1] + c->r.batch}; }, false);

@@ -571,132 +571,146 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
   // and compaction run after the all-reduce (cos_part mode, H = 1), identically on every shard
   if (part_out) return;
   __syncthreads();
+  __shared__ bool seq_last;
   if (threadIdx.x < 32) {
     const unsigned m = __ballot_sync(0xffffffffu, row_flag[threadIdx.x] != 0);
     if (threadIdx.x == 0) {
       masks[s * nchunks + chunk] = m;
       __threadfence();
-      const unsigned t = atomicAdd(ticket, 1u);
-      is_last = (t == gridDim.x * gridDim.y - 1);
+      // fraction mode: the last CTA of each sequence finds that sequence's threshold (the
+      // sequences in parallel, one SM each) before it arrives at the global ticket
+      seq_last = frac >= 0.f && atomicAdd(ticket + 1 + s, 1u) == static_cast<unsigned>(nchunks - 1);
+      is_last = false;
+      if (!seq_last) is_last = atomicAdd(ticket, 1u) == gridDim.x * gridDim.y - 1;
     }
   }
   __syncthreads();
-  if (!is_last) return;
-  // ---- last CTA: scan all masks (b * nchunks words) and emit the packed list
-  __threadfence();
   const int batch = gridDim.y;
-  const int nwords = batch * nchunks;
-  __shared__ int seq_base[1025];
-  if (frac >= 0.f) {
-    // fraction-controlled mode (D19): per sequence, tau* = the similarity of rank k = round(f*L)
-    // (0-based) found by an 8-bit radix select over the order-preserving uint32 keys of s, then
-    // the masks are rebuilt as s < tau* (k rows when there are no ties), s <= tau* under cmp = 1.
-    __shared__ unsigned hist[kSelWarps][256];
-    for (int sq = warp; sq < batch; sq += kSelWarps) {
-      const float *sv = sim_out + static_cast<int64_t>(sq) * N + row_lo;
-      const int k = static_cast<int>(floorf(frac * L + 0.5f));
-      // the sequence's similarities, loaded once (all loads in flight together) into registers:
-      // element j of lane l is row j*32 + l (L <= 1024; longer inputs stream from L2 per pass)
-      constexpr int kRegRows = 32;
-      const bool in_regs = L <= 32 * kRegRows;
-      float sreg[kRegRows];
-#pragma unroll
-      for (int j = 0; j < kRegRows; ++j) {
-        const int i = j * 32 + lane;
-        sreg[j] = (in_regs && i < L) ? __ldcg(sv + i) : INFINITY;
-      }
-      auto key_of = [](float f) {
-        const uint32_t u = __float_as_uint(f);
-        return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-      };
-      float thr = INFINITY;
-      if (k < L) {
-        uint32_t prefix = 0, pmask = 0;
-        int rank = k;
-        for (int shift = 24; shift >= 0; shift -= 8) {
-          for (int i = lane; i < 256; i += 32) hist[warp][i] = 0;
-          __syncwarp();
-          if (in_regs) {
-            // similarities cluster in a few top-byte bins: lanes with equal digits are merged
-            // (match.any) so each bin takes one shared-memory atomic per instruction instead of
-            // up to 32 serialised ones
-#pragma unroll
-            for (int j = 0; j < kRegRows; ++j) {
-              if (j * 32 >= L) break;
-              const uint32_t key = key_of(sreg[j]);
-              const bool in = j * 32 + lane < L && (key & pmask) == prefix;
-              const unsigned act = __ballot_sync(0xffffffffu, in);
-              if (in) {
-                const uint32_t dig = (key >> shift) & 255u;
-                const unsigned same = __match_any_sync(act, dig);
-                if (lane == __ffs(same) - 1) atomicAdd(&hist[warp][dig], static_cast<unsigned>(__popc(same)));
-              }
-            }
-          } else {
-            for (int i = lane; i < L; i += 32) {
-              const uint32_t key = key_of(__ldcg(sv + i));
-              if ((key & pmask) == prefix) atomicAdd(&hist[warp][(key >> shift) & 255u], 1u);
-            }
-          }
-          __syncwarp();
-          unsigned loc[8], sum = 0;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            loc[j] = hist[warp][lane * 8 + j];
-            sum += loc[j];
-          }
-          unsigned incl = sum;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-          }
-          const unsigned excl = incl - sum;
-          const bool mine = static_cast<unsigned>(rank) >= excl && static_cast<unsigned>(rank) < incl;
-          const unsigned bal = __ballot_sync(0xffffffffu, mine);
-          const int src = __ffs(bal) - 1;
-          int digit = 0, nrank = 0;
-          if (lane == src) {
-            unsigned c = excl;
-            for (int j = 0; j < 8; ++j) {
-              if (static_cast<unsigned>(rank) < c + loc[j]) {
-                digit = lane * 8 + j;
-                nrank = rank - static_cast<int>(c);
-                break;
-              }
-              c += loc[j];
-            }
-          }
-          digit = __shfl_sync(0xffffffffu, digit, src);
-          rank = __shfl_sync(0xffffffffu, nrank, src);
-          prefix |= static_cast<uint32_t>(digit) << shift;
-          pmask |= 255u << shift;
-          __syncwarp();
+  if (seq_last) {
+    __threadfence();
+  {
+      // fraction-controlled mode (D19): per sequence, tau* = the similarity of rank k = round(f*L)
+      // (0-based) found by an 8-bit radix select over the order-preserving uint32 keys of s, then
+      // the masks are rebuilt as s < tau* (k rows when there are no ties), s <= tau* under cmp = 1.
+      __shared__ unsigned hist[kSelWarps][256];
+      if (warp == 0) {
+        const int sq = s;
+        const float *sv = sim_out + static_cast<int64_t>(sq) * N + row_lo;
+        const int k = static_cast<int>(floorf(frac * L + 0.5f));
+        // the sequence's similarities, loaded once (all loads in flight together) into registers:
+        // element j of lane l is row j*32 + l (L <= 1024; longer inputs stream from L2 per pass)
+        constexpr int kRegRows = 32;
+        const bool in_regs = L <= 32 * kRegRows;
+        float sreg[kRegRows];
+  #pragma unroll
+        for (int j = 0; j < kRegRows; ++j) {
+          const int i = j * 32 + lane;
+          sreg[j] = (in_regs && i < L) ? __ldcg(sv + i) : INFINITY;
         }
-        const uint32_t u = (prefix & 0x80000000u) ? (prefix & 0x7FFFFFFFu) : ~prefix;
-        thr = __uint_as_float(u);
-      }
-      if (in_regs) {
-#pragma unroll
-        for (int w = 0; w < kRegRows; ++w) {
-          if (w < nchunks) {
-            const bool fl = w * 32 + lane < L && (cmp ? sreg[w] <= thr : sreg[w] < thr);
+        auto key_of = [](float f) {
+          const uint32_t u = __float_as_uint(f);
+          return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+        };
+        float thr = INFINITY;
+        if (k < L) {
+          uint32_t prefix = 0, pmask = 0;
+          int rank = k;
+          for (int shift = 24; shift >= 0; shift -= 8) {
+            for (int i = lane; i < 256; i += 32) hist[warp][i] = 0;
+            __syncwarp();
+            if (in_regs) {
+              // similarities cluster in a few top-byte bins: lanes with equal digits are merged
+              // (match.any) so each bin takes one shared-memory atomic per instruction instead of
+              // up to 32 serialised ones
+  #pragma unroll
+              for (int j = 0; j < kRegRows; ++j) {
+                if (j * 32 >= L) break;
+                const uint32_t key = key_of(sreg[j]);
+                const bool in = j * 32 + lane < L && (key & pmask) == prefix;
+                const unsigned act = __ballot_sync(0xffffffffu, in);
+                if (in) {
+                  const uint32_t dig = (key >> shift) & 255u;
+                  const unsigned same = __match_any_sync(act, dig);
+                  if (lane == __ffs(same) - 1) atomicAdd(&hist[warp][dig], static_cast<unsigned>(__popc(same)));
+                }
+              }
+            } else {
+              for (int i = lane; i < L; i += 32) {
+                const uint32_t key = key_of(__ldcg(sv + i));
+                if ((key & pmask) == prefix) atomicAdd(&hist[warp][(key >> shift) & 255u], 1u);
+              }
+            }
+            __syncwarp();
+            unsigned loc[8], sum = 0;
+  #pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              loc[j] = hist[warp][lane * 8 + j];
+              sum += loc[j];
+            }
+            unsigned incl = sum;
+  #pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+              if (lane >= o) incl += t;
+            }
+            const unsigned excl = incl - sum;
+            const bool mine = static_cast<unsigned>(rank) >= excl && static_cast<unsigned>(rank) < incl;
+            const unsigned bal = __ballot_sync(0xffffffffu, mine);
+            const int src = __ffs(bal) - 1;
+            int digit = 0, nrank = 0;
+            if (lane == src) {
+              unsigned c = excl;
+              for (int j = 0; j < 8; ++j) {
+                if (static_cast<unsigned>(rank) < c + loc[j]) {
+                  digit = lane * 8 + j;
+                  nrank = rank - static_cast<int>(c);
+                  break;
+                }
+                c += loc[j];
+              }
+            }
+            digit = __shfl_sync(0xffffffffu, digit, src);
+            rank = __shfl_sync(0xffffffffu, nrank, src);
+            prefix |= static_cast<uint32_t>(digit) << shift;
+            pmask |= 255u << shift;
+            __syncwarp();
+          }
+          const uint32_t u = (prefix & 0x80000000u) ? (prefix & 0x7FFFFFFFu) : ~prefix;
+          thr = __uint_as_float(u);
+        }
+        if (in_regs) {
+  #pragma unroll
+          for (int w = 0; w < kRegRows; ++w) {
+            if (w < nchunks) {
+              const bool fl = w * 32 + lane < L && (cmp ? sreg[w] <= thr : sreg[w] < thr);
+              const unsigned m = __ballot_sync(0xffffffffu, fl);
+              if (lane == 0) masks[sq * nchunks + w] = m;
+            }
+          }
+        } else {
+          for (int w = 0; w < nchunks; ++w) {
+            const int i = w * kSelRowsPerCta + lane;
+            const float sv_i = i < L ? __ldcg(sv + i) : INFINITY;
+            const bool fl = i < L && (cmp ? sv_i <= thr : sv_i < thr);
             const unsigned m = __ballot_sync(0xffffffffu, fl);
             if (lane == 0) masks[sq * nchunks + w] = m;
           }
         }
-      } else {
-        for (int w = 0; w < nchunks; ++w) {
-          const int i = w * kSelRowsPerCta + lane;
-          const float sv_i = i < L ? __ldcg(sv + i) : INFINITY;
-          const bool fl = i < L && (cmp ? sv_i <= thr : sv_i < thr);
-          const unsigned m = __ballot_sync(0xffffffffu, fl);
-          if (lane == 0) masks[sq * nchunks + w] = m;
-        }
       }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      ticket[1 + s] = 0u;  // re-arm (stream-ordered)
+      __threadfence();
+      is_last = atomicAdd(ticket, 1u) == gridDim.x * gridDim.y - 1;
     }
     __syncthreads();
   }
+  if (!is_last) return;
+  // ---- last CTA: scan all masks (b * nchunks words) and emit the packed list
+  __threadfence();
+  const int nwords = batch * nchunks;
+  __shared__ int seq_base[1025];
   // per-sequence counts (one warp per sequence, strided)
   for (int sq = warp; sq < batch; sq += kSelWarps) {
     int c = 0;
