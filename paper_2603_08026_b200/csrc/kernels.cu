@@ -139,7 +139,11 @@ __global__ void scatter_rows_kernel(const bf16 *__restrict__ src, const int *__r
 // For packed row i (row id r = idx[i], pos = r % N): q,k,v = qkv[i] (+bias); RoPE(q,k) at pos
 // (rotate-half, D10); dV = v - V_cache[r] captured BEFORE the overwrite;
 // Q_cache[r], K_cache[r], V_cache[r] <- q, k, v (D6).
-__global__ void qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restrict__ idx,
+// two CTAs of 512 threads per SM (92 registers left one resident: 4 waves of CTAs for 592 rows)
+#ifndef DYLLM_QKVPOST_LB
+#define DYLLM_QKVPOST_LB 2
+#endif
+__global__ void __launch_bounds__(512, DYLLM_QKVPOST_LB) qkv_post_kernel(const bf16 *__restrict__ qkv, const int *__restrict__ idx,
                                 const int *__restrict__ M_ptr, int M_cap, const bf16 *__restrict__ bias, int N,
                                 int H, int KVH, int hd, const float2 *__restrict__ rope_cs, bf16 *__restrict__ Qc,
                                 bf16 *__restrict__ Kc, bf16 *__restrict__ Vc, bf16 *__restrict__ dV,

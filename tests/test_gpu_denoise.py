@@ -263,3 +263,15 @@ def test_denoise_fused_similarity_partials(select_mode):
         _denoise_parity("small128", select_mode, 1)
     finally:
         dy.set_option(dy.OPT_ATTN_COS, prev)
+
+
+def test_denoise_two_kernel_attention_path():
+    """head_dim 128 through the two-kernel attention of attn.cu (statistics, then P.V:
+    DYLLM_OPT_ATTN_FUSED = 0), the path of every other head dim (dense Alg. 4, no incremental
+    statistics)."""
+    from paper_2603_08026_b200 import dyllm as dy
+    prev = dy.set_option(dy.OPT_ATTN_FUSED, 0)
+    try:
+        _denoise_parity("small128", 1, 1)
+    finally:
+        dy.set_option(dy.OPT_ATTN_FUSED, prev)

@@ -38,7 +38,7 @@ def main():
     ctx = dy.Context(0)
     dy.set_option(dy.OPT_SKINNY_GEMM, a.skinny)
     dy.set_option(dy.OPT_SKINNY_ONE_CHUNK, a.one_chunk)
-    cap = 2048
+    cap = max(2048, max(int(x) for x in a.rows.split(",")))
     for name, (N, K) in shapes.items():
         if name not in a.which.split(","):
             continue
