@@ -377,10 +377,11 @@ int gemm_launch(const GemmCall &g, int num_sms, cudaStream_t st) {
   // count both kernels are enqueued and each exits unless the count is in its regime.
   GemmCall s = g;
   if (g_skinny_enabled && skinny_eligible(g)) {
-    // host-known large M with a wide N (FullStep gate/up, QKV): the single-CTA 128x256 kernel
-    // measures ~10% faster there (profiles/r1c_gemm_split_sweep.txt); everything else -> skinny
-    const bool wide_full = !g.M_ptr && g.M_cap > 4096 && g.N >= 12288;
-    if (!g.M_ptr && g.M_cap <= kSkinnyMaxM && !wide_full) return gemm_skinny_launch(g, num_sms, st);
+    // every row count up to 16384, the FullStep's included: the CTA-pair 256-row weight tiles move
+    // 131 FLOP per L2 byte against the single-CTA 128x256 tiles' 87, and the L2 -> SM operand
+    // stream (~12 TB/s, tools/tma_probe.cu) bounds both (M = 15296: QKV 1225 vs 1481 us,
+    // gate/up 2417 vs 2862 us, profiles/r2/gemm_15296.txt)
+    if (!g.M_ptr && g.M_cap <= kSkinnyMaxM) return gemm_skinny_launch(g, num_sms, st);
     if (g.M_ptr) {
       int rc = gemm_skinny_launch(g, num_sms, st);
       if (rc) return rc;

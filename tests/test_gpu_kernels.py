@@ -39,7 +39,7 @@ def test_gemm_vs_torch(dy, ctx, M_cap, M, N, K):
     ref = A[:M].float() @ W.float().T
     got = D[:M].float()
     if M:
-        err = ((got - ref).abs().max() / ref.abs().max()).item()
+        err = ((got - ref).abs().amax(1) / ref.abs().amax(1).clamp_min(1e-30)).max().item()  # per row
         assert err < 1e-2, err
     assert torch.all(D[M:] == 7.0)            # rows beyond the device count untouched
 
@@ -74,7 +74,7 @@ def test_gemm_skinny_vs_torch(dy, ctx, skinny, M_cap, M, N, K):
             ref = A[:M].float() @ W.float().T + B.float()
             if resid is not None:
                 ref = ref + R[:M].float()
-            err = ((D[:M].float() - ref).abs().max() / ref.abs().max()).item()
+            err = ((D[:M].float() - ref).abs().amax(1) / ref.abs().amax(1).clamp_min(1e-30)).max().item()
             assert err < 1e-2, (resid is not None, err)
             assert torch.all(D[M:] == 7.0)
             # split-K partials are reduced in a fixed contributor order: bit-identical reruns
@@ -84,6 +84,20 @@ def test_gemm_skinny_vs_torch(dy, ctx, skinny, M_cap, M, N, K):
             assert torch.equal(D, D2)
     finally:
         dy.set_option(dy.OPT_SKINNY_GEMM, prev)
+
+
+@pytest.mark.parametrize("M,N,K", [(4608, 12288, 512), (15296, 512, 256)])
+def test_gemm_host_known_rows(dy, ctx, M, N, K):
+    """Host-known row counts (the FullStep's GEMMs, M up to 16384) on the CTA-pair kernel."""
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    A = (torch.randn(M, K, device="cuda", generator=g) * 0.5).bfloat16()
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    D = torch.empty((M, N), device="cuda").bfloat16()
+    ctx.gemm_bf16(A, W, D)
+    torch.cuda.synchronize()
+    ref = A.float() @ W.float().T
+    err = ((D.float() - ref).abs().amax(1) / ref.abs().amax(1).clamp_min(1e-30)).max().item()
+    assert err < 1e-2, err
 
 
 @pytest.mark.parametrize("S", [1, 2, 3, 4, 16, 64])
@@ -102,7 +116,7 @@ def test_gemm_skinny_split_granularity(dy, ctx, S, M, N, K):
         ctx.gemm_bf16(A, W, D, M_dev=Md, resid=R)
         torch.cuda.synchronize()
         ref = A[:M].float() @ W.float().T + R[:M].float()
-        err = ((D[:M].float() - ref).abs().max() / ref.abs().max()).item()
+        err = ((D[:M].float() - ref).abs().amax(1) / ref.abs().amax(1).clamp_min(1e-30)).max().item()
         assert err < 1e-2, err
         assert torch.all(D[M:] == 7.0)
     finally:

@@ -12,6 +12,7 @@ from gpu_helpers import (Model, bf16_round, from_dev, import_states, oracle_stat
 
 pytestmark = pytest.mark.gpu
 TOL = 2e-2
+S_TOL = 5e-3   # similarities: bf16 contexts, fp32 sums (the denoise-step tests' bar)
 BAND = 1e-3
 
 
@@ -121,7 +122,7 @@ def _teacher_forced_layer(name, layer, mode, frac_in=0.4, seed=0, select_mode=0,
     V_gpu = from_dev(cache.tensor(layer, dy.V))
     n_band = 0
     for s, ((r, lc), idx) in enumerate(zip(refs, idx_lists)):
-        assert np.abs(sim[s, row_lo:] - r.s).max() < 2e-2
+        assert np.abs(sim[s, row_lo:] - r.s).max() < S_TOL
         band = set(input_rows[np.abs(r.s - taus[s]) < BAND].tolist())
         n_band += len(band)
         got, ref = set(got_lists[s].tolist()), set(r.idx_out.tolist())
