@@ -170,3 +170,37 @@ def test_tp_denoise_steps_match_tp1(name, residual_mode, select_mode=1):
     # a fifth of the rows (the group's own rule is checked on every row above)
     print(f"{name}: band {band_n} of {compared} rows")
     assert band_n <= 0.8 * compared
+
+
+def test_tp_nccl_backend_single_rank_equals_plain_path():
+    """The NCCL backend (dlopen'd libnccl, ncclCommInitRank, ncclAllReduce with the list length read
+    back) with one rank: the group path — partial similarities, thresholding of the reduced sums,
+    O / down projections into scratch, all-reduce, scatter-back — reproduces the plain single-GPU
+    path bit for bit (a one-rank all-reduce is the identity)."""
+    m = Model("small128", qk_std=0.09, lm_std=0.25, select_mode=1)
+    cfg, run, dy = m.cfg, m.run, m.dyllm
+    b, N, nl = run.batch, run.N, cfg.n_layers
+    try:
+        uid = dy.TensorParallel.unique_id()
+    except dy.DyllmError as e:
+        pytest.skip(f"NCCL unavailable: {e}")
+    tp = dy.TensorParallel(m.ctx, 1, 0, uid)
+    c_tp = m.new_cache()
+    tp.attach(0, c_tp)
+    c_ref = m.new_cache()
+    prompts = gen.prompt_tokens(29, b, run.L_P, cfg.mask_id)
+    toks = torch.tensor(np.stack([np.concatenate([p, np.full(run.L_R, cfg.mask_id)]) for p in prompts]),
+                        dtype=torch.int32).cuda()
+    toks_tp = toks.clone()
+    dp, dt = (torch.full((b, run.n_u), -1, dtype=torch.int32, device="cuda") for _ in range(2))
+    dp2, dt2 = dp.clone(), dt.clone()
+    tau = np.full(nl, 0.25, np.float32)
+    for t in range(run.T_full + 8):
+        c_ref.denoise_step(t, tau, toks, dp, dt)
+        tp.denoise_step([m.w], t, tau, toks_tp, dp2, dt2)
+        torch.cuda.synchronize()
+        assert torch.equal(toks, toks_tp), t
+        for l in range(nl):
+            assert torch.equal(c_ref.export(l + 1, dy.H), c_tp.export(l + 1, dy.H)), (t, l)
+            assert torch.equal(c_ref.export(l, dy.CTX), c_tp.export(l, dy.CTX)), (t, l)
+    tp.close()
