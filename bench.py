@@ -459,7 +459,9 @@ def main():
     # every rank's generated tokens, gathered (rank order = global batch order)
     all_tokens = pd.gather_tokens(eng.tokens, b * world)
     assert all_tokens.shape == (b * world, N)
-    assert not bool((all_tokens[:, run.L_P:] == cfg.mask_id).any()), "masked tokens left after a generation"
+    left = (all_tokens[:, run.L_P:] == cfg.mask_id)
+    assert not bool(left.any()), ("masked tokens left after a generation: per sequence "
+                                  f"{left.sum(1).tolist()}, first positions {torch.nonzero(left)[:8].tolist()}")
 
     vals = [ms, ms_e2e] + ([ms_full] if ms_full is not None else [])
     vals = pd.max_over_ranks(vals, device=f"cuda:{local}")

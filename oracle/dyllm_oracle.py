@@ -326,20 +326,24 @@ def candidate_rows(tokens, cfg, run):
     return blk[tokens[blk] == cfg.mask_id]
 
 
-def process_logit(cand_pos, logits, n_u):
-    """process_logit (Alg. 1 line 20; D13).
+def process_logit(cand_pos, logits, n_u, mask_id=None):
+    """process_logit (Alg. 1 line 20; D13, D22).
 
-    confidence = max softmax probability = 1 / sum(exp(z - max)); token = argmax (lowest id on ties);
-    pick the min(n_u, |cand|) most confident positions, ties to the lowest position.
-    Returns (positions, tokens, confidences) in selection order.
+    token = argmax over the vocabulary without the mask token (lowest id on ties; D22: unmasking
+    commits a token, so [M] is never a prediction); confidence = that token's softmax probability
+    over the whole vocabulary = 1 / sum(exp(z - z_token)); pick the min(n_u, |cand|) most confident
+    positions, ties to the lowest position. Returns (positions, tokens, confidences) in selection order.
     """
     cand_pos = np.asarray(cand_pos, dtype=np.int64)
     if len(cand_pos) == 0:
         return cand_pos, np.zeros(0, dtype=np.int64), np.zeros(0)
     z = np.asarray(logits, dtype=np.float64)
-    m = z.max(axis=1)
+    za = z.copy()
+    if mask_id is not None:
+        za[:, mask_id] = -np.inf
+    tok = za.argmax(axis=1)
+    m = za.max(axis=1)
     conf = 1.0 / np.exp(z - m[:, None]).sum(axis=1)
-    tok = z.argmax(axis=1)
     order = sorted(range(len(cand_pos)), key=lambda i: (-conf[i], cand_pos[i]))[:n_u]
     order = np.asarray(order, dtype=np.int64)
     return cand_pos[order], tok[order], conf[order]
@@ -431,7 +435,7 @@ def denoise_step(st, W, cfg, run, t, tau, q_mode="cache", force_full=False):
         HL = sparse_step(st, W, cfg, run, mode, tau, q_mode=q_mode)
     cand = candidate_rows(st.tokens, cfg, run)
     logits = lm_logits(HL[cand], W, cfg) if len(cand) else np.zeros((0, cfg.vocab))
-    pos, tok, _ = process_logit(cand, logits, run.n_u)
+    pos, tok, _ = process_logit(cand, logits, run.n_u, cfg.mask_id)
     st.tokens[pos] = tok
     st.decoded_prev = np.sort(pos)
     return pos, tok

@@ -564,8 +564,10 @@ void dyllm_cache_destroy(dyllm_cache *c) {
 // ------------------------------------------------------------------ step internals
 static int gemm(dyllm_ctx *ctx, const int *M_ptr, int M_cap, int N, int K, const bf16 *A, const bf16 *W, bf16 *D,
                 int ldd, int epi, const bf16 *resid = nullptr, int ldr = 0, const int *resid_rows = nullptr,
-                const bf16 *bias = nullptr, float4 *partials = nullptr, const int *out_rows = nullptr) {
+                const bf16 *bias = nullptr, float4 *partials = nullptr, const int *out_rows = nullptr,
+                int excl_col = -1) {
   GemmCall g;
+  g.excl_col = excl_col;
   g.M_ptr = M_ptr;
   g.M_cap = M_cap;
   g.N = N;
@@ -956,14 +958,14 @@ static int unmask_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, i
     KL(GATHER, f32::gather_rmsnorm(fp(c->L[m.n_layers - 1].H), c->lm_rows, M_lm, lm_cap, w->g_final, m.rms_eps,
                                    fp(c->Xf), m.d_model, st));
     KL(LM_GEMM, f32::gemm(g32(M_lm, lm_cap, m.vocab, m.d_model, fp(c->Xf), w->lm_head, c->logits32, m.vocab), st));
-    KL(OTHER, f32::lm_reduce(c->logits32, M_lm, lm_cap, m.vocab, c->partials, st));
+    KL(OTHER, f32::lm_reduce(c->logits32, M_lm, lm_cap, m.vocab, m.mask_id, c->partials, st));
     KL(OTHER, launch_lm_select_commit(c->partials, 1, c->lm_rows, c->lm_off, r.batch, r.n_u, d_tokens, c->dec_prev,
                                       d_dec_tok, w->emb, nullptr, m.d_model, st, fp(c->H0)));
   } else {
   KL(GATHER, launch_gather_rmsnorm(HL, c->lm_rows, c->lm_off + r.batch, lm_cap, w->g_final, m.rms_eps, c->Xf,
                                    m.d_model, st));
   KL(LM_GEMM, RET(gemm(ctx, c->lm_off + r.batch, lm_cap, m.vocab, m.d_model, c->Xf, w->lm_head, nullptr, 0, EPI_LMHEAD,
-                       nullptr, 0, nullptr, nullptr, c->partials)));
+                       nullptr, 0, nullptr, nullptr, c->partials, nullptr, m.mask_id)));
   KL(OTHER, launch_lm_select_commit(c->partials, gemm_lmhead_ntiles(m.vocab), c->lm_rows, c->lm_off, r.batch, r.n_u,
                                     d_tokens, c->dec_prev, d_dec_tok, w->emb, c->H0, m.d_model, st));
   }

@@ -353,7 +353,7 @@ __global__ void threshold_compact_kernel(const float *__restrict__ sim, int batc
 // ---------------------------------------------------------------- a9: LM-head row reduction
 // One warp per candidate row: (max, sum exp(z - max), argmax with ties to the lowest id) in the
 // float4 partial layout of lm_select_commit_kernel (one tile per row).
-__global__ void lm_reduce_kernel(const float *__restrict__ logits, const int *__restrict__ M_ptr, int V,
+__global__ void lm_reduce_kernel(const float *__restrict__ logits, const int *__restrict__ M_ptr, int V, int excl,
                                  float4 *__restrict__ partials) {
   pdl_wait();
   const int M = *M_ptr;
@@ -362,8 +362,8 @@ __global__ void lm_reduce_kernel(const float *__restrict__ logits, const int *__
     const float *z = logits + static_cast<int64_t>(i) * V;
     float m = -INFINITY;
     int am = 0x7fffffff;
-    for (int c = lane; c < V; c += 32)
-      if (z[c] > m) {
+    for (int c = lane; c < V; c += 32)  // the mask token is never a prediction (D22)
+      if (c != excl && z[c] > m) {
         m = z[c];
         am = c;
       }
@@ -424,8 +424,8 @@ void select(const float *cn, float *cc, int batch, int N, int row_lo, int width,
   DY_CUDA_LAUNCH(launch_k(threshold_compact_kernel, dim3(1), dim3(1024), 0, st, 1, static_cast<const float *>(sim),
                           batch, N, row_lo, tau, cmp, frac, idx_out, off_out, counts));
 }
-void lm_reduce(const float *logits, const int *M_ptr, int M_cap, int V, float4 *partials, cudaStream_t st) {
-  DY_CUDA_LAUNCH(launch_k(lm_reduce_kernel, dim3(grid_cap(M_cap, 8)), dim3(256), 0, st, 1, logits, M_ptr, V,
+void lm_reduce(const float *logits, const int *M_ptr, int M_cap, int V, int excl, float4 *partials, cudaStream_t st) {
+  DY_CUDA_LAUNCH(launch_k(lm_reduce_kernel, dim3(grid_cap(M_cap, 8)), dim3(256), 0, st, 1, logits, M_ptr, V, excl,
                           partials));
 }
 

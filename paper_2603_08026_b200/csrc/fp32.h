@@ -51,7 +51,7 @@ void posmap(const int *idx, const int *M_ptr, int rows, int *pm, cudaStream_t st
 void attention(const F32Attn &a, cudaStream_t st);
 void select(const float *cn, float *cc, int batch, int N, int row_lo, int width, float tau, int cmp, float frac,
             float *sim, int *idx_out, int *off_out, int *counts, cudaStream_t st);
-void lm_reduce(const float *logits, const int *M_ptr, int M_cap, int V, float4 *partials, cudaStream_t st);
+void lm_reduce(const float *logits, const int *M_ptr, int M_cap, int V, int excl, float4 *partials, cudaStream_t st);
 
 }  // namespace f32
 }  // namespace dy

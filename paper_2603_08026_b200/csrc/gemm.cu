@@ -52,6 +52,7 @@ struct GemmParams {
   const int *out_rows;  // nullable: destination row of each output row (fused scatter-back, a8)
   float4 *partials;
   int m_skip_le;
+  int excl_col;  // EPI_LMHEAD: column left out of the max / argmax (the mask token, D22), -1: none
 };
 
 __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int &m, int &n) {
@@ -205,7 +206,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
       } else if constexpr (EPI == EPI_LMHEAD) {
-        float mx = -INFINITY, sm = 0.f;
+        // per row and 256-column tile: max and argmax over the columns except the mask token
+        // (D22: [M] is never a prediction), sum of exp(z - max) over every column (the
+        // probability of the chosen token is normalised over the whole vocabulary)
+        float mx = -INFINITY, sm = 0.f, zx = -INFINITY;
         int arg = 0;
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -214,7 +218,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int col = nb * BN + c0 + j;
-            if (col < p.N) {
+            if (col == p.excl_col) {
+              zx = v[j];
+            } else if (col < p.N) {
               const float z = v[j];
               if (z > mx) {
                 sm = sm * __expf(mx - z) + 1.f;
@@ -226,6 +232,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
           }
         }
+        if (zx > -INFINITY && mx > -INFINITY) sm += __expf(zx - mx);
         if (row_ok) p.partials[static_cast<int64_t>(row) * num_n + nb] = make_float4(mx, sm, __int_as_float(arg), 0.f);
       } else {
 #pragma unroll 1
@@ -353,7 +360,7 @@ static int launch_t(const GemmCall &g, int num_sms, cudaStream_t st) {
   rc = make_tmap(&tb, g.W, g.N, g.K, BN);
   if (rc) return rc;
   GemmParams p{g.M_ptr, g.M_cap, g.N, g.K, g.D, g.ldd, g.resid, g.ldr, g.resid_rows, g.bias, g.out_rows, g.partials,
-               g.m_skip_le};
+               g.m_skip_le, g.excl_col};
   const int max_tiles = ((g.M_cap + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   const int grid = max_tiles < num_sms ? max_tiles : num_sms;
   DY_CUDA(launch_k(kern, dim3(grid), dim3(kGemmThreads), C::SMEM_BYTES, st, 1, ta, tb, p));

@@ -45,7 +45,7 @@ constexpr int SK_A_BYTES = 128 * 256;        // <= 128 activation rows x 128 bf1
 constexpr int SK_STAGE = SK_W_BYTES + 2 * SK_A_BYTES;
 constexpr int SK_XCH = 2 * 32 * 128 * 4;     // epilogue transpose tiles: one [32 rows][128 weight rows] fp32 per half
 constexpr int SK_RING = SK_STAGES * SK_STAGE;  // 192 KB: 2 stages of 96 KB (M in (256, 512]) or 3 of 64 KB
-constexpr int SK_MAX_STAGES = SK_RING / (SK_W_BYTES + SK_A_BYTES);
+constexpr int SK_MAX_STAGES = 8;           // ring stages sized to the launch's activation rows (below)
 constexpr int SK_SMEM = 1024 + SK_RING + SK_XCH + 256;
 constexpr int SK_THREADS = 352;              // W producer, MMA, 8 epilogue warps, A producer
 constexpr int SKINNY_MAX_M = kSkinnyMaxM;
@@ -273,8 +273,11 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   const uint32_t stage_tx = 2u * (SK_W_BYTES + (NA0 / 2 + NA1 / 2) * 256);
   // ring: a stage holds 32 KB of weights + one (or, for M in (256, 512], two) 32 KB activation
   // slots; with one slot the same 192 KB hold 3 stages instead of 2
-  const int stage_bytes = NA1 ? SK_STAGE : SK_W_BYTES + SK_A_BYTES;
-  const int nstages = SK_RING / stage_bytes;
+  // a stage holds the weight box and exactly this launch's activation boxes (the second MMA's rows
+  // right after the first's), so fewer activation rows buy a deeper ring: the L2 -> SM latency of
+  // the 32 KB boxes is what a 3-stage ring exposes (the k-block time barely depends on the rows)
+  const int stage_bytes = (SK_W_BYTES + (NA0 / 2) * 256 + (NA1 / 2) * 256 + 1023) & ~1023;
+  const int nstages = min(SK_RING / stage_bytes, SK_MAX_STAGES);
   // Unsplit tiles (upi == 1) are dealt round-robin (pair p: tiles p, p + P, ...), so the pairs
   // running at the same time hold consecutive tiles (the activation chunks of one weight block:
   // its HBM read is shared through L2); split tiles use contiguous stream-K ranges.
@@ -335,7 +338,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             tma_load_3d_pair(sb + SK_W_BYTES, &maps.a[NA0 / 32 - 1], &full[st], 0,
                              arow + static_cast<int>(rank) * (NA0 / 2), kb * 2);
             if (NA1)
-              tma_load_3d_pair(sb + SK_W_BYTES + SK_A_BYTES, &maps.a[NA1 / 32 - 1], &full[st], 0,
+              tma_load_3d_pair(sb + SK_W_BYTES + (NA0 / 2) * 256, &maps.a[NA1 / 32 - 1], &full[st], 0,
                                256 + static_cast<int>(rank) * (NA1 / 2), kb * 2);
           }
           if (++st == nstages) {
@@ -378,7 +381,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
                              sw128_kmajor_desc(a0 + ch * (NA0 / 2 * 128) + ko), id0, accum);
               if (NA1)
                 umma_bf16_pair(acc + 256, sw128_kmajor_desc(w0 + ch * (128 * 128) + ko),
-                               sw128_kmajor_desc(a0 + SK_A_BYTES + ch * (NA1 / 2 * 128) + ko), id1, accum);
+                               sw128_kmajor_desc(a0 + (NA0 / 2) * 256 + ch * (NA1 / 2 * 128) + ko), id1, accum);
             }
             umma_commit_pair(&empty[st]);
             if (kb == sg.kb1 - 1) umma_commit_pair(&tfull[b]);

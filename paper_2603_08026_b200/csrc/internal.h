@@ -85,6 +85,7 @@ struct GemmCall {
   float4 *partials = nullptr;       // EPI_LMHEAD: [M_cap][n_tiles] (max, sumexp, argmax, 0)
   int epi = EPI_BF16;
   int m_skip_le = 0;  // standard kernel: do nothing when the device row count is <= this
+  int excl_col = -1;  // EPI_LMHEAD: column excluded from the max / argmax (the mask token, D22)
   float *ws = nullptr;  // skinny split-K workspace (skinny_ws_floats(num_sms) floats per ctx)
   int *ctr = nullptr;   // skinny split-K counters (kSkinnyCtrCap, zero between launches)
 };

@@ -67,11 +67,13 @@ def _check_decode(gp, gt, HL_rows, cand, W, cfg, n_u, rnd=bf16_round):
     if len(cand) == 0:
         return len(gp) == 0
     z = rnd(O.rms_norm(HL_rows, W["g_final"], cfg.rms_eps)) @ W["lm_head"].T
-    pos, tok, conf = O.process_logit(cand, z, n_u)
+    pos, tok, conf = O.process_logit(cand, z, n_u, cfg.mask_id)
     k = len(pos)
-    allc = np.sort(1.0 / np.exp(z - z.max(axis=1, keepdims=True)).sum(axis=1))[::-1]
+    zn = z.copy()
+    zn[:, cfg.mask_id] = -np.inf                     # D22: [M] is never a prediction
+    allc = np.sort(1.0 / np.exp(z - zn.max(axis=1, keepdims=True)).sum(axis=1))[::-1]
     chosen = np.searchsorted(cand, pos)
-    top2 = np.sort(z[chosen], axis=1)[:, -2:]
+    top2 = np.sort(zn[chosen], axis=1)[:, -2:]
     if (len(allc) > k and allc[k - 1] - allc[k] < CONF_RTOL * allc[k - 1]) or np.any(top2[:, 1] - top2[:, 0] < LOGIT_ATOL):
         return False
     assert sorted(gp.tolist()) == sorted(pos.tolist()), (gp, pos)

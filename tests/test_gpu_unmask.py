@@ -54,10 +54,12 @@ def test_unmask_matches_oracle(n_u):
     for s in range(b):
         cand = O.candidate_rows(toks[s], cfg, run)
         z = O.lm_logits(HL[s, cand].astype(np.float64), m.W, cfg)
-        pos_ref, tok_ref, conf_ref = O.process_logit(cand, z, n_u)
+        pos_ref, tok_ref, conf_ref = O.process_logit(cand, z, n_u, cfg.mask_id)
         k = len(pos_ref)
+        zn = z.copy()
+        zn[:, cfg.mask_id] = -np.inf                 # D22: [M] is never a prediction
         # ranking near-tie at the cut: the oracle's choice of positions is not decidable in bf16
-        conf_all = np.sort(1.0 / np.exp(z - z.max(axis=1, keepdims=True)).sum(axis=1))[::-1]
+        conf_all = np.sort(1.0 / np.exp(z - zn.max(axis=1, keepdims=True)).sum(axis=1))[::-1]
         cut_tie = k < len(cand) and abs(conf_all[k - 1] - conf_all[k]) <= 1e-3 * conf_all[k - 1]
         got_pos = pos_gpu[s][pos_gpu[s] >= 0] - s * N   # decoded row ids -> positions
         assert len(got_pos) == len(pos_ref)
@@ -66,7 +68,7 @@ def test_unmask_matches_oracle(n_u):
         else:
             assert sorted(got_pos.tolist()) == sorted(pos_ref.tolist()), (s, got_pos, pos_ref)
         for p, t in zip(pos_ref, tok_ref):
-            zz = np.sort(z[list(cand).index(p)])[::-1]
+            zz = np.sort(zn[list(cand).index(p)])[::-1]
             if zz[0] - zz[1] <= 2e-2:
                 excluded += 1
                 continue
@@ -80,3 +82,29 @@ def test_unmask_matches_oracle(n_u):
         keep[list(got_pos)] = False
         assert np.array_equal(t_gpu[s, keep], toks[s, keep])
     assert excluded <= b * (n_u + 1) // 2
+
+
+def test_mask_token_never_committed_on_gpu():
+    """D22 on the GPU (LM-head epilogue leaves the mask column out of the max / argmax, keeps it in
+    the normaliser): a model whose masked rows all score [M] highest still unmasks min(n_u,
+    remaining) positions per step, never writes the mask id, and finishes the generation."""
+    m = Model("tiny")
+    cfg, run, dy = m.cfg, m.run, m.dyllm
+    u = np.random.default_rng(0).standard_normal(cfg.d_model)
+    u /= np.linalg.norm(u)
+    W = dict(m.W)
+    W["emb"], W["lm_head"] = m.W["emb"].copy(), m.W["lm_head"].copy()
+    W["emb"][cfg.mask_id], W["lm_head"][cfg.mask_id] = 5.0 * u, 2.0 * u
+    w = dy.Weights.from_blob(m.ctx, cfg, dy.blob_from_weights(cfg, W))
+    eng = dy.Engine(m.ctx, w, run)
+    prompts = torch.tensor(gen.prompt_tokens(2, run.batch, run.L_P, cfg.mask_id), dtype=torch.int32)
+    eng.load_prompts(prompts.cuda())
+    left = run.L_R
+    for t in range(run.T_total):
+        eng.cache.denoise_step(t, np.full(cfg.n_layers, 0.99, np.float32), eng.tokens, eng.dec_pos, eng.dec_tok)
+        torch.cuda.synchronize()
+        n_dec = int((eng.dec_pos >= 0).sum())
+        assert n_dec == run.batch * min(run.n_u, left), t
+        assert cfg.mask_id not in eng.dec_tok.cpu().numpy().ravel().tolist()
+        left -= min(run.n_u, left)
+    assert not bool((eng.tokens[:, run.L_P:] == cfg.mask_id).any())

@@ -229,6 +229,52 @@ def test_process_logit_brute_force():
         assert t.tolist() == [int(np.argmax(z[i])) for i in brute]
 
 
+def test_process_logit_never_commits_the_mask_token():
+    """D22: even when [M] has the largest logit, the committed token is the best other one and its
+    confidence is its probability over the whole vocabulary (brute force)."""
+    rng = np.random.default_rng(5)
+    V, mask = 9, 8
+    pos = np.arange(30, 36)
+    z = rng.standard_normal((6, V))
+    z[:, mask] = z.max(axis=1) + 1.0 + rng.random(6)          # the mask logit dominates every row
+    p, t, c = O.process_logit(pos, z, 3, mask_id=mask)
+    probs = np.exp(z) / np.exp(z).sum(1, keepdims=True)
+    best = np.argmax(np.where(np.arange(V) == mask, -np.inf, z), axis=1)
+    conf = probs[np.arange(6), best]
+    brute = sorted(range(6), key=lambda i: (-round(conf[i], 12), pos[i]))[:3]
+    assert mask not in t.tolist()
+    assert p.tolist() == [pos[i] for i in brute]
+    assert t.tolist() == [int(best[i]) for i in brute]
+    assert np.allclose(c, conf[brute], rtol=1e-12)
+
+
+def test_generation_unmasks_exactly_n_u_per_step_with_a_dominant_mask_logit():
+    """S:347 budget under D22: a model whose LM head favours [M] still unmasks min(n_u, remaining)
+    positions every step and never writes the mask id."""
+    from dataclasses import replace
+    from synth import configs, gen
+    cfg, run = configs.preset("tiny")
+    W = gen.model_weights(cfg, 1)
+    # [M]'s embedding and LM-head row share a direction that the residual stream of every masked
+    # row carries: [M] wins every masked row's logits
+    u = np.random.default_rng(0).standard_normal(cfg.d_model)
+    u /= np.linalg.norm(u)
+    W["emb"], W["lm_head"] = W["emb"].copy(), W["lm_head"].copy()
+    W["emb"][cfg.mask_id], W["lm_head"][cfg.mask_id] = 5.0 * u, 2.0 * u
+    st0 = O.init_state(gen.prompt_tokens(2, run.batch, run.L_P, cfg.mask_id)[0], cfg, run)
+    HL = O.full_step(st0, W, cfg)
+    cand = O.candidate_rows(st0.tokens, cfg, run)
+    assert np.all(O.lm_logits(HL[cand], W, cfg).argmax(1) == cfg.mask_id)
+    prompts = gen.prompt_tokens(2, run.batch, run.L_P, cfg.mask_id)
+    st = O.init_state(prompts[0], cfg, run)
+    left = run.L_R
+    for t in range(run.T_total):
+        pos, tok = O.denoise_step(st, W, cfg, run, t, 0.99)
+        assert len(pos) == min(run.n_u, left) and cfg.mask_id not in tok.tolist()
+        left -= len(pos)
+    assert not np.any(st.tokens == cfg.mask_id)
+
+
 def test_process_logit_all_equal_picks_lowest_positions():
     pos = np.array([40, 41, 42, 43])
     p, t, _ = O.process_logit(pos, np.zeros((4, 5)), 2)
