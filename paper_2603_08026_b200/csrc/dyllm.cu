@@ -555,8 +555,11 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
   return DYLLM_OK;
 }
 
+static void tp_forget(dyllm_tp *tp, const dyllm_cache *c);  // tensor-parallel group bookkeeping (below)
+
 void dyllm_cache_destroy(dyllm_cache *c) {
   if (!c) return;
+  if (c->tp) tp_forget(c->tp, c);  // a group must not keep a destroyed shard
   for (void *p : c->allocs) cudaFree(p);
   delete c;
 }
@@ -1137,6 +1140,11 @@ struct dyllm_tp {
   std::vector<dyllm_cache *> shard;  // loopback: world shards; NCCL: this rank's
   int *h_cnt = nullptr;              // pinned: device row counts read back for NCCL
 };
+
+static void tp_forget(dyllm_tp *tp, const dyllm_cache *c) {
+  for (dyllm_cache *&sh : tp->shard)
+    if (sh == c) sh = nullptr;
+}
 
 // Sum of a per-shard buffer over the group, in shard order, left in every shard's buffer.
 // buf_of(c): the shard's buffer; M_ptr (nullable): shard 0's device row count; width: elements per row.
