@@ -149,6 +149,18 @@ def measured_traffic(cls, sparse_t, run):
     return (n_ro * t["ro"] + n_fi * t["fi"]) / max(n_ro + n_fi, 1)
 
 
+def arm_config(args, run, world, taus=None):
+    """The `config` object of both arms' JSON lines (the reference arm times the same workload)."""
+    return {"workload": f"{args.config}: L_P={run.L_P} L_R={run.L_R} block={run.block} "
+                        f"n_u={run.n_u} T={run.T_total} (T_full={run.T_full}, period={run.full_period}); "
+                        f"random-init bf16 weights; one step = one full generation",
+            "global_batch": run.batch * world, "per_gpu_batch": run.batch, "seq_len": run.N,
+            "parallelism": f"dp{world} (batch-parallel replicas)",
+            "l2": "inputs larger than L2 (14 GB of weights streamed per denoising step)",
+            "selection": (f"fraction-controlled f={args.frac} per layer and sequence (D19)" if taus is None
+                          else f"fixed tau per layer {np.round(taus, 6).tolist()}")}
+
+
 # ----------------------------------------------------------------------------- CPU oracle leg
 def cpu_oracle_sample(cfg, run, seconds: float, frac: float, seed: int = 0):
     """Time the oracle (as it stands) on one sequence of the bench workload: one response-only
@@ -235,7 +247,12 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    from dataclasses import replace as _replace
     cfg, run = configs.preset(args.config)
+    if args.batch:
+        run = _replace(run, batch=args.batch)
+    if args.n_u:
+        run = _replace(run, n_u=args.n_u)
     vals = []
     for _ in range(args.warmup + args.steps):
         vals.append(cpu_oracle_sample(cfg, run, args.cpu_seconds / 4, args.frac))
@@ -245,7 +262,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * run.L_R / v,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": f"{args.config} oracle sample", "batch": 1},
+        "data": "synthetic", "config": arm_config(args, run, args.gpus),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": base["cores"], "kind": "oracle",
                          "sample": base["sample"]},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -553,14 +570,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"{args.config}: L_P={run.L_P} L_R={run.L_R} block={run.block} "
-                                   f"n_u={run.n_u} T={T} (T_full={run.T_full}, period={run.full_period}); "
-                                   f"random-init bf16 weights; one step = one full generation",
-                       "global_batch": b * world, "per_gpu_batch": b, "seq_len": N,
-                       "parallelism": f"dp{world} (batch-parallel replicas)",
-                       "l2": "inputs larger than L2 (14 GB of weights streamed per denoising step)",
-                       "selection": (f"fraction-controlled f={args.frac} per layer and sequence (D19)" if fmode
-                                     else f"fixed tau per layer {np.round(taus, 6).tolist()}")},
+            "config": arm_config(args, run, world, None if fmode else taus),
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(b * run.L_P * 4),
                     "d2h_bytes_per_step": int(b * N * 4)},
             "gpu_launches": int(launches),
