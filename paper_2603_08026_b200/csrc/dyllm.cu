@@ -1556,6 +1556,10 @@ int dyllm_debug_trace_buffer(int which, void *d_buf) {
     g_attn_events = static_cast<unsigned long long *>(d_buf);
     return DYLLM_OK;
   }
+  if (which == 3) {
+    g_sel_trace = static_cast<unsigned long long *>(d_buf);
+    return DYLLM_OK;
+  }
   set_error("unknown trace buffer");
   return DYLLM_E_ARG;
 }

@@ -154,5 +154,6 @@ extern bool g_attn_fused_enabled;  // test hook (dyllm_set_option)
 extern int g_attn_t4_rows;        // fused attention: exact-row items of <= this many rows run transposed (0: off)
 extern unsigned long long *g_attn_trace;  // debug hook (dyllm_debug_trace_buffer, which = 1)
 extern unsigned long long *g_attn_events;  // debug hook (dyllm_debug_trace_buffer, which = 2)
+extern unsigned long long *g_sel_trace;    // debug hook (dyllm_debug_trace_buffer, which = 3)
 
 }  // namespace dy

@@ -8,6 +8,8 @@
 
 namespace dy {
 
+unsigned long long *g_sel_trace = nullptr;  // debug hook (dyllm_debug_trace_buffer, which = 3)
+
 // ============================================================================ a0: embeddings
 // H0[r] = E[tokens[r]] for every row r of the list (or all rows when rows == nullptr).
 __global__ void embed_rows_kernel(const int *__restrict__ tokens, const int *__restrict__ rows,
@@ -456,16 +458,32 @@ __global__ void build_u_kernel(const int *__restrict__ idx_in, const int *__rest
 // sequences and writes the packed list + offsets (no second launch, no host sync).
 constexpr int kSelRowsPerCta = 32;
 
-constexpr int kSelThreads = 1024;  // 32 warps: one input row per warp
+#ifndef DYLLM_SEL_THREADS
+#define DYLLM_SEL_THREADS 512
+#endif
+// 16 warps, two of the CTA's 32 rows each, 16 16-byte loads in flight per lane (the 1024-thread
+// variant held 8: 64 registers per thread)
+constexpr int kSelThreads = DYLLM_SEL_THREADS;
 constexpr int kSelWarps = kSelThreads / 32;
+constexpr int kSelU = kSelThreads >= 1024 ? 4 : 8;
 
 __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
     const bf16 *__restrict__ c_new, bf16 *__restrict__ c_cache, int N, int row_lo, int width, float tau,
     int cmp, float frac, int *__restrict__ idx_out, int *__restrict__ off_out, float *__restrict__ sim_out,
     unsigned *__restrict__ masks, unsigned *__restrict__ ticket, int *__restrict__ counts_out,
     const uint32_t *__restrict__ rowflag, uint32_t tag, const int *__restrict__ dl_off,
-    const float4 *__restrict__ cos_part, int H, float4 *__restrict__ part_out) {
+    const float4 *__restrict__ cos_part, int H, float4 *__restrict__ part_out, unsigned long long *trace) {
   pdl_wait();
+  // debug hook (dyllm_debug_trace_buffer which = 3): %globaltimer per CTA at start / end of its rows,
+  // and of the last CTA's tail: [cta][4]
+  auto stamp = [&](int slot) {
+    if (trace && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[(blockIdx.y * gridDim.x + blockIdx.x) * 4 + slot] = t;
+    }
+  };
+  stamp(0);
   __shared__ unsigned row_flag[kSelRowsPerCta];
   __shared__ bool is_last;
   const int s = blockIdx.y;
@@ -474,8 +492,7 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
   const int nchunks = gridDim.x;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nv = width / 8;
-  {
-    const int rr = warp;  // one row per warp (32 warps = the CTA's 32 rows)
+  for (int rr = warp; rr < kSelRowsPerCta; rr += kSelWarps) {  // the CTA's 32 rows over its warps
     const int p = row_lo + chunk * kSelRowsPerCta + rr;
     unsigned f = 0;
     if (p < N && cos_part) {
@@ -512,7 +529,7 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
         add = !take_new && dl_off[s + 1] > dl_off[s];
       }
       float dot = 0.f, na = 0.f, nb = 0.f;
-      constexpr int U = 4;  // 2*U independent 16-byte loads in flight per lane
+      constexpr int U = kSelU;  // 2*U independent 16-byte loads in flight per lane
       for (int c0 = lane; c0 < nv; c0 += 32 * U) {
         uint4 ua[U], ub[U];
         // both rows are loaded unconditionally (no dependence on the row-kind loads above); an
@@ -575,6 +592,7 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
   // and compaction run after the all-reduce (cos_part mode, H = 1), identically on every shard
   if (part_out) return;
   __syncthreads();
+  stamp(1);
   __shared__ bool seq_last;
   if (threadIdx.x < 32) {
     const unsigned m = __ballot_sync(0xffffffffu, row_flag[threadIdx.x] != 0);
@@ -592,117 +610,98 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
   const int batch = gridDim.y;
   if (seq_last) {
     __threadfence();
-  {
-      // fraction-controlled mode (D19): per sequence, tau* = the similarity of rank k = round(f*L)
-      // (0-based) found by an 8-bit radix select over the order-preserving uint32 keys of s, then
-      // the masks are rebuilt as s < tau* (k rows when there are no ties), s <= tau* under cmp = 1.
-      __shared__ unsigned hist[kSelWarps][256];
-      if (warp == 0) {
-        const int sq = s;
-        const float *sv = sim_out + static_cast<int64_t>(sq) * N + row_lo;
-        const int k = static_cast<int>(floorf(frac * L + 0.5f));
-        // the sequence's similarities, loaded once (all loads in flight together) into registers:
-        // element j of lane l is row j*32 + l (L <= 1024; longer inputs stream from L2 per pass)
-        constexpr int kRegRows = 32;
-        const bool in_regs = L <= 32 * kRegRows;
-        float sreg[kRegRows];
-  #pragma unroll
-        for (int j = 0; j < kRegRows; ++j) {
-          const int i = j * 32 + lane;
-          sreg[j] = (in_regs && i < L) ? __ldcg(sv + i) : INFINITY;
-        }
-        auto key_of = [](float f) {
-          const uint32_t u = __float_as_uint(f);
-          return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-        };
-        float thr = INFINITY;
-        if (k < L) {
-          uint32_t prefix = 0, pmask = 0;
-          int rank = k;
-          for (int shift = 24; shift >= 0; shift -= 8) {
-            for (int i = lane; i < 256; i += 32) hist[warp][i] = 0;
-            __syncwarp();
-            if (in_regs) {
-              // similarities cluster in a few top-byte bins: lanes with equal digits are merged
-              // (match.any) so each bin takes one shared-memory atomic per instruction instead of
-              // up to 32 serialised ones
-  #pragma unroll
-              for (int j = 0; j < kRegRows; ++j) {
-                if (j * 32 >= L) break;
-                const uint32_t key = key_of(sreg[j]);
-                const bool in = j * 32 + lane < L && (key & pmask) == prefix;
-                const unsigned act = __ballot_sync(0xffffffffu, in);
-                if (in) {
-                  const uint32_t dig = (key >> shift) & 255u;
-                  const unsigned same = __match_any_sync(act, dig);
-                  if (lane == __ffs(same) - 1) atomicAdd(&hist[warp][dig], static_cast<unsigned>(__popc(same)));
-                }
-              }
-            } else {
-              for (int i = lane; i < L; i += 32) {
-                const uint32_t key = key_of(__ldcg(sv + i));
-                if ((key & pmask) == prefix) atomicAdd(&hist[warp][(key >> shift) & 255u], 1u);
-              }
-            }
-            __syncwarp();
-            unsigned loc[8], sum = 0;
-  #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              loc[j] = hist[warp][lane * 8 + j];
-              sum += loc[j];
-            }
-            unsigned incl = sum;
-  #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
-              if (lane >= o) incl += t;
-            }
-            const unsigned excl = incl - sum;
-            const bool mine = static_cast<unsigned>(rank) >= excl && static_cast<unsigned>(rank) < incl;
-            const unsigned bal = __ballot_sync(0xffffffffu, mine);
-            const int src = __ffs(bal) - 1;
-            int digit = 0, nrank = 0;
-            if (lane == src) {
-              unsigned c = excl;
-              for (int j = 0; j < 8; ++j) {
-                if (static_cast<unsigned>(rank) < c + loc[j]) {
-                  digit = lane * 8 + j;
-                  nrank = rank - static_cast<int>(c);
-                  break;
-                }
-                c += loc[j];
-              }
-            }
-            digit = __shfl_sync(0xffffffffu, digit, src);
-            rank = __shfl_sync(0xffffffffu, nrank, src);
-            prefix |= static_cast<uint32_t>(digit) << shift;
-            pmask |= 255u << shift;
-            __syncwarp();
-          }
-          const uint32_t u = (prefix & 0x80000000u) ? (prefix & 0x7FFFFFFFu) : ~prefix;
-          thr = __uint_as_float(u);
-        }
-        if (in_regs) {
-  #pragma unroll
-          for (int w = 0; w < kRegRows; ++w) {
-            if (w < nchunks) {
-              const bool fl = w * 32 + lane < L && (cmp ? sreg[w] <= thr : sreg[w] < thr);
-              const unsigned m = __ballot_sync(0xffffffffu, fl);
-              if (lane == 0) masks[sq * nchunks + w] = m;
-            }
-          }
-        } else {
-          for (int w = 0; w < nchunks; ++w) {
-            const int i = w * kSelRowsPerCta + lane;
-            const float sv_i = i < L ? __ldcg(sv + i) : INFINITY;
-            const bool fl = i < L && (cmp ? sv_i <= thr : sv_i < thr);
-            const unsigned m = __ballot_sync(0xffffffffu, fl);
-            if (lane == 0) masks[sq * nchunks + w] = m;
-          }
-        }
-      }
-      __syncthreads();
+    // fraction-controlled mode (D19): tau* = the similarity of rank k = round(f*L) (0-based) of
+    // this sequence, found by an 8-bit radix select over the order-preserving uint32 keys of s
+    // with the whole CTA (each pass: a shared histogram of the candidates' next digit, one warp
+    // scans it); then the masks are rebuilt as s < tau* (k rows when there are no ties), s <= tau*
+    // under cmp = 1. (One warp per sequence measured 14 / 27 us per response-only / full-input
+    // launch between the last rows and the compaction, tools/select_trace.py.)
+    __shared__ unsigned hist[256];
+    __shared__ uint32_t sh_prefix;
+    __shared__ int sh_rank;
+    const float *sv = sim_out + static_cast<int64_t>(s) * N + row_lo;
+    const int k = static_cast<int>(floorf(frac * L + 0.5f));
+    auto key_of = [](float f) {
+      const uint32_t u = __float_as_uint(f);
+      return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    };
+    constexpr int kPer = 4;  // similarities per thread kept in registers (L <= 4 * kSelThreads)
+    const bool in_regs = L <= kPer * kSelThreads;
+    uint32_t keyr[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = threadIdx.x + j * kSelThreads;
+      keyr[j] = (in_regs && i < L) ? key_of(__ldcg(sv + i)) : 0u;
     }
+    float thr = INFINITY;
+    if (k < L) {
+      uint32_t prefix = 0, pmask = 0;
+      int rank = k;
+      for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int i = threadIdx.x; i < 256; i += kSelThreads) hist[i] = 0;
+        __syncthreads();
+        auto count = [&](uint32_t key, bool valid) {
+          const bool in = valid && (key & pmask) == prefix;
+          const unsigned act = __ballot_sync(0xffffffffu, in);
+          if (in) {  // lanes with the same digit merged: one shared atomic per digit and warp
+            const uint32_t dig = (key >> shift) & 255u;
+            const unsigned same = __match_any_sync(act, dig);
+            if (lane == __ffs(same) - 1) atomicAdd(&hist[dig], static_cast<unsigned>(__popc(same)));
+          }
+        };
+        if (in_regs) {
+#pragma unroll
+          for (int j = 0; j < kPer; ++j) count(keyr[j], threadIdx.x + j * kSelThreads < L);
+        } else {
+          for (int i0 = 0; i0 < L; i0 += kSelThreads) {
+            const int i = i0 + threadIdx.x;
+            count(i < L ? key_of(__ldcg(sv + i)) : 0u, i < L);
+          }
+        }
+        __syncthreads();
+        if (warp == 0) {
+          unsigned loc[8], sum = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            loc[j] = hist[lane * 8 + j];
+            sum += loc[j];
+          }
+          unsigned incl = sum;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+          }
+          const unsigned excl = incl - sum;
+          if (static_cast<unsigned>(rank) >= excl && static_cast<unsigned>(rank) < incl) {
+            unsigned cnt = excl;
+            for (int j = 0; j < 8; ++j) {
+              if (static_cast<unsigned>(rank) < cnt + loc[j]) {
+                sh_prefix = prefix | (static_cast<uint32_t>(lane * 8 + j) << shift);
+                sh_rank = rank - static_cast<int>(cnt);
+                break;
+              }
+              cnt += loc[j];
+            }
+          }
+        }
+        __syncthreads();
+        prefix = sh_prefix;
+        rank = sh_rank;
+        pmask |= 255u << shift;
+      }
+      const uint32_t u = (prefix & 0x80000000u) ? (prefix & 0x7FFFFFFFu) : ~prefix;
+      thr = __uint_as_float(u);
+    }
+    for (int w = warp; w < nchunks; w += kSelWarps) {
+      const int i = w * kSelRowsPerCta + lane;
+      const float x = i < L ? __ldcg(sv + i) : INFINITY;
+      const bool fl = i < L && (cmp ? x <= thr : x < thr);
+      const unsigned m = __ballot_sync(0xffffffffu, fl);
+      if (lane == 0) masks[s * nchunks + w] = m;
+    }
+    __threadfence();
+    __syncthreads();
     if (threadIdx.x == 0) {
       ticket[1 + s] = 0u;  // re-arm (stream-ordered)
       __threadfence();
@@ -711,6 +710,7 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
     __syncthreads();
   }
   if (!is_last) return;
+  stamp(2);
   // ---- last CTA: scan all masks (b * nchunks words) and emit the packed list
   __threadfence();
   const int nwords = batch * nchunks;
@@ -757,6 +757,7 @@ __global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
   }
   (void)nwords;
   if (threadIdx.x == 0) *ticket = 0u;  // re-arm for the next launch (stream-ordered)
+  stamp(3);
 }
 
 // ============================================================================ TP: loopback all-reduce
@@ -1025,7 +1026,8 @@ void launch_select(const bf16 *c_new, bf16 *c_cache, int batch, int N, int row_l
   const int L = N - row_lo;
   dim3 grid((L + kSelRowsPerCta - 1) / kSelRowsPerCta, batch);
   DY_CUDA_LAUNCH(launch_k(select_salient_kernel, dim3(grid), dim3(kSelThreads), 0, st, 1, c_new, c_cache, N, row_lo, width, tau, cmp, frac, idx_out, off_out,
-                                              sim_out, masks, ticket, counts, rowflag, tag, dl_off, cos_part, H, part_out));
+                                              sim_out, masks, ticket, counts, rowflag, tag, dl_off, cos_part, H, part_out,
+                                              g_sel_trace));
 }
 void launch_lm_candidates(const int *tokens, int batch, int L_P, int L_R, int block, int mask_id, int *rows, int *off,
                           cudaStream_t st) {
