@@ -330,6 +330,12 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int NKT = (p.N + FA_BK - 1) / FA_BK;
+  // fixup launch with an empty list (the common case): leave before any setup (no barrier init,
+  // no TMEM allocation), so the step's next kernel follows right away
+  if (p.mode == 1) {
+    pdl_wait();
+    if (*reinterpret_cast<volatile const int *>(p.fix) == 0) return;
+  }
   // event roles: 0 MMA, 1 softmax warp 2, 2 producer warp 0, 3 V producer
   FaEv ev;
   {
@@ -371,16 +377,6 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
   pdl_trigger();  // grid <= #SMs at one CTA per SM: resident, the next kernel may launch
-  // fixup launch with an empty list (the common case): nothing to claim, no counters touched
-  if (p.mode == 1 && *reinterpret_cast<volatile const int *>(p.fix) == 0) {
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1) {
-      tc_fence_after();
-      tmem_dealloc(tmem, FA_TMEM_COLS);
-    }
-    return;
-  }
   // Dynamic scheduling: the producer thread claims items with an atomic counter (items of one
   // (sequence, kv head) stay adjacent in claim order, so concurrently running CTAs share K/V in L2,
   // and heavy exact-row items no longer pile up on fixed CTAs) and passes them to the other roles

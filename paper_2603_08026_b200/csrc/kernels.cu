@@ -997,7 +997,10 @@ void launch_qkv_post(const bf16 *qkv, const int *idx, const int *M_ptr, int M_ca
                      uint32_t *dtag, uint32_t epoch) {
   const int g = M_cap < 148 * 4 ? M_cap : 148 * 4;  // one row per CTA per pass; capped like grid_for
   const int work = std::max((H + KVH) * (hd / 16), KVH * hd / 8);  // vectors per row of each part
-  const int threads = std::min(1024, std::max(32, (work + 31) / 32 * 32));
+#ifndef DYLLM_QKVPOST_THREADS
+#define DYLLM_QKVPOST_THREADS 256  // two work items per thread, every row of a response-only step resident at once
+#endif
+  const int threads = std::min(DYLLM_QKVPOST_THREADS, std::max(32, (work + 31) / 32 * 32));
   DY_CUDA_LAUNCH(launch_k(qkv_post_kernel, dim3(g > 0 ? g : 1), dim3(threads), 0, st, 1, qkv, idx, M_ptr, M_cap, bias, N, H, KVH, hd, rope_cs, Qc, Kc, Vc,
                                                  dV, Qx, Kx, Kxo, rowflag, tag, q_only, Kfi, dtag, epoch));
 }

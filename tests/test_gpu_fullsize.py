@@ -34,7 +34,7 @@ TOL = 2e-2      # north_star bar for hidden states (H rows), K/V/Q rows
 C_TOL = 3e-2
 BAND = 1e-3
 SEED = 3
-CHECK_SEQS = (0, 7, 15)
+CHECK_SEQS = (0, 3, 7, 11, 15)   # oracle recomputations per full-size case (the others: list counts)
 STD = {"cK": 1.25, "cQ": 1.5, "cV": 1.25, "cC": 0.1, "cH": 1.0, "cX": 1.0}
 
 
