@@ -458,21 +458,20 @@ __global__ void build_u_kernel(const int *__restrict__ idx_in, const int *__rest
 // sequences and writes the packed list + offsets (no second launch, no host sync).
 constexpr int kSelRowsPerCta = 32;
 
-#ifndef DYLLM_SEL_THREADS
-#define DYLLM_SEL_THREADS 512
-#endif
-// 16 warps, two of the CTA's 32 rows each, 16 16-byte loads in flight per lane (the 1024-thread
-// variant held 8: 64 registers per thread)
-constexpr int kSelThreads = DYLLM_SEL_THREADS;
-constexpr int kSelWarps = kSelThreads / 32;
-constexpr int kSelU = kSelThreads >= 1024 ? 4 : 8;
-
-__global__ void __launch_bounds__(kSelThreads) select_salient_kernel(
+// Two shapes of the same kernel, chosen by the input length: response-only launches (few CTAs:
+// one per SM) run 512 threads = 16 warps x 2 of the CTA's 32 rows with 16 16-byte loads in flight
+// per lane; full-input launches (30 CTAs per sequence) run 256 threads = 8 warps x 4 rows with 8
+// loads in flight and 64 registers, four CTAs per SM, so that all of them are resident at once
+// (with one 512-thread CTA per SM, 480 CTAs took 3.24 waves).
+template <int kSelThreads>
+__global__ void __launch_bounds__(kSelThreads, kSelThreads >= 512 ? 1 : 4) select_salient_kernel(
     const bf16 *__restrict__ c_new, bf16 *__restrict__ c_cache, int N, int row_lo, int width, float tau,
     int cmp, float frac, int *__restrict__ idx_out, int *__restrict__ off_out, float *__restrict__ sim_out,
     unsigned *__restrict__ masks, unsigned *__restrict__ ticket, int *__restrict__ counts_out,
     const uint32_t *__restrict__ rowflag, uint32_t tag, const int *__restrict__ dl_off,
     const float4 *__restrict__ cos_part, int H, float4 *__restrict__ part_out, unsigned long long *trace) {
+  constexpr int kSelWarps = kSelThreads / 32;
+  constexpr int kSelU = kSelThreads >= 512 ? 8 : 4;
   pdl_wait();
   // debug hook (dyllm_debug_trace_buffer which = 3): %globaltimer per CTA at start / end of its rows,
   // and of the last CTA's tail: [cta][4]
@@ -1028,9 +1027,11 @@ void launch_select(const bf16 *c_new, bf16 *c_cache, int batch, int N, int row_l
                    const float4 *cos_part, int H, float4 *part_out) {
   const int L = N - row_lo;
   dim3 grid((L + kSelRowsPerCta - 1) / kSelRowsPerCta, batch);
-  DY_CUDA_LAUNCH(launch_k(select_salient_kernel, dim3(grid), dim3(kSelThreads), 0, st, 1, c_new, c_cache, N, row_lo, width, tau, cmp, frac, idx_out, off_out,
-                                              sim_out, masks, ticket, counts, rowflag, tag, dl_off, cos_part, H, part_out,
-                                              g_sel_trace));
+  const bool wide = L > 512;
+  DY_CUDA_LAUNCH(launch_k(wide ? select_salient_kernel<256> : select_salient_kernel<512>, dim3(grid),
+                          dim3(wide ? 256 : 512), 0, st, 1, c_new, c_cache, N, row_lo, width, tau, cmp, frac, idx_out,
+                          off_out, sim_out, masks, ticket, counts, rowflag, tag, dl_off, cos_part, H, part_out,
+                          g_sel_trace));
 }
 void launch_lm_candidates(const int *tokens, int batch, int L_P, int L_R, int block, int mask_id, int *rows, int *off,
                           cudaStream_t st) {
