@@ -262,11 +262,13 @@ __device__ __forceinline__ void cp_async_8(void *smem, const void *gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-// bar.sync is .aligned: every thread of the warp must execute it converged (compute-sanitizer
-// synccheck flagged a warp that had not reconverged after a lane-0 mbarrier arrive)
+// Named barrier of a TMEM lane quadrant's softmax warps. The non-.aligned form: the warps of a
+// quadrant reach it from different code paths (e.g. type-3 warps with and without changed keys in
+// their columns), which bar.sync (= barrier.sync.aligned) does not allow (compute-sanitizer
+// synccheck); each warp is converged when it arrives.
 __device__ __forceinline__ void fa_named_sync(int id, int n) {
   __syncwarp();
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 // debug event log (compiled in with -DDYLLM_ATTN_EVENTS=1, tools/attn_events.py): one 8192-entry

@@ -534,6 +534,10 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
                   cudaMemsetAsync(c->Qx, 0, rows * qw * c->es, st) == cudaSuccess &&
                   cudaMemsetAsync(c->zero_off, 0, (r->batch + 1) * sizeof(int), st) == cudaSuccess;
   bool ok2 = ok;
+  // list buffers start defined (whole-capacity copies of partly used lists, e.g. the carried set,
+  // would otherwise read uninitialised tails: compute-sanitizer initcheck)
+  for (int i = 0; i < 2; ++i) ok2 = ok2 && cudaMemsetAsync(c->lst[i], 0, rows * sizeof(int), st) == cudaSuccess;
+  ok2 = ok2 && cudaMemsetAsync(c->carried, 0, rows * sizeof(int), st) == cudaSuccess;
   for (auto &L : c->L)
     if (L.dtag) ok2 = ok2 && cudaMemsetAsync(L.dtag, 0, rows * sizeof(uint32_t), st) == cudaSuccess;
   if (c->Kun)
