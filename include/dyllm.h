@@ -294,7 +294,14 @@ uint64_t dyllm_launch_count(void);
  * (SURVEY §8f1, D20). 0 = dense prompt tiles. */
 enum { DYLLM_OPT_SKINNY_GEMM = 1, DYLLM_OPT_SKINNY_SPLIT = 2, DYLLM_OPT_ATTN_FUSED = 3, DYLLM_OPT_SKINNY_ONE_CHUNK = 4,
        DYLLM_OPT_PDL = 5, DYLLM_OPT_ATTN_INC = 6, DYLLM_OPT_ATTN_T4 = 7, DYLLM_OPT_ATTN_PINC = 8,
-       DYLLM_OPT_ATTN_COS = 9, DYLLM_OPT_SKINNY_CHUNK = 10 };
+       DYLLM_OPT_ATTN_COS = 9, DYLLM_OPT_SKINNY_CHUNK = 10, DYLLM_OPT_SKINNY_KROT = 11,
+       DYLLM_OPT_SKINNY_DEBUG = 12 };
+/* DYLLM_OPT_SKINNY_DEBUG (default 0; measurement only, results are garbage when set): bit 0 runs
+ * the skinny kernel without its operand TMA loads, bit 1 without its MMAs. */
+/* DYLLM_OPT_SKINNY_KROT (default 0): the skinny kernel walks the k-blocks of a weight block's
+ * segment starting at (block index x value) mod its k-block count, so that the pairs running
+ * at the same time read different parts of the shared activation rows (same sums, another
+ * accumulation order). */
 /* DYLLM_OPT_SKINNY_CHUNK (default 0 = 256): largest number of activation rows per chunk of the
  * skinny GEMM when the rows are chunked (tuning hook). */
 /* DYLLM_OPT_ATTN_COS (default 0, measured slower): head_dim-128 sparse steps form C_new, commit it to the C cache and

@@ -1528,6 +1528,16 @@ int dyllm_set_option(int option, int value) {
     g_skinny_chunk_rows = value < 0 ? 0 : value;
     return prev;
   }
+  if (option == DYLLM_OPT_SKINNY_DEBUG) {
+    const int prev = g_skinny_dbg;
+    g_skinny_dbg = value & 15;
+    return prev;
+  }
+  if (option == DYLLM_OPT_SKINNY_KROT) {
+    const int prev = g_skinny_krot;
+    g_skinny_krot = value < 0 ? 0 : value;
+    return prev;
+  }
   if (option == DYLLM_OPT_ATTN_COS) {
     const int prev = g_attn_fuse_cos ? 1 : 0;
     g_attn_fuse_cos = value != 0;

@@ -123,6 +123,9 @@ struct SkinnyParams {
   int one_chunk_max;  // largest M kept in ONE activation chunk (two MMAs per k-step above 256
                       // rows, single-buffered accumulator); above: chunks of <= 256 rows
   int chunk_rows;     // test hook: largest rows per activation chunk when chunked (0: 256)
+  int krot;           // k-block start offset per weight block (x block index, mod the segment's k-blocks)
+  int dbg;            // measurement hook: bit 0 skips the operand TMA loads, bit 1 the MMAs, bit 2 the
+                      // epilogue's global stores, bit 3 its shared-memory transpose
 };
 
 // Stream-K partition of the (item, k-block) space: pair p owns units [start(p), start(p+1)).
@@ -171,6 +174,18 @@ struct SkIter {
     return true;
   }
 };
+
+// k-block order of a segment: starts at an offset that depends on the weight block, so that pairs
+// running at the same time read different k-blocks of the shared activation rows
+__device__ __forceinline__ int sk_rot(const SkSeg &s, int nchunk, int krot) {
+  const int n = s.kb1 - s.kb0;
+  return n > 0 ? (s.item / nchunk) * krot % n : 0;
+}
+__device__ __forceinline__ int sk_kb(const SkSeg &s, int j, int rot) {
+  const int n = s.kb1 - s.kb0;
+  const int q = j + rot;
+  return s.kb0 + (q >= n ? q - n : q);
+}
 
 // tensor maps: weights (box 128 rows) and activations (box 16 * (i + 1) rows, i = 0..7: one op
 // loads exactly a CTA's half of the activation rows of an MMA, whatever the device-side M)
@@ -307,16 +322,18 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       // hit L2 (only the first activation chunk's pair prefetches a weight block)
       SkIter pit = it;
       SkSeg ps{0, 0, 0};
-      int pkb = 0;
+      int pkb = 0, prot = 0;
       int64_t n_pf = 0, n_ld = 0;
       auto prefetch_ahead = [&]() {
         while (n_pf < n_ld + kSkPrefetch) {
           if (pkb >= ps.kb1) {
             if (!pit.next(ps)) return;
             pkb = ps.kb0;
+            prot = sk_rot(ps, nchunk, p.krot);
           }
           if (ps.item % nchunk == 0)
-            tma_prefetch_l2_3d(&maps.w, 0, ps.item / nchunk * 256 + static_cast<int>(rank) * 128, pkb * 2);
+            tma_prefetch_l2_3d(&maps.w, 0, ps.item / nchunk * 256 + static_cast<int>(rank) * 128,
+                               sk_kb(ps, pkb - ps.kb0, prot) * 2);
           ++pkb;
           ++n_pf;
         }
@@ -325,10 +342,14 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       while (it.next(sg)) {
         const int wrow = sg.item / nchunk * 256 + static_cast<int>(rank) * 128;
         const int arow = sg.item % nchunk * R;  // first activation row of the tile
-        for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
+        const int rot = sk_rot(sg, nchunk, p.krot);
+        for (int j = 0; j < sg.kb1 - sg.kb0; ++j) {
+          const int kb = sk_kb(sg, j, rot);
           mbar_wait(&empty[st], ph ^ 1);
           uint8_t *sb = stages + st * stage_bytes;
-          if (wprod) {
+          if (p.dbg & 1) {
+            if (wprod && rank == 0) mbar_arrive(&full[st]);
+          } else if (wprod) {
             if (rank == 0) mbar_expect_tx(&full[st], stage_tx);
             tma_load_3d_pair(sb, &maps.w, &full[st], 0, wrow, kb * 2);
             ++n_ld;
@@ -365,16 +386,17 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         const uint32_t acc = tmem_base + b * 256;
         mbar_wait(&tempty[b], tph ^ 1);
         tc_fence_after();
-        for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
+        const int nkb = sg.kb1 - sg.kb0;
+        for (int j = 0; j < nkb; ++j) {
           mbar_wait(&full[st], ph);
           tc_fence_after();
           if (lane == 0) {
             const uint32_t w0 = smem_u32(stages + st * stage_bytes);
             const uint32_t a0 = w0 + SK_W_BYTES;
-            const uint32_t first = (kb == sg.kb0) ? 1u : 0u;
+            const uint32_t first = (j == 0) ? 1u : 0u;
             // k-step kk: 64-column chunk kk / 4 (chunk stride = box rows x 128 B), +32 B per 16
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
+            for (int kk = 0; kk < ((p.dbg & 2) ? 0 : 8); ++kk) {
               const uint32_t accum = (first && kk == 0) ? 0u : 1u;
               const uint32_t ko = (kk & 3) * 32, ch = kk >> 2;
               umma_bf16_pair(acc, sw128_kmajor_desc(w0 + ch * (128 * 128) + ko),
@@ -384,7 +406,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
                                sw128_kmajor_desc(a0 + (NA0 / 2) * 256 + ch * (NA1 / 2 * 128) + ko), id1, accum);
             }
             umma_commit_pair(&empty[st]);
-            if (kb == sg.kb1 - 1) umma_commit_pair(&tfull[b]);
+            if (j == nkb - 1) umma_commit_pair(&tfull[b]);
           }
           __syncwarp();
           if (++st == nstages) {
@@ -414,10 +436,13 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
     // Register slot i holds the float4 at (row m0 + sl_m(i), weight rows sl_n(i)..+3): SwiGLU
     // slots 0-3 gate, 4-7 up (weight rows [0,64) gate, [64,128) up of the same 64 FFN channels).
     constexpr bool kSw = EPI == EPI_SWIGLU;
-    const int n4 = kSw ? (t & 15) : (t & 31);
-    const int msub = kSw ? (t >> 4) : (t >> 5);
-    auto sl_m = [&](int i) { return kSw ? msub + 8 * (i & 3) : msub + 4 * i; };
-    auto sl_n = [&](int i) { return kSw ? (i < 4 ? 4 * n4 : 64 + 4 * n4) : 4 * n4; };
+    // SwiGLU: 16 threads per row x 4 channels (8-byte stores of 4 outputs, gate and up slots);
+    // otherwise 16 threads per row x 8 output columns (16-byte stores: a warp writes two rows'
+    // 256-byte segments per instruction)
+    const int n4 = t & 15;
+    const int msub = t >> 4;
+    auto sl_m = [&](int i) { return kSw ? msub + 8 * (i & 3) : msub + 8 * (i >> 1); };
+    auto sl_n = [&](int i) { return kSw ? (i < 4 ? 4 * n4 : 64 + 4 * n4) : 8 * n4 + 4 * (i & 1); };
     auto store = [&](const float4 r[8], int m0, int tile) {
       const int item = tile / nchunk;  // weight block (output columns)
       m0 += tile % nchunk * R;         // output rows of the tile's activation chunk
@@ -435,28 +460,38 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           }
         }
       } else {
-        const int n = item * 256 + static_cast<int>(rank) * 128 + 4 * n4;
-        float bb[4] = {0.f, 0.f, 0.f, 0.f};
+        const int n = item * 256 + static_cast<int>(rank) * 128 + 8 * n4;
+        float bb[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         if (p.bias) {
-          const uint2 bv = *reinterpret_cast<const uint2 *>(p.bias + n);
-          const float2 b01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&bv.x));
-          const float2 b23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&bv.y));
-          bb[0] = b01.x; bb[1] = b01.y; bb[2] = b23.x; bb[3] = b23.y;
+          const uint4 bv = *reinterpret_cast<const uint4 *>(p.bias + n);
+          const uint32_t bw[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&bw[q]));
+            bb[2 * q] = f.x;
+            bb[2 * q + 1] = f.y;
+          }
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int m = m0 + sl_m(i);
+        for (int i = 0; i < 4; ++i) {
+          const int m = m0 + sl_m(2 * i);
           if (m < M) {
-            float o[4] = {r[i].x + bb[0], r[i].y + bb[1], r[i].z + bb[2], r[i].w + bb[3]};
+            const float4 a = r[2 * i], b = r[2 * i + 1];
+            float o[8] = {a.x + bb[0], a.y + bb[1], a.z + bb[2], a.w + bb[3],
+                          b.x + bb[4], b.y + bb[5], b.z + bb[6], b.w + bb[7]};
             if constexpr (EPI == EPI_RESID) {
               const int rr = p.resid_rows ? p.resid_rows[m] : m;
-              const uint2 rv = *reinterpret_cast<const uint2 *>(p.resid + static_cast<int64_t>(rr) * p.ldr + n);
-              const float2 r01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&rv.x));
-              const float2 r23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&rv.y));
-              o[0] += r01.x; o[1] += r01.y; o[2] += r23.x; o[3] += r23.y;
+              const uint4 rv = *reinterpret_cast<const uint4 *>(p.resid + static_cast<int64_t>(rr) * p.ldr + n);
+              const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&rw[q]));
+                o[2 * q] += f.x;
+                o[2 * q + 1] += f.y;
+              }
             }
-            *reinterpret_cast<uint2 *>(p.D + static_cast<int64_t>(p.out_rows ? p.out_rows[m] : m) * p.ldd + n) =
-                make_uint2(pack2(o[0], o[1]), pack2(o[2], o[3]));
+            *reinterpret_cast<uint4 *>(p.D + static_cast<int64_t>(p.out_rows ? p.out_rows[m] : m) * p.ldd + n) =
+                make_uint4(pack2(o[0], o[1]), pack2(o[2], o[3]), pack2(o[4], o[5]), pack2(o[6], o[7]));
           }
         }
       }
@@ -465,6 +500,13 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
     // this half's tile and store it. The leading barrier also orders the previous chunk's tile
     // reads before this chunk's writes.
     auto transpose_store = [&](const float v[32], int m0, int item) {
+      if (p.dbg & 8) {
+        float4 r[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        if (!(p.dbg & 4)) store(r, m0, item);
+        return;
+      }
       named_bar_sync(1 + half, 128);
 #pragma unroll
       for (int j = 0; j < 32; ++j) x[j * 128 + row] = v[j];
@@ -473,7 +515,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       float4 r[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) r[i] = x4[sl_m(i) * 32 + sl_n(i) / 4];
-      store(r, m0, item);
+      if (!(p.dbg & 4)) store(r, m0, item);
     };
     // split-K partials, TMEM-native layout: slot-major, then rank, then [16 chunks][8][128 n]
     // float4 (element j of a thread's 32 values at [j / 4][n]), so every warp store / load of one
@@ -665,7 +707,8 @@ static int launch_skinny_t(const GemmCall &g, int num_sms, cudaStream_t st) {
   // count: the kernel derives them; the grid is every co-resident pair
   SkinnyParams p{g.M_ptr, g.M_cap, g.N, g.K, g.D, g.ldd, g.resid, g.ldr, g.resid_rows, g.bias, g.out_rows, g.ws, g.ctr,
                  max_pairs,
-                 g_skinny_trace, g_skinny_split, g_skinny_one_chunk > 0 ? g_skinny_one_chunk : -1, g_skinny_chunk_rows};
+                 g_skinny_trace, g_skinny_split, g_skinny_one_chunk > 0 ? g_skinny_one_chunk : -1, g_skinny_chunk_rows,
+                 g_skinny_krot, g_skinny_dbg};
   DY_CUDA(launch_k(kern, dim3(2 * max_pairs), dim3(SK_THREADS), SK_SMEM, st, 2, maps, p));
   return DYLLM_OK;
 }
@@ -674,9 +717,14 @@ unsigned long long *g_skinny_trace = nullptr;
 int g_skinny_split = 0;
 int g_skinny_one_chunk = 0;  // 0: automatic
 int g_skinny_chunk_rows = 0;  // 0: 256
+int g_skinny_krot = 0;
+int g_skinny_dbg = 0;
 
 bool skinny_eligible(const GemmCall &g) {
-  return g.N % 256 == 0 && g.K % SK_KB == 0 && (g.epi == EPI_BF16 || g.epi == EPI_RESID || g.epi == EPI_SWIGLU);
+  // the epilogue stores 16-byte row segments (8 output columns) and reads bias / residual alike
+  const auto a16 = [](const void *q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  return g.N % 256 == 0 && g.K % SK_KB == 0 && (g.epi == EPI_BF16 || g.epi == EPI_RESID || g.epi == EPI_SWIGLU) &&
+         g.ldd % 8 == 0 && a16(g.D) && (!g.resid || (g.ldr % 8 == 0 && a16(g.resid))) && (!g.bias || a16(g.bias));
 }
 
 int gemm_skinny_launch(const GemmCall &g, int num_sms, cudaStream_t st) {

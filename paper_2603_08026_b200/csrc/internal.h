@@ -102,6 +102,8 @@ inline int64_t skinny_ws_floats(int num_sms) { return static_cast<int64_t>(num_s
 extern bool g_skinny_enabled;  // test hook (dyllm_set_option)
 extern unsigned long long *g_skinny_trace;
 extern int g_skinny_split;
+extern int g_skinny_dbg;         // measurement hook: 1 no operand loads, 2 no MMAs
+extern int g_skinny_krot;        // k-block start offset per weight block (dyllm_set_option)
 extern int g_skinny_chunk_rows;  // test hook: largest rows per activation chunk (dyllm_set_option)
 extern int g_skinny_one_chunk;  // test hook: largest M in one activation chunk (dyllm_set_option)  // test hook: units per weight block (0 = auto)  // debug hook (dyllm_debug_trace_buffer)
 int gemm_skinny_launch(const GemmCall &g, int num_sms, cudaStream_t st);  // gemm_skinny.cu

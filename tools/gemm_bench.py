@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--which", default="qkv,o,gu,down")
     ap.add_argument("--one-chunk", type=int, default=0, help="largest M in one activation chunk (0 auto)")
     ap.add_argument("--chunk", default="0", help="comma list of largest rows per activation chunk (0 = 256)")
+    ap.add_argument("--dbg", type=int, default=0, help="skinny measurement hook: 1 no loads, 2 no MMAs")
+    ap.add_argument("--krot", default="0", help="comma list of k-block rotations per weight block (0 = none)")
     a = ap.parse_args()
     cfg, _ = configs.preset(a.config)
     d, F = cfg.d_model, cfg.d_ff
@@ -38,6 +40,7 @@ def main():
     ctx = dy.Context(0)
     dy.set_option(dy.OPT_SKINNY_GEMM, a.skinny)
     dy.set_option(dy.OPT_SKINNY_ONE_CHUNK, a.one_chunk)
+    dy.set_option(dy.OPT_SKINNY_DEBUG, a.dbg)
     cap = max(2048, max(int(x) for x in a.rows.split(",")))
     for name, (N, K) in shapes.items():
         if name not in a.which.split(","):
@@ -45,10 +48,12 @@ def main():
         W = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
         A = torch.randn(cap, K, device="cuda").bfloat16()
         D = torch.empty(cap, N, device="cuda").bfloat16()
-        for M, S, CR in [(int(x), int(y), int(z)) for x in a.rows.split(",") for y in a.split.split(",")
-                         for z in a.chunk.split(",")]:
+        ref = {}
+        for M, S, CR, KR in [(int(x), int(y), int(z), int(r)) for x in a.rows.split(",") for y in a.split.split(",")
+                             for z in a.chunk.split(",") for r in a.krot.split(",")]:
             dy.set_option(dy.OPT_SKINNY_SPLIT, S)
             dy.set_option(dy.OPT_SKINNY_CHUNK, CR)
+            dy.set_option(dy.OPT_SKINNY_KROT, KR)
             Md = torch.tensor([M], dtype=torch.int32, device="cuda")
             for _ in range(3):
                 ctx.gemm_bf16(A, W, D, M_dev=Md)
@@ -61,7 +66,12 @@ def main():
             ctx.profile(False)
             tf = 2.0 * M * N * K / us / 1e6
             gbs = 2.0 * N * K / us / 1e3
-            print(f"{name:5s} N={N:6d} K={K:6d} M={M:5d} S={S:3d} C={CR:3d}: {us:8.2f} us  {tf:7.1f} TFLOP/s  weights {gbs:7.1f} GB/s")
+            out = D[:M].float()
+            if M not in ref:
+                ref[M] = out.clone()
+            dev = float((out - ref[M]).abs().max() / ref[M].abs().max().clamp_min(1e-30))
+            print(f"{name:5s} N={N:6d} K={K:6d} M={M:5d} S={S:3d} C={CR:3d} R={KR:2d}: {us:8.2f} us  {tf:7.1f} TFLOP/s  "
+                  f"weights {gbs:7.1f} GB/s  dev {dev:.1e}")
 
 
 if __name__ == "__main__":

@@ -18,8 +18,14 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--which", default="o")
 ap.add_argument("--rows", type=int, default=410)
 ap.add_argument("--split", type=int, default=0, help="units per weight block (0 = auto)")
+ap.add_argument("--one-chunk", type=int, default=0, help="largest M in one activation chunk (0 = auto)")
+ap.add_argument("--dbg", type=int, default=0, help="1 no operand loads, 2 no MMAs")
+ap.add_argument("--per-cta", action="store_true", help="also print every CTA's stamps")
 a = ap.parse_args()
 dy.set_option(dy.OPT_SKINNY_SPLIT, a.split)
+dy.set_option(dy.OPT_SKINNY_DEBUG, a.dbg)
+if a.one_chunk:
+    dy.set_option(dy.OPT_SKINNY_ONE_CHUNK, a.one_chunk)
 shapes = {"qkv": (12288, 4096), "o": (4096, 4096), "gu": (24576, 4096), "down": (4096, 12288)}
 N, K = shapes[a.which]
 ctx = dy.Context(0)
@@ -37,6 +43,7 @@ torch.cuda.synchronize()
 dy.lib().dyllm_debug_trace_buffer(0, None)
 t = tr.view(148, 16).cpu().numpy().astype(np.float64)
 valid = t[:, 0] > 0
+ids = np.nonzero(valid)[0]
 t = t[valid]
 t0 = t[:, 0].min()
 rel = np.where(t > 0, (t - t0) / 1e3, np.nan)
@@ -48,3 +55,6 @@ for i, n in enumerate(names):
     if np.all(np.isnan(col)):
         continue
     print(f"  {n:10s} min {np.nanmin(col):7.2f}  med {np.nanmedian(col):7.2f}  max {np.nanmax(col):7.2f} us")
+if a.per_cta:
+    for i, row in zip(ids, rel):
+        print(f"  cta {i:3d} " + " ".join("   -   " if np.isnan(v) else f"{v:7.2f}" for v in row[:12]))
