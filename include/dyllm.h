@@ -295,7 +295,9 @@ uint64_t dyllm_launch_count(void);
 enum { DYLLM_OPT_SKINNY_GEMM = 1, DYLLM_OPT_SKINNY_SPLIT = 2, DYLLM_OPT_ATTN_FUSED = 3, DYLLM_OPT_SKINNY_ONE_CHUNK = 4,
        DYLLM_OPT_PDL = 5, DYLLM_OPT_ATTN_INC = 6, DYLLM_OPT_ATTN_T4 = 7, DYLLM_OPT_ATTN_PINC = 8,
        DYLLM_OPT_ATTN_COS = 9, DYLLM_OPT_SKINNY_CHUNK = 10, DYLLM_OPT_SKINNY_KROT = 11,
-       DYLLM_OPT_SKINNY_DEBUG = 12 };
+       DYLLM_OPT_SKINNY_DEBUG = 12, DYLLM_OPT_SKINNY_KB = 13 };
+/* DYLLM_OPT_SKINNY_KB (default 0 = 128): k-block width of the skinny kernel's shared-memory ring
+ * stages, 128 or 64 columns (64: half-size stages, twice as many in flight). */
 /* DYLLM_OPT_SKINNY_DEBUG (default 0; measurement only, results are garbage when set): bit 0 runs
  * the skinny kernel without its operand TMA loads, bit 1 without its MMAs. */
 /* DYLLM_OPT_SKINNY_KROT (default 0): the skinny kernel walks the k-blocks of a weight block's

@@ -1528,6 +1528,11 @@ int dyllm_set_option(int option, int value) {
     g_skinny_chunk_rows = value < 0 ? 0 : value;
     return prev;
   }
+  if (option == DYLLM_OPT_SKINNY_KB) {
+    const int prev = g_skinny_kb;
+    g_skinny_kb = value == 64 ? 64 : 0;
+    return prev;
+  }
   if (option == DYLLM_OPT_SKINNY_DEBUG) {
     const int prev = g_skinny_dbg;
     g_skinny_dbg = value & 15;

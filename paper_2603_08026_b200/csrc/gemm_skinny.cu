@@ -210,9 +210,13 @@ __device__ __forceinline__ void tma_prefetch_l2_3d(const void *tmap, int c0, int
                : "memory");
 }
 
-template <int EPI>
+// CH = 64-column chunks per k-block: 2 (128-wide k-blocks, one 32 KB weight op per stage) or 1
+// (64-wide k-blocks: half-size stages, twice as many in the same ring)
+template <int EPI, int CH>
 __global__ void __launch_bounds__(SK_THREADS, 1)
     gemm_skinny_kernel(const __grid_constant__ SkMaps maps, const SkinnyParams p) {
+  constexpr int kWBytes = 128 * 128 * CH;  // 128 weight rows x CH chunks of 64 bf16
+  constexpr int kRowBytes = 128 * CH;      // one activation row of a stage
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t *stages = smem;
@@ -271,7 +275,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   const int nchunk = one ? 1 : (M + crow - 1) / crow;
   const int R = nchunk == 1 ? M : (((M + nchunk - 1) / nchunk + 31) & ~31);
   const int items = p.N / 256 * nchunk;
-  const int num_kb = p.K / SK_KB;
+  const int num_kb = p.K / (64 * CH);
   // split granularity (stream-K units per tile), from the device-side M: tiles are cut into
   // S units when there are fewer tiles than pairs (S = pairs / tiles), so all pairs stream
   int upi = p.S_force > 0 ? p.S_force : max(1, p.P_max / items);
@@ -285,13 +289,13 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   const int NA1 = (nchunk == 1 && M > 256) ? ((M - 256 + 31) & ~31) : 0;
   // M <= 256: two 256-column TMEM accumulators (epilogue of segment i overlaps the MMAs of i+1)
   const int nbuf = NA1 ? 1 : 2;
-  const uint32_t stage_tx = 2u * (SK_W_BYTES + (NA0 / 2 + NA1 / 2) * 256);
+  const uint32_t stage_tx = 2u * (kWBytes + (NA0 / 2 + NA1 / 2) * kRowBytes);
   // ring: a stage holds 32 KB of weights + one (or, for M in (256, 512], two) 32 KB activation
   // slots; with one slot the same 192 KB hold 3 stages instead of 2
   // a stage holds the weight box and exactly this launch's activation boxes (the second MMA's rows
   // right after the first's), so fewer activation rows buy a deeper ring: the L2 -> SM latency of
   // the 32 KB boxes is what a 3-stage ring exposes (the k-block time barely depends on the rows)
-  const int stage_bytes = (SK_W_BYTES + (NA0 / 2) * 256 + (NA1 / 2) * 256 + 1023) & ~1023;
+  const int stage_bytes = (kWBytes + (NA0 / 2) * kRowBytes + (NA1 / 2) * kRowBytes + 1023) & ~1023;
   const int nstages = min(SK_RING / stage_bytes, SK_MAX_STAGES);
   // Unsplit tiles (upi == 1) are dealt round-robin (pair p: tiles p, p + P, ...), so the pairs
   // running at the same time hold consecutive tiles (the activation chunks of one weight block:
@@ -333,7 +337,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           }
           if (ps.item % nchunk == 0)
             tma_prefetch_l2_3d(&maps.w, 0, ps.item / nchunk * 256 + static_cast<int>(rank) * 128,
-                               sk_kb(ps, pkb - ps.kb0, prot) * 2);
+                               sk_kb(ps, pkb - ps.kb0, prot) * CH);
           ++pkb;
           ++n_pf;
         }
@@ -351,16 +355,16 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             if (wprod && rank == 0) mbar_arrive(&full[st]);
           } else if (wprod) {
             if (rank == 0) mbar_expect_tx(&full[st], stage_tx);
-            tma_load_3d_pair(sb, &maps.w, &full[st], 0, wrow, kb * 2);
+            tma_load_3d_pair(sb, &maps.w, &full[st], 0, wrow, kb * CH);
             ++n_ld;
             prefetch_ahead();
           } else {
             // this CTA's half of the activation rows of each MMA: one op of exactly that many rows
-            tma_load_3d_pair(sb + SK_W_BYTES, &maps.a[NA0 / 32 - 1], &full[st], 0,
-                             arow + static_cast<int>(rank) * (NA0 / 2), kb * 2);
+            tma_load_3d_pair(sb + kWBytes, &maps.a[NA0 / 32 - 1], &full[st], 0,
+                             arow + static_cast<int>(rank) * (NA0 / 2), kb * CH);
             if (NA1)
-              tma_load_3d_pair(sb + SK_W_BYTES + (NA0 / 2) * 256, &maps.a[NA1 / 32 - 1], &full[st], 0,
-                               256 + static_cast<int>(rank) * (NA1 / 2), kb * 2);
+              tma_load_3d_pair(sb + kWBytes + (NA0 / 2) * kRowBytes, &maps.a[NA1 / 32 - 1], &full[st], 0,
+                               256 + static_cast<int>(rank) * (NA1 / 2), kb * CH);
           }
           if (++st == nstages) {
             st = 0;
@@ -392,18 +396,18 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           tc_fence_after();
           if (lane == 0) {
             const uint32_t w0 = smem_u32(stages + st * stage_bytes);
-            const uint32_t a0 = w0 + SK_W_BYTES;
+            const uint32_t a0 = w0 + kWBytes;
             const uint32_t first = (j == 0) ? 1u : 0u;
             // k-step kk: 64-column chunk kk / 4 (chunk stride = box rows x 128 B), +32 B per 16
 #pragma unroll
-            for (int kk = 0; kk < ((p.dbg & 2) ? 0 : 8); ++kk) {
+            for (int kk = 0; kk < ((p.dbg & 2) ? 0 : 4 * CH); ++kk) {
               const uint32_t accum = (first && kk == 0) ? 0u : 1u;
               const uint32_t ko = (kk & 3) * 32, ch = kk >> 2;
               umma_bf16_pair(acc, sw128_kmajor_desc(w0 + ch * (128 * 128) + ko),
                              sw128_kmajor_desc(a0 + ch * (NA0 / 2 * 128) + ko), id0, accum);
               if (NA1)
                 umma_bf16_pair(acc + 256, sw128_kmajor_desc(w0 + ch * (128 * 128) + ko),
-                               sw128_kmajor_desc(a0 + (NA0 / 2) * 256 + ch * (NA1 / 2 * 128) + ko), id1, accum);
+                               sw128_kmajor_desc(a0 + (NA0 / 2) * kRowBytes + ch * (NA1 / 2 * 128) + ko), id1, accum);
             }
             umma_commit_pair(&empty[st]);
             if (j == nkb - 1) umma_commit_pair(&tfull[b]);
@@ -656,9 +660,9 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   }
 }
 
-template <int EPI>
+template <int EPI, int CH>
 static int launch_skinny_t(const GemmCall &g, int num_sms, cudaStream_t st) {
-  auto kern = gemm_skinny_kernel<EPI>;
+  auto kern = gemm_skinny_kernel<EPI, CH>;
   static DeviceOnce attr_done;
   static int max_pairs_dev[DeviceOnce::kMaxDev] = {};
   cudaLaunchConfig_t cfg{};
@@ -698,10 +702,10 @@ static int launch_skinny_t(const GemmCall &g, int num_sms, cudaStream_t st) {
     // boxes taller than the (16-rounded) capacity are never selected: clamp them to stay encodable
     const int cap16 = (g.M_cap + 15) / 16 * 16;
     const int box = 16 * (i + 1) < cap16 ? 16 * (i + 1) : cap16;
-    int rc = make_tmap3(&maps.a[i], g.A, g.M_cap, g.K, box, 2);
+    int rc = make_tmap3(&maps.a[i], g.A, g.M_cap, g.K, box, CH);
     if (rc) return rc;
   }
-  int rc = make_tmap3(&maps.w, g.W, g.N, g.K, 128, 2);
+  int rc = make_tmap3(&maps.w, g.W, g.N, g.K, 128, CH);
   if (rc) return rc;
   // the tile count (hence the split and the number of pairs used) depends on the device-side row
   // count: the kernel derives them; the grid is every co-resident pair
@@ -719,6 +723,7 @@ int g_skinny_one_chunk = 0;  // 0: automatic
 int g_skinny_chunk_rows = 0;  // 0: 256
 int g_skinny_krot = 0;
 int g_skinny_dbg = 0;
+int g_skinny_kb = 0;  // k-block width: 0 / 128 (default) or 64
 
 bool skinny_eligible(const GemmCall &g) {
   // the epilogue stores 16-byte row segments (8 output columns) and reads bias / residual alike
@@ -728,10 +733,17 @@ bool skinny_eligible(const GemmCall &g) {
 }
 
 int gemm_skinny_launch(const GemmCall &g, int num_sms, cudaStream_t st) {
+  if (g_skinny_kb == 64) {
+    switch (g.epi) {
+      case EPI_SWIGLU: return launch_skinny_t<EPI_SWIGLU, 1>(g, num_sms, st);
+      case EPI_RESID: return launch_skinny_t<EPI_RESID, 1>(g, num_sms, st);
+      default: return launch_skinny_t<EPI_BF16, 1>(g, num_sms, st);
+    }
+  }
   switch (g.epi) {
-    case EPI_SWIGLU: return launch_skinny_t<EPI_SWIGLU>(g, num_sms, st);
-    case EPI_RESID: return launch_skinny_t<EPI_RESID>(g, num_sms, st);
-    default: return launch_skinny_t<EPI_BF16>(g, num_sms, st);
+    case EPI_SWIGLU: return launch_skinny_t<EPI_SWIGLU, 2>(g, num_sms, st);
+    case EPI_RESID: return launch_skinny_t<EPI_RESID, 2>(g, num_sms, st);
+    default: return launch_skinny_t<EPI_BF16, 2>(g, num_sms, st);
   }
 }
 

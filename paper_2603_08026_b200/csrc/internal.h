@@ -102,6 +102,7 @@ inline int64_t skinny_ws_floats(int num_sms) { return static_cast<int64_t>(num_s
 extern bool g_skinny_enabled;  // test hook (dyllm_set_option)
 extern unsigned long long *g_skinny_trace;
 extern int g_skinny_split;
+extern int g_skinny_kb;          // skinny k-block width: 0 / 128 or 64 (dyllm_set_option)
 extern int g_skinny_dbg;         // measurement hook: 1 no operand loads, 2 no MMAs
 extern int g_skinny_krot;        // k-block start offset per weight block (dyllm_set_option)
 extern int g_skinny_chunk_rows;  // test hook: largest rows per activation chunk (dyllm_set_option)

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--which", default="qkv,o,gu,down")
     ap.add_argument("--one-chunk", type=int, default=0, help="largest M in one activation chunk (0 auto)")
     ap.add_argument("--chunk", default="0", help="comma list of largest rows per activation chunk (0 = 256)")
+    ap.add_argument("--kb", default="0", help="comma list of skinny k-block widths (0 = 128, or 64)")
     ap.add_argument("--dbg", type=int, default=0, help="skinny measurement hook: 1 no loads, 2 no MMAs")
     ap.add_argument("--krot", default="0", help="comma list of k-block rotations per weight block (0 = none)")
     a = ap.parse_args()
@@ -49,8 +50,10 @@ def main():
         A = torch.randn(cap, K, device="cuda").bfloat16()
         D = torch.empty(cap, N, device="cuda").bfloat16()
         ref = {}
-        for M, S, CR, KR in [(int(x), int(y), int(z), int(r)) for x in a.rows.split(",") for y in a.split.split(",")
-                             for z in a.chunk.split(",") for r in a.krot.split(",")]:
+        for M, S, CR, KR, KB in [(int(x), int(y), int(z), int(r), int(b)) for x in a.rows.split(",")
+                                 for y in a.split.split(",") for z in a.chunk.split(",") for r in a.krot.split(",")
+                                 for b in a.kb.split(",")]:
+            dy.set_option(dy.OPT_SKINNY_KB, KB)
             dy.set_option(dy.OPT_SKINNY_SPLIT, S)
             dy.set_option(dy.OPT_SKINNY_CHUNK, CR)
             dy.set_option(dy.OPT_SKINNY_KROT, KR)
@@ -70,7 +73,7 @@ def main():
             if M not in ref:
                 ref[M] = out.clone()
             dev = float((out - ref[M]).abs().max() / ref[M].abs().max().clamp_min(1e-30))
-            print(f"{name:5s} N={N:6d} K={K:6d} M={M:5d} S={S:3d} C={CR:3d} R={KR:2d}: {us:8.2f} us  {tf:7.1f} TFLOP/s  "
+            print(f"{name:5s} N={N:6d} K={K:6d} M={M:5d} S={S:3d} C={CR:3d} R={KR:2d} KB={KB or 128:3d}: {us:8.2f} us  {tf:7.1f} TFLOP/s  "
                   f"weights {gbs:7.1f} GB/s  dev {dev:.1e}")
 
 

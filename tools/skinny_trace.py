@@ -20,10 +20,12 @@ ap.add_argument("--rows", type=int, default=410)
 ap.add_argument("--split", type=int, default=0, help="units per weight block (0 = auto)")
 ap.add_argument("--one-chunk", type=int, default=0, help="largest M in one activation chunk (0 = auto)")
 ap.add_argument("--dbg", type=int, default=0, help="1 no operand loads, 2 no MMAs")
+ap.add_argument("--kb", type=int, default=0, help="k-block width (0 = 128, or 64)")
 ap.add_argument("--per-cta", action="store_true", help="also print every CTA's stamps")
 a = ap.parse_args()
 dy.set_option(dy.OPT_SKINNY_SPLIT, a.split)
 dy.set_option(dy.OPT_SKINNY_DEBUG, a.dbg)
+dy.set_option(dy.OPT_SKINNY_KB, a.kb)
 if a.one_chunk:
     dy.set_option(dy.OPT_SKINNY_ONE_CHUNK, a.one_chunk)
 shapes = {"qkv": (12288, 4096), "o": (4096, 4096), "gu": (24576, 4096), "down": (4096, 12288)}
