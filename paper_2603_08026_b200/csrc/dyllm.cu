@@ -2,6 +2,7 @@
 // FullStep (Alg. 2), the per-layer SparseStep (Alg. 3 with Alg. 4 folded into the attention
 // kernel), the denoise step (Alg. 1 body) and the unmasking rule. No host synchronisation
 // inside a step: every kernel reads its row counts from device memory.
+#include <nvtx3/nvToolsExt.h>
 #include <dlfcn.h>
 #include <math.h>
 #include <nccl.h>
@@ -70,6 +71,25 @@ static cudaEvent_t prof_event(dyllm_ctx *c) {
   }
   return c->pool[c->pool_next++];
 }
+// NVTX ranges (SURVEY §5 tracing): one per denoising / full step, per layer and per kernel
+// launch, named by the kernel class; header-only NVTX v3 (no-ops unless a tool such as nsys or
+// ncu --nvtx injects itself)
+static const char *const kClassName[DYLLM_KC_COUNT] = {"qkv_gemm", "qkv_post", "attn",   "select",
+                                                        "o_gemm",   "gu_gemm",  "down_gemm", "gather",
+                                                        "scatter",  "lm_gemm",  "other"};
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+struct NvtxLayer {
+  explicit NvtxLayer(int l) {
+    char b[24];
+    snprintf(b, sizeof(b), "layer %d", l);
+    nvtxRangePushA(b);
+  }
+  ~NvtxLayer() { nvtxRangePop(); }
+};
+
 // RAII scope around one kernel launch: counts it and, when profiling, brackets it with events.
 struct KScope {
   dyllm_ctx *c;
@@ -77,6 +97,7 @@ struct KScope {
   cudaEvent_t a = nullptr;
   KScope(dyllm_ctx *ctx, int k) : c(ctx), cls(k + ctx->cls_offset) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    nvtxRangePushA(kClassName[k]);
     if (c->prof) {
       a = prof_event(c);
       cudaEventRecord(a, c->stream);
@@ -88,6 +109,7 @@ struct KScope {
       cudaEventRecord(b, c->stream);
       c->recs.push_back({cls, a, b});
     }
+    nvtxRangePop();
   }
 };
 #define KL(cls, stmt)                  \
@@ -809,6 +831,7 @@ static int full_step_impl(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c
   ctx->cls_offset = DYLLM_KC_FULL;
   KL(OTHER, launch_embed_rows(d_tokens, nullptr, nullptr, rows, w->emb, c->H0, d, st));
   for (int l = 0; l < m.n_layers; ++l) {
+    const NvtxLayer layer_range(l);
     const LayerW &L = w->L[l];
     LayerC &C = c->L[l];
     const bf16 *Hprev = l == 0 ? c->H0 : c->L[l - 1].H;
@@ -1059,6 +1082,8 @@ int dyllm_denoise_step(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, i
   if (t >= T_total) return DYLLM_DONE;
   RET(sticky(ctx));
   cudaStream_t st = ctx->stream;
+  const NvtxRange step_range(t < r.T_full ? "dyllm full step" : (t % r.full_period == 0 ? "dyllm full-input step"
+                                                                                         : "dyllm response-only step"));
   if (t < r.T_full) {
     RET(full_step_impl(ctx, w, c, d_tokens));
   } else {
@@ -1071,6 +1096,7 @@ int dyllm_denoise_step(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, i
     RET(layer1_prepare(ctx, w, c, row_lo));
     int cur = 0;
     for (int l = 0; l < c->m.n_layers; ++l) {
+      const NvtxLayer layer_range(l);
       float *sim_tr = c->tr_sims ? c->tr_sims + static_cast<int64_t>(l) * c->rows : nullptr;
       RET(layer_step_impl(ctx, w, c, l, row_lo, c->lst[cur], c->lst_off[cur], h_tau[l], c->lst[cur ^ 1],
                           c->lst_off[cur ^ 1], sim_tr, d_sal_counts ? d_sal_counts + l * r.batch : nullptr));
@@ -1093,6 +1119,7 @@ int dyllm_full_step(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, int3
                     int32_t *d_dec_tok) {
   CHECK_ARG(ctx && w && c && d_tokens && d_dec_tok, "null argument");
   RET(sticky(ctx));
+  const NvtxRange step_range("dyllm full step");
   RET(full_step_impl(ctx, w, c, d_tokens));
   return unmask_impl(ctx, w, c, d_tokens, d_dec_pos, d_dec_tok);
 }
