@@ -28,6 +28,10 @@
 // epilogue warps: four per TMEM lane quadrant, one row per thread, 32 of the 128 key columns of
 // each score tile each; P is stored bf16x2-packed into TMEM with tcgen05.st.
 #include "common.cuh"
+
+#ifndef DYLLM_FA_X_FIRST
+#define DYLLM_FA_X_FIRST 1  // exact-row items claimed first (fa_decode)
+#endif
 #include "internal.h"
 
 namespace dy {
@@ -122,11 +126,30 @@ struct FaItem {
 
 // Item decode from its index and the exact-row range (off, e) of its sequence (the producer reads
 // those once and passes them through the work queue, so no role stalls on global loads).
+// item index -> ((sequence, kv head, group member) index sh, slot t: row tiles 0..MT-1, exact-row
+// tiles MT..MT+XT-1). DYLLM_FA_X_FIRST: every exact-row (type 2, the longest) item is claimed
+// before any row-tile item, in (sequence, head) order, so the launch ends on short items; the two
+// kinds read different key data (full K / V vs the compact changed keys), so nothing shared in L2
+// is split. Otherwise the items of one (sequence, head) are adjacent, exact rows last.
+__device__ __forceinline__ void fa_decode(const FaParams &p, int w, int &sh, int &t) {
+  if (DYLLM_FA_X_FIRST) {
+    const int n2 = p.items / (p.MT + p.XT) * p.XT;
+    if (w < n2) {
+      sh = w / p.XT;
+      t = p.MT + w % p.XT;
+    } else {
+      sh = (w - n2) / p.MT;
+      t = (w - n2) % p.MT;
+    }
+  } else {
+    sh = w / (p.MT + p.XT);
+    t = w % (p.MT + p.XT);
+  }
+}
 __device__ __forceinline__ FaItem fa_item(const FaParams &p, int w, int off, int e, int nU) {
   FaItem it;
-  const int per = p.MT + p.XT;
-  const int t = w % per;
-  int sh = w / per;
+  int sh, t;
+  fa_decode(p, w, sh, t);
   const int g = sh % p.grp;
   sh /= p.grp;
   it.kvh = sh % p.KVH;
@@ -174,7 +197,11 @@ __device__ __forceinline__ FaItem fa_item(const FaParams &p, int w, int off, int
   }
   return it;
 }
-__device__ __forceinline__ int fa_seq(const FaParams &p, int w) { return w / (p.MT + p.XT) / p.grp / p.KVH; }
+__device__ __forceinline__ int fa_seq(const FaParams &p, int w) {
+  int sh, t;
+  fa_decode(p, w, sh, t);
+  return sh / p.grp / p.KVH;
+}
 
 // UMMA descriptor of an MN-major operand tile written by TMA with 128B swizzle: 64-element
 // (128 B) rows along MN, 8-row (K) core groups 1024 B apart (SBO), consecutive 64-element MN
