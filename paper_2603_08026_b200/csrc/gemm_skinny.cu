@@ -271,7 +271,13 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   const int nwb = p.N / 256;
   const bool one = p.one_chunk_max >= 0 ? M <= p.one_chunk_max
                                         : (M <= 256 || (M <= 512 && 2 * nwb >= p.P_max && nwb < p.P_max));
-  const int crow = p.chunk_rows > 0 ? min(p.chunk_rows, 256) : 256;
+  // M > 512 with few weight blocks (O-proj / FFN-down: 16): floor(P / blocks) chunks of up to 512
+  // rows, so every tile runs in ONE round over the pairs (256-row chunks would need two rounds:
+  // 96 tiles for 74 pairs at M = 1530); else chunks of <= 256 rows (tools/gemm_bench.py --chunk,
+  // profiles/r2/skinny/chunk512.txt)
+  const int n1 = p.P_max / nwb;
+  const bool oneround = p.chunk_rows == 0 && !one && n1 >= 2 && M <= 512 * n1 && M > 512;
+  const int crow = oneround ? (M + n1 - 1) / n1 : p.chunk_rows > 0 ? min(p.chunk_rows, 512) : 256;
   const int nchunk = one ? 1 : (M + crow - 1) / crow;
   const int R = nchunk == 1 ? M : (((M + nchunk - 1) / nchunk + 31) & ~31);
   const int items = p.N / 256 * nchunk;
@@ -285,8 +291,9 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   const int64_t Wt = static_cast<int64_t>(items) * upi;      // units of the stream-K partition
   const int P = static_cast<int>(min(static_cast<int64_t>(p.P_max), Wt));
   // activation rows per MMA, rounded to 32 so that each CTA's half is a multiple of 16 rows
-  const int NA0 = nchunk == 1 ? ((min(M, 256) + 31) & ~31) : R;
-  const int NA1 = (nchunk == 1 && M > 256) ? ((M - 256 + 31) & ~31) : 0;
+  // (a chunk of more than 256 rows runs as two MMAs per k-step: rows [0, 256) and [256, R))
+  const int NA0 = (min(R, 256) + 31) & ~31;
+  const int NA1 = R > 256 ? ((R - 256 + 31) & ~31) : 0;
   // M <= 256: two 256-column TMEM accumulators (epilogue of segment i overlaps the MMAs of i+1)
   const int nbuf = NA1 ? 1 : 2;
   const uint32_t stage_tx = 2u * (kWBytes + (NA0 / 2 + NA1 / 2) * kRowBytes);
@@ -364,7 +371,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
                              arow + static_cast<int>(rank) * (NA0 / 2), kb * CH);
             if (NA1)
               tma_load_3d_pair(sb + kWBytes + (NA0 / 2) * kRowBytes, &maps.a[NA1 / 32 - 1], &full[st], 0,
-                               256 + static_cast<int>(rank) * (NA1 / 2), kb * CH);
+                               arow + NA0 + static_cast<int>(rank) * (NA1 / 2), kb * CH);
           }
           if (++st == nstages) {
             st = 0;
