@@ -299,7 +299,8 @@ __device__ __forceinline__ void fa_named_sync(int id, int n) {
 }
 
 // debug event log (compiled in with -DDYLLM_ATTN_EVENTS=1, tools/attn_events.py): one 8192-entry
-// region per (CTA < 2, role); entry = code << 56 | clock64
+// region per (CTA < 2, role); entry = code << 56 | clock64. With -DDYLLM_ATTN_EVENTS=2 the fourth
+// role logs softmax warp 6 (quad 2, column group 1) instead of the V producer
 #ifndef DYLLM_ATTN_EVENTS
 #define DYLLM_ATTN_EVENTS 0
 #endif
@@ -368,7 +369,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   // event roles: 0 MMA, 1 softmax warp 2, 2 producer warp 0, 3 V producer
   FaEv ev;
   {
-    const int role = warp == 1 ? 0 : warp == 2 ? 1 : warp == 0 ? 2 : warp == FA_WV ? 3 : -1;
+    const int role = warp == 1 ? 0 : warp == 2 ? 1 : warp == 0 ? 2 : warp == (DYLLM_ATTN_EVENTS == 2 ? 6 : FA_WV) ? 3 : -1;
     if (p.events && p.mode == 0 && blockIdx.x < 2 && lane == 0 && role >= 0) ev.attach(p.events + (blockIdx.x * 4 + role) * FA_EV_N);
   }
 
@@ -920,6 +921,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_empty[sb]);
+            ev(47);
             float sub = 0.f;
 #pragma unroll
             for (int t = 0; t < FA_CW; ++t) sub += ex2f(t < nvalid ? fmaf(v[t], c, -mref) : -INFINITY);
@@ -984,6 +986,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_empty[sb]);
+            ev(44);
             float tmax = -INFINITY;
 #pragma unroll
             for (int t = 0; t < FA_CW; ++t) {
@@ -998,11 +1001,13 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             fa_named_sync(1 + quad, 32 * FA_NG);
             if (rvalid) so = rp->so;
             mref = fmaxf(so.x, mn * c);
+            ev(45);
             if (it.passP) {
               // P over the salient keys (columns < nkP), bf16x2-packed into the P buffer; every
               // valid column's term (masked keys: 2^-inf = 0) enters the normaliser
               const int npv = it.nkP - hh * FA_CW;
               fa_wait(&p_empty[pb], (((pc - 1) >> 1) & 1) ^ 1);
+              ev(46);
               tc_fence_after();
 #pragma unroll
               for (int ch = 0; ch < NCH; ++ch) {
@@ -1059,12 +1064,15 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         float Lnew = 1.f;
         bool bad = false;
         if (wact) {
+          ev(48);
           xch[hh * 128 + r].y = over ? NAN : part;  // every column group of the row sees the verdict
           fa_named_sync(1 + quad, 32 * FA_NG);
+          ev(49);
           float tot = 0.f;
 #pragma unroll
           for (int g2 = 0; g2 < FA_NG; ++g2) tot += xch[g2 * 128 + r].y;
           fa_named_sync(1 + quad, 32 * FA_NG);
+          ev(53);
           const float base = so.y * ex2f(so.x - mref);
           Lnew = base + tot;
           bad = !(so.y > 0.f) || !(Lnew > base * 0x1p-14f) || !(Lnew < INFINITY);
@@ -1091,6 +1099,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(acc_empty);
+          ev(54);
         }
         oscale = 1.f / Lnew;
       } else if (it.single) {
@@ -1458,6 +1467,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             for (int t = 0; t < 8; ++t) o[t] = acc[u * 8 + t] * oscale;
             ch[u] = pack8(o);
           }
+          ev(55);
           store_rows(ch);
         }
       }

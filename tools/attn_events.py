@@ -2,12 +2,14 @@
 per-role event logs of CTAs 0-1 for the last layer of one denoising step of the bench workload.
 
     DYLLM_NVCC_FLAGS=-DDYLLM_ATTN_EVENTS=1 python -m paper_2603_08026_b200.build --force
+    (=2: the fourth role logs softmax warp 6, a second column group of quad 2, instead of the V producer)
     python tools/attn_events.py --mode ro|fi|full [--items 3]
 
 Codes: MMA 1/2/3/4 item (type 1/2/3, 4 = type 3 over the prompt U lists), 9 Q ready, 10 QK begin, 11 S buffer free, 12 K tile ready, 13 QK issued,
 20 PV begin, 21 P ready, 22 V/acc ready, 23 PV issued. Softmax (warp 2) 1/2 item, 30 S wait,
 31 S ready, 32 S read (buffer released), 33 S tile done, 40 P-pass S wait, 41 ready, 42 P stored,
-50 acc wait, 51 acc ready, 52 epilogue done. Producer 60 K slot wait, 61 K issued, 62/63 claim begin/end, 64/65 Q slot wait begin/end. V 70, 71.
+50 acc wait, 51 acc ready, 52 epilogue done; type 3 phases 44 S_new read, 45 row max exchanged, 46 P buffer free,
+47 S_old read, 48 statistics exchange, 49 after its first barrier, 53 after the second, 54 accumulator read, 55 scaled. Producer 60 K slot wait, 61 K issued, 62/63 claim begin/end, 64/65 Q slot wait begin/end. V 70, 71.
 """
 import argparse
 import collections
@@ -61,7 +63,7 @@ def decode(arr):
     return [(int(x >> np.uint64(56)), int(x & np.uint64((1 << 56) - 1))) for x in arr]
 
 
-roles = ["MMA", "softmax(w2)", "producer(w0)", "V producer"]
+roles = ["MMA", "softmax(w2)", "producer(w0)", "V producer / softmax(w6)"]
 pairs = {0: [(10, 11, "S buf free wait"), (11, 12, "K tile wait"), (12, 13, "QK issue"), (20, 21, "P wait"),
              (21, 22, "V/acc wait"), (22, 23, "PV issue")],
          1: [(30, 31, "S wait (pass S)"), (31, 32, "S read"), (32, 33, "S math"), (40, 41, "S wait (pass P)"),
@@ -95,6 +97,31 @@ for role in range(4):
             d = [x for x, k in durs if k == kind]
             if d:
                 print(f"   items type {kind}: n={len(d)} mean {np.mean(d):.2f} us  min {np.min(d):.2f}  max {np.max(d):.2f}")
+# per-item phase breakdown of the softmax roles: mean time between consecutive event codes inside
+# the items of each type (role 3 is softmax warp 6, a no-key column group, in DYLLM_ATTN_EVENTS=2 builds)
+for role in (0, 1, 3):
+    ev = decode(raw[0, role])
+    if not ev or not any(c in (1, 2, 3, 4) for c, _ in ev):
+        continue
+    items = []
+    for code, t in ev:
+        if code in (1, 2, 3, 4):
+            items.append([code, [(code, t)]])
+        elif items:
+            items[-1][1].append((code, t))
+    for kind in (2, 3, 4):
+        its = [x for k, x in items[:-1] if k == kind]
+        if not its:
+            continue
+        tr = collections.defaultdict(list)
+        for x in its:
+            for (c0, t0_), (c1, t1_) in zip(x, x[1:]):
+                tr[(c0, c1)].append((t1_ - t0_) * cyc)
+        tot = np.mean([(x[-1][1] - x[0][1]) * cyc for x in its])
+        print(f"== role {roles[role] if role < 2 else 'softmax(w6)'} type {kind}: {len(its)} items, mean {tot:.2f} us to last event")
+        for (c0, c1), d in sorted(tr.items(), key=lambda kv: -np.sum(kv[1])):
+            if np.sum(d) / len(its) > 0.02:
+                print(f"   {c0:3d} -> {c1:3d}  n={len(d):4d}  mean {np.mean(d) * 1e3:7.0f} ns  per item {np.sum(d) / len(its) * 1e3:7.0f} ns")
 # detailed timeline of the first items (MMA and softmax interleaved)
 mm = decode(raw[0, 0])
 sm = decode(raw[0, 1])
