@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--config", default="llada8b")
     ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (0 = config)")
     ap.add_argument("--n-u", type=int, default=0, help="tokens unmasked per step (0 = config; f2: 2, 4)")
+    ap.add_argument("--lp", type=int, default=0, help="prompt length L_P (0 = config; the paper's representative case: 1024, P:610)")
     ap.add_argument("--frac", type=float, default=0.10, help="target salient fraction for tau calibration")
     ap.add_argument("--tau", type=float, default=None, help="fixed tau for all layers (skips calibration)")
     ap.add_argument("--select-mode", default="fraction", choices=["fraction", "tau"],
@@ -253,6 +254,8 @@ def run_reference(args):
         run = _replace(run, batch=args.batch)
     if args.n_u:
         run = _replace(run, n_u=args.n_u)
+    if args.lp:
+        run = _replace(run, L_P=args.lp)
     vals = []
     for _ in range(args.warmup + args.steps):
         vals.append(cpu_oracle_sample(cfg, run, args.cpu_seconds / 4, args.frac))
@@ -384,6 +387,8 @@ def main():
         run = replace(run, batch=args.batch)
     if args.n_u:
         run = replace(run, n_u=args.n_u)
+    if args.lp:
+        run = replace(run, L_P=args.lp)
     fmode = args.select_mode == "fraction"
     run = replace(run, select_mode=1 if fmode else 0)
     b, N = run.batch, run.N

@@ -84,6 +84,13 @@ def test_layer_step_full_size_sampled(big, mode, frac_in):
     _check_full_size(big, mode, frac_in)
 
 
+@pytest.mark.parametrize("mode,frac_in", [("ro", 0.10), ("fi", 0.10)])
+def test_layer_step_full_size_every_sequence(big, mode, frac_in):
+    """Every one of the 16 sequences of the bench batch recomputed by the oracle and compared row
+    by row (the other full-size cases sample five)."""
+    _check_full_size(big, mode, frac_in, seqs=range(big[3].batch))
+
+
 def test_layer_step_full_size_sampled_untransposed(big):
     """Response-only step (26 exact rows per sequence) with the transposed exact-row tiles off
     (only differs from the default in -DDYLLM_FA_T4=1 builds)."""
@@ -113,7 +120,7 @@ def test_layer_step_full_size_sampled_dream(big_dream, mode, frac_in):
     _check_full_size(big_dream, mode, frac_in)
 
 
-def _check_full_size(big, mode, frac_in, frac=0.10):
+def _check_full_size(big, mode, frac_in, frac=0.10, seqs=CHECK_SEQS):
     dy, ctx, cfg, run, w, W, host = big
     b, N = run.batch, run.N
     row_lo = 0 if mode == "fi" else run.L_P
@@ -138,7 +145,7 @@ def _check_full_size(big, mode, frac_in, frac=0.10):
     got_lists = unpack_lists(out_d, oof_d, N)
     sim = sim_d.view(b, N).cpu().numpy()
     n_band, checked = 0, 0
-    for s in CHECK_SEQS:
+    for s in seqs:
         # oracle on this sequence only, from the same synthetic inputs (fp64)
         x_all = host["cX"][s].astype(np.float64)
         lc = O.LayerCache(K=host["cK"][s].astype(np.float64), V=host["cV"][s].astype(np.float64),
@@ -180,7 +187,7 @@ def _check_full_size(big, mode, frac_in, frac=0.10):
         untouched = sorted(set(range(N)) - got)
         assert torch.equal(cache.tensor(1, dy.H)[s, untouched], h_before[s, untouched])
         checked += len(input_rows)
-    assert n_band <= 0.05 * checked + 2 * len(CHECK_SEQS)
+    assert n_band <= 0.05 * checked + 2 * len(seqs)
     # every sequence of the batch (checked or not) selected round(f * rows) rows (D19)
     k = int(np.floor(frac * len(input_rows) + 0.5))
     assert all(abs(len(g) - k) <= 1 for g in got_lists)
