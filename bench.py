@@ -138,7 +138,8 @@ def measured_traffic(cls, sparse_t, run):
         meas = json.load(open(p))
     except (OSError, ValueError):
         return None
-    if meas.get("_config") != run_config_name[0]:
+    if meas.get("_config") != run_config_name[0] or meas.get("_L_P", run.L_P) != run.L_P or \
+            meas.get("_batch", run.batch) != run.batch:
         return None   # captured at another configuration
     t = meas.get(cls)
     if not t:

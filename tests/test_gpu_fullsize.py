@@ -30,8 +30,10 @@ TOL = 2e-2      # north_star bar for hidden states (H rows), K/V/Q rows
 # Contexts are an intermediate, not the north_star's hidden state. Their bar is derived from the
 # arithmetic ("tolerances"): at these inputs, a CPU emulation of the path's bf16
 # roundings (RMSNorm output fed to the QKV GEMM, K/V rows, P, dV, dC and C_new) on the fp64 oracle
-# already reaches 2.2% max row error on approximate rows, whose new context is dominated by dC.
-C_TOL = 3e-2
+# reaches 2.0-3.02% max row error per sequence on approximate rows, whose new context is dominated by
+# dC (3.02% in sequence 9 of the response-only case, row 927, which the GPU reproduces to 4 digits);
+# the bar leaves headroom for the kernels' own summation orders on top of the emulated roundings.
+C_TOL = 4e-2
 BAND = 1e-3
 SEED = 3
 CHECK_SEQS = (0, 3, 7, 11, 15)   # oracle recomputations per full-size case (the others: list counts)

@@ -21,7 +21,7 @@ from synth import configs, gen
 
 SEED = 3
 STD = {"cK": 1.25, "cQ": 1.5, "cV": 1.25, "cC": 0.1, "cX": 1.0}
-C_TOL = 3e-2     # tests/test_gpu_fullsize.py
+C_TOL = 4e-2     # tests/test_gpu_fullsize.py
 TOL = 2e-2       # the north_star's hidden-state bar
 
 
@@ -97,15 +97,18 @@ def test_oracle_steps_reproduce_sparse_layer_contexts():
     assert np.abs(C - ref.C).max() < 1e-12
 
 
-@pytest.mark.parametrize("mode,frac_in", [("fi", 0.06), ("ro", 0.10)])
-def test_bf16_roundings_alone_reach_the_context_tolerance(mode, frac_in):
-    cfg, run, host, W, rows, idx = _inputs(mode, frac_in)
+# (sequence 9 of the response-only case is the maximum over the 16 sequences of the bench batch:
+# 3.02%, row 927; full-input sequences reach 2.2-2.8%)
+@pytest.mark.parametrize("mode,frac_in,seq", [("fi", 0.06, 0), ("ro", 0.10, 0), ("ro", 0.10, 9)])
+def test_bf16_roundings_alone_reach_the_context_tolerance(mode, frac_in, seq):
+    cfg, run, host, W, rows, idx = _inputs(mode, frac_in, seq)
     ref = _contexts(cfg, host, W, rows, idx, emulate=False)
     emu = _contexts(cfg, host, W, rows, idx, emulate=True)
     num = np.abs(emu - ref).max(axis=1)
     err = num / np.maximum(np.abs(ref).max(axis=1), 1e-30)
     print(f"{mode} frac_in {frac_in}: max row error {err.max():.4f}, rows over 1e-2: {(err > 1e-2).sum()}/{len(err)}")
     # the roundings alone use most of the 2e-2 hidden-state bar on these contexts (approximate rows
-    # whose new context is dominated by dC), so the kernel's own reordering needs the 3e-2 bar
+    # whose new context is dominated by dC) and exceed it in some sequences, so the contexts get
+    # their own bar with headroom for the kernels' summation orders
     assert err.max() < C_TOL
     assert err.max() > 0.5 * TOL
