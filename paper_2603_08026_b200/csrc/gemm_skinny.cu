@@ -454,7 +454,20 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
     const int msub = t >> 4;
     auto sl_m = [&](int i) { return kSw ? msub + 8 * (i & 3) : msub + 8 * (i >> 1); };
     auto sl_n = [&](int i) { return kSw ? (i < 4 ? 4 * n4 : 64 + 4 * n4) : 8 * n4 + 4 * (i & 1); };
-    auto store = [&](const float4 r[8], int m0, int tile) {
+    // the output / residual row ids of the four rows a thread stores of a chunk, loaded before the
+    // chunk's transpose so that their latency overlaps it (and before any store: D may alias nothing
+    // they read, but the compiler cannot know that, and a load written after a store waits for it)
+    auto row_ids = [&](int m0, int tile, int orow[4], int rrow[4]) {
+      m0 += tile % nchunk * R;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int m = m0 + sl_m(kSw ? i : 2 * i);
+        const bool ok = m < M;
+        orow[i] = ok && p.out_rows ? __ldg(p.out_rows + m) : m;
+        rrow[i] = ok && p.resid_rows ? __ldg(p.resid_rows + m) : m;
+      }
+    };
+    auto store = [&](const float4 r[8], int m0, int tile, const int orow[4], const int rrow[4]) {
       const int item = tile / nchunk;  // weight block (output columns)
       m0 += tile % nchunk * R;         // output rows of the tile's activation chunk
       if constexpr (kSw) {
@@ -466,7 +479,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             const float4 g = r[i], u = r[4 + i];
             const float o0 = g.x / (1.f + __expf(-g.x)) * u.x, o1 = g.y / (1.f + __expf(-g.y)) * u.y;
             const float o2 = g.z / (1.f + __expf(-g.z)) * u.z, o3 = g.w / (1.f + __expf(-g.w)) * u.w;
-            *reinterpret_cast<uint2 *>(p.D + static_cast<int64_t>(p.out_rows ? p.out_rows[m] : m) * p.ldd + ch) =
+            *reinterpret_cast<uint2 *>(p.D + static_cast<int64_t>(orow[i]) * p.ldd + ch) =
                 make_uint2(pack2(o0, o1), pack2(o2, o3));
           }
         }
@@ -483,6 +496,15 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             bb[2 * q + 1] = f.y;
           }
         }
+        // the four residual rows are loaded before the first store (one round trip per chunk)
+        uint4 rv[4];
+        if constexpr (EPI == EPI_RESID) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            rv[i] = m0 + sl_m(2 * i) < M
+                        ? *reinterpret_cast<const uint4 *>(p.resid + static_cast<int64_t>(rrow[i]) * p.ldr + n)
+                        : make_uint4(0u, 0u, 0u, 0u);
+        }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int m = m0 + sl_m(2 * i);
@@ -491,9 +513,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             float o[8] = {a.x + bb[0], a.y + bb[1], a.z + bb[2], a.w + bb[3],
                           b.x + bb[4], b.y + bb[5], b.z + bb[6], b.w + bb[7]};
             if constexpr (EPI == EPI_RESID) {
-              const int rr = p.resid_rows ? p.resid_rows[m] : m;
-              const uint4 rv = *reinterpret_cast<const uint4 *>(p.resid + static_cast<int64_t>(rr) * p.ldr + n);
-              const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
+              const uint32_t rw[4] = {rv[i].x, rv[i].y, rv[i].z, rv[i].w};
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&rw[q]));
@@ -501,7 +521,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
                 o[2 * q + 1] += f.y;
               }
             }
-            *reinterpret_cast<uint4 *>(p.D + static_cast<int64_t>(p.out_rows ? p.out_rows[m] : m) * p.ldd + n) =
+            *reinterpret_cast<uint4 *>(p.D + static_cast<int64_t>(orow[i]) * p.ldd + n) =
                 make_uint4(pack2(o[0], o[1]), pack2(o[2], o[3]), pack2(o[4], o[5]), pack2(o[6], o[7]));
           }
         }
@@ -511,11 +531,13 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
     // this half's tile and store it. The leading barrier also orders the previous chunk's tile
     // reads before this chunk's writes.
     auto transpose_store = [&](const float v[32], int m0, int item) {
+      int orow[4], rrow[4];
+      row_ids(m0, item, orow, rrow);
       if (p.dbg & 8) {
         float4 r[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) r[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        if (!(p.dbg & 4)) store(r, m0, item);
+        if (!(p.dbg & 4)) store(r, m0, item, orow, rrow);
         return;
       }
       named_bar_sync(1 + half, 128);
@@ -526,7 +548,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       float4 r[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) r[i] = x4[sl_m(i) * 32 + sl_n(i) / 4];
-      if (!(p.dbg & 4)) store(r, m0, item);
+      if (!(p.dbg & 4)) store(r, m0, item, orow, rrow);
     };
     // split-K partials, TMEM-native layout: slot-major, then rank, then [16 chunks][8][128 n]
     // float4 (element j of a thread's 32 values at [j / 4][n]), so every warp store / load of one
