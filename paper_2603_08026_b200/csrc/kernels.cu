@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(512, DYLLM_QKVPOST_LB) qkv_post_kernel(const b
   const int half = hd / 2, hv = half / 8;  // 8 rotation pairs per thread (16-byte vectors)
   // q_only: refresh the Q cache rows alone (K / V / dV / row flag untouched)
   const int nqk = (q_only ? H : H + KVH) * hv, nvv = q_only ? 0 : kw / 8;
-  const int rounds = (max(nqk, nvv) + blockDim.x - 1) / blockDim.x;  // 1 with the host's block size
+  const int rounds = (max(nqk, nvv) + blockDim.x - 1) / blockDim.x;  // work items per thread (2 at 256 threads, LLaDA)
   for (int i = blockIdx.x; i < M; i += gridDim.x) {
     const int r = idx ? idx[i] : i;
     const int pos = r % N;
@@ -167,13 +167,10 @@ __global__ void __launch_bounds__(512, DYLLM_QKVPOST_LB) qkv_post_kernel(const b
     const float2 *cs = rope_cs + static_cast<int64_t>(pos) * half;
     // statistics epochs (incremental prompt statistics): the first write of a key row
     // since its layer's epoch began keeps the overwritten key in Kfi (the key the prompt rows'
-    // statistics were computed with) and marks the row changed
-    bool snap = false;
-    if (Kfi && !q_only) {
-      snap = dtag[r] != epoch;
-      __syncthreads();  // every thread has read the tag before it changes
-      if (snap && threadIdx.x == 0) dtag[r] = epoch;
-    }
+    // statistics were computed with) and marks the row changed. The tag is read here and rewritten
+    // after the row's barrier below, so no load of the row waits on a barrier: one round trip for
+    // the row id, one for everything else (the overwritten key is read whenever Kxo or Kfi is set)
+    const bool snap = Kfi && !q_only && dtag[r] != epoch;
     for (int rd = 0; rd < rounds; ++rd) {
       const int v = rd * blockDim.x + threadIdx.x;
       const bool has_qk = v < nqk, has_v = v < nvv;
@@ -194,7 +191,7 @@ __global__ void __launch_bounds__(512, DYLLM_QKVPOST_LB) qkv_post_kernel(const b
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) c4[j] = reinterpret_cast<const float4 *>(cs + k0)[j];
-        if ((Kxo || snap) && col >= qw) {  // the key row this step overwrites (incremental statistics)
+        if ((Kxo || (Kfi && !q_only)) && col >= qw) {  // the key row this step overwrites (incremental statistics)
           const bf16 *ko = Kc + static_cast<int64_t>(r) * kw + (col - qw);
           uk1 = *reinterpret_cast<const uint4 *>(ko);
           uk2 = *reinterpret_cast<const uint4 *>(ko + half);
@@ -274,6 +271,10 @@ __global__ void __launch_bounds__(512, DYLLM_QKVPOST_LB) qkv_post_kernel(const b
         }
         *vc = vb;
       }
+    }
+    if (Kfi && !q_only) {
+      __syncthreads();  // every thread has read the row's tag before it changes
+      if (snap && threadIdx.x == 0) dtag[r] = epoch;
     }
   }
 }
