@@ -40,11 +40,13 @@ CHECK_SEQS = (0, 3, 7, 11, 15)   # oracle recomputations per full-size case (the
 STD = {"cK": 1.25, "cQ": 1.5, "cV": 1.25, "cC": 0.1, "cH": 1.0, "cX": 1.0}
 
 
-def _make(name):
+def _make(name, L_P=None):
     from paper_2603_08026_b200 import dyllm as dy
     cfg, run = configs.preset(name)
     cfg = replace(cfg, n_layers=1, vocab=1024, mask_id=1023)    # layer_step never reads the vocab
     run = replace(run, select_mode=1)
+    if L_P is not None:
+        run = replace(run, L_P=L_P)
     b, N, d = run.batch, run.N, cfg.d_model
     ctx = dy.Context(0)
     w = dy.Weights.random(ctx, cfg, seed=SEED)                  # on-device IH4 (same streams)
@@ -70,6 +72,13 @@ def big_dream():
     return _make("dream7b")
 
 
+@pytest.fixture(scope="module")
+def big_long():
+    """The paper's representative prompt length L_P = 1024 (bench.py --lp 1024): N = 1280, so
+    full-input selection runs the kernel's L > 1024 shape."""
+    return _make("llada8b", L_P=1024)
+
+
 def _upload(dy, ctx, cache, host):
     for which, k, layer in [(dy.K, "cK", 0), (dy.V, "cV", 0), (dy.Q, "cQ", 0), (dy.CTX, "cC", 0),
                             (dy.H, "cH", 1), (dy.H, "cX", 0)]:
@@ -91,6 +100,11 @@ def test_layer_step_full_size_every_sequence(big, mode, frac_in):
     """Every one of the 16 sequences of the bench batch recomputed by the oracle and compared row
     by row (the other full-size cases sample five)."""
     _check_full_size(big, mode, frac_in, seqs=range(big[3].batch))
+
+
+@pytest.mark.parametrize("mode", ["ro", "fi"])
+def test_layer_step_full_size_long_prompt(big_long, mode):
+    _check_full_size(big_long, mode, 0.10, seqs=(0, 9, 15))
 
 
 def test_layer_step_full_size_sampled_untransposed(big):
