@@ -125,6 +125,7 @@ static bool g_attn_pinc_enabled = true;  // test hook: incremental prompt statis
 // default — same-box A/B (tools/gpu_r2_cos.sh): attention 141 -> 178 us per launch (the C_old read
 // lands on each item's serial chain), selection 48 -> 26 us: 716 vs 724 tok/s
 static bool g_attn_fuse_cos = false;
+static bool g_qkv_fused = false;  // EPI_QKV: a3 in the QKV projection's epilogue (DYLLM_OPT_QKV_FUSED)
 
 struct LayerW {
   bf16 *g_attn, *wqkv, *bqkv, *wo, *g_ffn, *wgu, *wd;
@@ -157,6 +158,7 @@ struct dyllm_cache {
   bf16 *H0;
   bf16 *Xn, *qkv, *dV, *Qx, *Kx, *Kxo, *Cn, *Cg, *h, *hn, *act, *ffo, *Xf;
   uint32_t *rowflag;     // [rows] == row_tag: exact row (idx_in) of the current layer step
+  uint8_t *snapm;        // [rows] packed rows written for the first time in their statistics epoch (EPI_QKV)
   uint32_t row_tag = 0;  // advanced by every layer step (no clearing pass over rowflag)
   float4 *partials;
   int *lst[2], *lst_off[2];
@@ -512,6 +514,7 @@ int dyllm_cache_create(dyllm_ctx *ctx, const dyllm_weights *w, const dyllm_run_c
   ALE(c->Kx, rows * kw);
   ALE(c->Kxo, rows * kw);
   AL(c->rowflag, rows);
+  AL(c->snapm, rows);
   ALE(c->Cn, rows * qw);
   ALE(c->Cg, rows * qw);
   ALE(c->h, rows * d);
@@ -614,6 +617,32 @@ static int gemm(dyllm_ctx *ctx, const int *M_ptr, int M_cap, int N, int K, const
   g.epi = epi;
   g.ws = ctx->sk_ws;
   g.ctr = ctx->sk_ctr;
+  return gemm_launch(g, ctx->num_sms, ctx->stream);
+}
+
+// a2 + a3 in one launch (EPI_QKV): the QKV projection of the rows of A whose epilogue applies the bias
+// and RoPE and writes the cache rows, dV and the compact copies (q: everything but A / W / bias)
+static bool qkv_fusable(const dyllm_cache *c) {
+  const dyllm_model_cfg &m = c->m;
+  const int qw = m.n_heads * m.head_dim, kw = m.n_kv_heads * m.head_dim;
+  return g_qkv_fused && g_skinny_enabled && m.head_dim == 128 && c->rows <= kSkinnyMaxM &&
+         (qw + 2 * kw) % 256 == 0 && m.d_model % 128 == 0;
+}
+static int gemm_qkv(dyllm_ctx *ctx, const dyllm_cache *c, const int *M_ptr, const bf16 *A, const bf16 *W,
+                    const bf16 *bias, const QkvEpi &q) {
+  const dyllm_model_cfg &m = c->m;
+  GemmCall g;
+  g.M_ptr = M_ptr;
+  g.M_cap = c->rows;
+  g.N = (m.n_heads + 2 * m.n_kv_heads) * m.head_dim;
+  g.K = m.d_model;
+  g.A = A;
+  g.W = W;
+  g.bias = bias;
+  g.epi = EPI_QKV;
+  g.ws = ctx->sk_ws;
+  g.ctr = ctx->sk_ctr;
+  g.qkv = q;
   return gemm_launch(g, ctx->num_sms, ctx->stream);
 }
 
@@ -779,9 +808,21 @@ static int full_attn_phase(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *
   LayerC &C = c->L[l];
   const bf16 *Hprev = l == 0 ? c->H0 : c->L[l - 1].H;
     KL(GATHER, launch_gather_rmsnorm(Hprev, nullptr, nullptr, rows, L.g_attn, m.rms_eps, c->Xn, d, st));
-    KL(QKV_GEMM, RET(gemm(ctx, nullptr, rows, qw + 2 * kw, d, c->Xn, L.wqkv, c->qkv, qw + 2 * kw, EPI_BF16)));
-    KL(QKV_POST, launch_qkv_post(c->qkv, nullptr, nullptr, rows, L.bqkv, c->N, m.n_heads, m.n_kv_heads, m.head_dim,
-                                 c->rope_cs, C.Q, C.K, C.V, nullptr, nullptr, nullptr, nullptr, nullptr, 0u, st));
+    if (qkv_fusable(c)) {
+      QkvEpi q;
+      q.N = c->N;
+      q.H = m.n_heads;
+      q.KVH = m.n_kv_heads;
+      q.rope_cs = c->rope_cs;
+      q.Qc = C.Q;
+      q.Kc = C.K;
+      q.Vc = C.V;
+      KL(QKV_GEMM, RET(gemm_qkv(ctx, c, nullptr, c->Xn, L.wqkv, L.bqkv, q)));
+    } else {
+      KL(QKV_GEMM, RET(gemm(ctx, nullptr, rows, qw + 2 * kw, d, c->Xn, L.wqkv, c->qkv, qw + 2 * kw, EPI_BF16)));
+      KL(QKV_POST, launch_qkv_post(c->qkv, nullptr, nullptr, rows, L.bqkv, c->N, m.n_heads, m.n_kv_heads, m.head_dim,
+                                   c->rope_cs, C.Q, C.K, C.V, nullptr, nullptr, nullptr, nullptr, nullptr, 0u, st));
+    }
     AttnArgs a{};
     a.batch = c->r.batch;
     a.N = c->N;
@@ -867,17 +908,53 @@ static int attn_phase(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, in
   // exact rows = idx_in; approximate rows = input rows \ idx_in: the fused path marks the exact
   // rows in qkv_post (row tag), the other attention kernels take an explicit approximate list
   if (!fused) KL(OTHER, launch_approx_rows(idx_in, off_in, b, N, row_lo, c->ap_rows, c->ap_off, st));
-  // a1 + a2: RMSNorm(x[idx_in]) -> QKV projection of the changed rows
-  KL(GATHER, launch_gather_rmsnorm(Hprev, idx_in, M_in, rows, L.g_attn, m.rms_eps, c->Xn, d, st));
-  KL(QKV_GEMM, RET(gemm(ctx, M_in, rows, qw + 2 * kw, d, c->Xn, L.wqkv, c->qkv, qw + 2 * kw, EPI_BF16)));
-  // a3: RoPE, dV (before overwrite), in-place K/V/Q cache rows
   // incremental statistics need the overwritten key rows (Kxo) and current
   // statistics; under the literal layer-1 policy, decoded rows outside idx_in get a new Q at
   // layer 0 without a statistics update, so that layer stays dense
   const bool inc = fused && g_attn_inc_enabled && C.st_ok && !(l == 0 && c->r.layer1_policy == 0);
-  KL(QKV_POST, launch_qkv_post(c->qkv, idx_in, M_in, rows, L.bqkv, N, m.n_heads, m.n_kv_heads, m.head_dim,
-                               c->rope_cs, C.Q, C.K, C.V, c->dV, c->Qx, c->Kx, inc ? c->Kxo : nullptr,
-                               fused ? c->rowflag : nullptr, tag, st, 0, fused ? C.Kfi : nullptr, C.dtag, C.epoch));
+  bf16 *Kfi = fused ? C.Kfi : nullptr;
+  // (option, default off) the fused epilogue pays where the projection runs several tiles per SM
+  // pair (full-input steps, the FullStep): there its a3 work overlaps the next tiles' main loops.
+  // In response-only steps each pair holds one tile, the epilogue is exposed, and a3 spread over
+  // every SM as its own kernel is faster (ncu launch lists: QKV + a3 53.1 + 14.0 us unfused vs
+  // 79.6 us fused at response-only size; 110.4 + 32.6 vs 128.9 us full-input)
+  if (qkv_fusable(c) && row_lo < c->r.L_P) {
+    // a1 (+ a3's row bookkeeping: exact-row tag, first write in the statistics epoch), then a2 + a3
+    // in the projection's epilogue: RoPE, dV (before the overwrite), in-place K / V / Q cache rows
+    RowMark mk;
+    mk.rowflag = fused ? c->rowflag : nullptr;
+    mk.tag = tag;
+    if (Kfi) {
+      mk.dtag = C.dtag;
+      mk.epoch = C.epoch;
+      mk.snap = c->snapm;
+    }
+    KL(GATHER, launch_gather_rmsnorm(Hprev, idx_in, M_in, rows, L.g_attn, m.rms_eps, c->Xn, d, st, mk));
+    QkvEpi q;
+    q.idx = idx_in;
+    q.N = N;
+    q.H = m.n_heads;
+    q.KVH = m.n_kv_heads;
+    q.rope_cs = c->rope_cs;
+    q.Qc = C.Q;
+    q.Kc = C.K;
+    q.Vc = C.V;
+    q.dV = c->dV;
+    q.Qx = c->Qx;
+    q.Kx = c->Kx;
+    q.Kxo = inc ? c->Kxo : nullptr;
+    q.Kfi = Kfi;
+    q.snap = c->snapm;
+    KL(QKV_GEMM, RET(gemm_qkv(ctx, c, M_in, c->Xn, L.wqkv, L.bqkv, q)));
+  } else {
+    // a1 + a2: RMSNorm(x[idx_in]) -> QKV projection of the changed rows
+    KL(GATHER, launch_gather_rmsnorm(Hprev, idx_in, M_in, rows, L.g_attn, m.rms_eps, c->Xn, d, st));
+    KL(QKV_GEMM, RET(gemm(ctx, M_in, rows, qw + 2 * kw, d, c->Xn, L.wqkv, c->qkv, qw + 2 * kw, EPI_BF16)));
+    // a3: RoPE, dV (before overwrite), in-place K/V/Q cache rows
+    KL(QKV_POST, launch_qkv_post(c->qkv, idx_in, M_in, rows, L.bqkv, N, m.n_heads, m.n_kv_heads, m.head_dim,
+                                 c->rope_cs, C.Q, C.K, C.V, c->dV, c->Qx, c->Kx, inc ? c->Kxo : nullptr,
+                                 fused ? c->rowflag : nullptr, tag, st, 0, Kfi, C.dtag, C.epoch));
+  }
   // full-input step with current prompt statistics: the keys changed since they were current
   const bool full_in = row_lo < c->r.L_P;
   const bool pinc = fused && full_in && g_attn_inc_enabled && g_attn_pinc_enabled && C.pst_ok;
@@ -1568,6 +1645,11 @@ int dyllm_set_option(int option, int value) {
   if (option == DYLLM_OPT_SKINNY_KROT) {
     const int prev = g_skinny_krot;
     g_skinny_krot = value < 0 ? 0 : value;
+    return prev;
+  }
+  if (option == DYLLM_OPT_QKV_FUSED) {
+    const int prev = g_qkv_fused ? 1 : 0;
+    g_qkv_fused = value != 0;
     return prev;
   }
   if (option == DYLLM_OPT_ATTN_COS) {

@@ -382,6 +382,10 @@ int gemm_launch(const GemmCall &g, int num_sms, cudaStream_t st) {
   }
   // Row counts <= kSkinnyMaxM (16384) go to the 2-CTA weight-stationary kernel. With a device-resident
   // count both kernels are enqueued and each exits unless the count is in its regime.
+  if (g.epi == EPI_QKV && !(g_skinny_enabled && skinny_eligible(g) && g.M_cap <= kSkinnyMaxM)) {
+    set_error("gemm: the fused QKV epilogue needs the skinny kernel (rows <= 16384, N % 256 == 0)");
+    return DYLLM_E_ARG;
+  }
   GemmCall s = g;
   if (g_skinny_enabled && skinny_eligible(g)) {
     // every row count up to 16384, the FullStep's included: the CTA-pair 256-row weight tiles move

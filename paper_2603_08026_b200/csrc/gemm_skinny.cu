@@ -50,6 +50,10 @@ constexpr int SK_SMEM = 1024 + SK_RING + SK_XCH + 256;
 constexpr int SK_THREADS = 352;              // W producer, MMA, 8 epilogue warps, A producer
 constexpr int SKINNY_MAX_M = kSkinnyMaxM;
 constexpr int kSkPrefetch = 12;   // k-blocks of weight L2 prefetch ahead of the ring
+#ifndef DYLLM_QKV_ROWS
+#define DYLLM_QKV_ROWS 1
+#endif
+constexpr int kQkvRows = DYLLM_QKV_ROWS;  // EPI_QKV: rows whose loads are issued together
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
@@ -126,6 +130,7 @@ struct SkinnyParams {
   int krot;           // k-block start offset per weight block (x block index, mod the segment's k-blocks)
   int dbg;            // measurement hook: bit 0 skips the operand TMA loads, bit 1 the MMAs, bit 2 the
                       // epilogue's global stores, bit 3 its shared-memory transpose
+  QkvEpi qkv;         // EPI_QKV (a2 + a3 fused)
 };
 
 // Stream-K partition of the (item, k-block) space: pair p owns units [start(p), start(p+1)).
@@ -527,6 +532,97 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         }
       }
     };
+    // EPI_QKV (SURVEY §8 a2 + a3; the a3 kernel qkv_post in kernels.cu does the same from a bf16
+    // QKV row): this CTA's 128 weight rows are one head — query head, key head or value head. The
+    // thread's 4 rows x 8 head dims of the chunk come from the transposed tile with the bias added;
+    // query and key heads are rotated at the row's global position (rotate-half, D10: dims d and
+    // d + 64 pair, the partner dims read from the same tile); key rows keep the key they overwrite
+    // (Kxo, and Kfi on the row's first write in its statistics epoch); value rows leave
+    // dV = V_new - V_cache (read before the overwrite). Loads of two rows, then their stores.
+    auto store_qkv = [&](const float4 *x4, int m0, int tile, const int orow[4]) {
+      const QkvEpi &q = p.qkv;
+      const int item = tile / nchunk;
+      m0 += tile % nchunk * R;
+      const int hid = item * 2 + static_cast<int>(rank);
+      const int kind = hid < q.H ? 0 : hid < q.H + q.KVH ? 1 : 2;  // query / key / value head
+      const int hk = kind == 0 ? hid : kind == 1 ? hid - q.H : hid - q.H - q.KVH;
+      const int n = 8 * n4, pn = n ^ 64, k0 = n & 63;
+      const int wid = (kind == 0 ? q.H : q.KVH) * 128;
+      bf16 *__restrict__ cache = kind == 0 ? q.Qc : kind == 1 ? q.Kc : q.Vc;
+      bf16 *__restrict__ compact = kind == 0 ? q.Qx : kind == 1 ? q.Kx : nullptr;
+      const bool keep_old = kind == 1 && (q.Kxo || q.Kfi);
+      float bb[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, bp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (p.bias) {
+        const int gc = item * 256 + static_cast<int>(rank) * 128;
+        unpack8(*reinterpret_cast<const uint4 *>(p.bias + gc + n), bb);
+        if (kind < 2) unpack8(*reinterpret_cast<const uint4 *>(p.bias + gc + pn), bp);
+      }
+#pragma unroll
+      for (int kp = 0; kp < 4; kp += kQkvRows) {
+        float4 cs[kQkvRows][4];
+        uint4 old[kQkvRows];
+        bool snap[kQkvRows];
+#pragma unroll
+        for (int u = 0; u < kQkvRows; ++u) {
+          const int k = kp + u;
+          const int m = m0 + msub + 8 * k;
+          snap[u] = false;
+          old[u] = make_uint4(0u, 0u, 0u, 0u);
+          if (m < M) {
+            const int64_t rid = orow[k];
+            if (kind < 2) {
+              const float4 *c4 = reinterpret_cast<const float4 *>(q.rope_cs + (rid % q.N) * 64 + k0);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) cs[u][j] = __ldg(c4 + j);
+            }
+            if (kind != 0 && (kind == 2 ? q.dV != nullptr : keep_old))
+              old[u] = *reinterpret_cast<const uint4 *>(cache + rid * wid + hk * 128 + n);
+            if (kind == 1 && q.Kfi) snap[u] = q.snap[m] != 0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kQkvRows; ++u) {
+          const int k = kp + u;
+          const int m = m0 + msub + 8 * k;
+          if (m >= M) continue;
+          const int64_t rid = orow[k];
+          const int xr = (msub + 8 * k) * 32;  // the row within the chunk's transposed tile
+          const float4 a = x4[xr + n / 4], b = x4[xr + n / 4 + 1];
+          float v[8] = {a.x + bb[0], a.y + bb[1], a.z + bb[2], a.w + bb[3], b.x + bb[4], b.y + bb[5], b.z + bb[6],
+                        b.w + bb[7]};
+          bf16 *dst = cache + rid * wid + hk * 128 + n;
+          if (kind < 2) {
+            const float4 pa = x4[xr + pn / 4], pb = x4[xr + pn / 4 + 1];
+            const float w[8] = {pa.x + bp[0], pa.y + bp[1], pa.z + bp[2], pa.w + bp[3],
+                                pb.x + bp[4], pb.y + bp[5], pb.z + bp[6], pb.w + bp[7]};
+            const float *cf = reinterpret_cast<const float *>(cs[u]);
+            float y[8];
+            // dims d < 64: x_d cos - x_(d+64) sin; dims d >= 64: x_d cos + x_(d-64) sin
+#pragma unroll
+            for (int j = 0; j < 8; ++j) y[j] = n < 64 ? v[j] * cf[2 * j] - w[j] * cf[2 * j + 1]
+                                                      : v[j] * cf[2 * j] + w[j] * cf[2 * j + 1];
+            const uint4 yb = pack8(y);
+            if (kind == 1) {
+              if (q.Kxo) *reinterpret_cast<uint4 *>(q.Kxo + static_cast<int64_t>(m) * wid + hk * 128 + n) = old[u];
+              if (snap[u]) *reinterpret_cast<uint4 *>(q.Kfi + rid * wid + hk * 128 + n) = old[u];
+            }
+            *reinterpret_cast<uint4 *>(dst) = yb;
+            if (compact) *reinterpret_cast<uint4 *>(compact + static_cast<int64_t>(m) * wid + hk * 128 + n) = yb;
+          } else {
+            const uint4 vb = pack8(v);
+            if (q.dV) {
+              float vn[8], vo[8], dd[8];
+              unpack8(vb, vn);
+              unpack8(old[u], vo);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) dd[j] = vn[j] - vo[j];
+              *reinterpret_cast<uint4 *>(q.dV + static_cast<int64_t>(m) * wid + hk * 128 + n) = pack8(dd);
+            }
+            *reinterpret_cast<uint4 *>(dst) = vb;
+          }
+        }
+      }
+    };
     // transpose one chunk (thread = weight row `row`, v = its 32 output rows m0..m0+31) through
     // this half's tile and store it. The leading barrier also orders the previous chunk's tile
     // reads before this chunk's writes.
@@ -537,7 +633,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         float4 r[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) r[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        if (!(p.dbg & 4)) store(r, m0, item, orow, rrow);
+        if (!(p.dbg & 4) && EPI != EPI_QKV) store(r, m0, item, orow, rrow);
         return;
       }
       named_bar_sync(1 + half, 128);
@@ -545,6 +641,10 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       for (int j = 0; j < 32; ++j) x[j * 128 + row] = v[j];
       named_bar_sync(1 + half, 128);
       const float4 *x4 = reinterpret_cast<const float4 *>(x);
+      if constexpr (EPI == EPI_QKV) {
+        if (!(p.dbg & 4)) store_qkv(x4, m0, item, orow);
+        return;
+      }
       float4 r[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) r[i] = x4[sl_m(i) * 32 + sl_n(i) / 4];
@@ -741,7 +841,8 @@ static int launch_skinny_t(const GemmCall &g, int num_sms, cudaStream_t st) {
   SkinnyParams p{g.M_ptr, g.M_cap, g.N, g.K, g.D, g.ldd, g.resid, g.ldr, g.resid_rows, g.bias, g.out_rows, g.ws, g.ctr,
                  max_pairs,
                  g_skinny_trace, g_skinny_split, g_skinny_one_chunk > 0 ? g_skinny_one_chunk : -1, g_skinny_chunk_rows,
-                 g_skinny_krot, g_skinny_dbg};
+                 g_skinny_krot, g_skinny_dbg, g.qkv};
+  if (EPI == EPI_QKV) p.out_rows = g.qkv.idx;  // the epilogue's row ids (loaded ahead of the chunk's transpose)
   DY_CUDA(launch_k(kern, dim3(2 * max_pairs), dim3(SK_THREADS), SK_SMEM, st, 2, maps, p));
   return DYLLM_OK;
 }
@@ -757,12 +858,13 @@ int g_skinny_kb = 0;  // k-block width: 0 / 128 (default) or 64
 bool skinny_eligible(const GemmCall &g) {
   // the epilogue stores 16-byte row segments (8 output columns) and reads bias / residual alike
   const auto a16 = [](const void *q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-  return g.N % 256 == 0 && g.K % SK_KB == 0 && (g.epi == EPI_BF16 || g.epi == EPI_RESID || g.epi == EPI_SWIGLU) &&
+  return g.N % 256 == 0 && g.K % SK_KB == 0 &&
+         (g.epi == EPI_BF16 || g.epi == EPI_RESID || g.epi == EPI_SWIGLU || g.epi == EPI_QKV) &&
          g.ldd % 8 == 0 && a16(g.D) && (!g.resid || (g.ldr % 8 == 0 && a16(g.resid))) && (!g.bias || a16(g.bias));
 }
 
 int gemm_skinny_launch(const GemmCall &g, int num_sms, cudaStream_t st) {
-  if (g_skinny_kb == 64) {
+  if (g_skinny_kb == 64 && g.epi != EPI_QKV) {
     switch (g.epi) {
       case EPI_SWIGLU: return launch_skinny_t<EPI_SWIGLU, 1>(g, num_sms, st);
       case EPI_RESID: return launch_skinny_t<EPI_RESID, 1>(g, num_sms, st);
@@ -772,6 +874,7 @@ int gemm_skinny_launch(const GemmCall &g, int num_sms, cudaStream_t st) {
   switch (g.epi) {
     case EPI_SWIGLU: return launch_skinny_t<EPI_SWIGLU, 2>(g, num_sms, st);
     case EPI_RESID: return launch_skinny_t<EPI_RESID, 2>(g, num_sms, st);
+    case EPI_QKV: return launch_skinny_t<EPI_QKV, 2>(g, num_sms, st);
     default: return launch_skinny_t<EPI_BF16, 2>(g, num_sms, st);
   }
 }

@@ -63,7 +63,21 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 #define DY_CUDA_LAUNCH(expr) static_cast<void>(expr)
 
 // ------------------------------------------------------------------ GEMM (gemm.cu)
-enum Epi { EPI_BF16 = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_LMHEAD = 3 };
+enum Epi { EPI_BF16 = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_LMHEAD = 3, EPI_QKV = 4 };
+// EPI_QKV (skinny kernel, head_dim 128): the QKV projection's epilogue does a3 itself (SURVEY §8
+// rows a2 + a3: RoPE at global positions, bias, dV before the overwrite, in-place Q / K / V cache
+// rows, the compact copies the attention reads); each CTA's 128 weight rows are one head
+struct QkvEpi {
+  const int *idx = nullptr;     // row id of each output row (nullable: identity, the FullStep)
+  int N = 0, H = 0, KVH = 0;    // sequence length (position = row id % N), query / kv heads
+  const float2 *rope_cs = nullptr;  // [N][64] (cos, sin)
+  bf16 *Qc = nullptr, *Kc = nullptr, *Vc = nullptr;  // caches [rows][H * 128] / [rows][KVH * 128]
+  bf16 *dV = nullptr;           // nullable [M][KVH * 128]: V_new - V_cache (compact)
+  bf16 *Qx = nullptr, *Kx = nullptr;  // nullable compact copies of the new Q / K rows
+  bf16 *Kxo = nullptr;          // nullable compact copy of the overwritten K rows
+  bf16 *Kfi = nullptr;          // nullable: overwritten K rows kept at their row id where snap[m]
+  const uint8_t *snap = nullptr;  // [M] first write of the row in its statistics epoch (a1, RowMark)
+};
 // gate/up rows of W_gu are interleaved in blocks of kGuIl rows ([gate x64][up x64] ...), so a
 // 128-row weight tile holds the gate and up rows of the same 64 FFN channels.
 constexpr int kGuIl = 64;
@@ -88,6 +102,7 @@ struct GemmCall {
   int excl_col = -1;  // EPI_LMHEAD: column excluded from the max / argmax (the mask token, D22)
   float *ws = nullptr;  // skinny split-K workspace (skinny_ws_floats(num_sms) floats per ctx)
   int *ctr = nullptr;   // skinny split-K counters (kSkinnyCtrCap, zero between launches)
+  QkvEpi qkv;           // EPI_QKV
 };
 int gemm_launch(const GemmCall &g, int num_sms, cudaStream_t st);
 // 2D bf16 tensor map [rows][K] (K contiguous), box {64, box_rows}, SWIZZLE_128B

@@ -31,7 +31,7 @@ __global__ void embed_rows_kernel(const int *__restrict__ tokens, const int *__r
 // dst[i] = RMSNorm(src[idx[i]]) * g  (D3), one warp per row, fp32 statistics.
 __global__ void gather_rmsnorm_kernel(const bf16 *__restrict__ src, const int *__restrict__ idx,
                                       const int *__restrict__ M_ptr, int M_cap, const bf16 *__restrict__ g,
-                                      float eps, bf16 *__restrict__ dst, int d) {
+                                      float eps, bf16 *__restrict__ dst, int d, RowMark mk) {
   pdl_wait();
   const int M = M_ptr ? *M_ptr : M_cap;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
@@ -39,6 +39,16 @@ __global__ void gather_rmsnorm_kernel(const bf16 *__restrict__ src, const int *_
   constexpr int VMAX = 16;  // rows up to 4096 wide stay in registers (16 x 16 B per lane)
   for (int i = warp; i < M; i += gridDim.x * blockDim.x / 32) {
     const int r = idx ? idx[i] : i;
+    // a3's row bookkeeping when the QKV GEMM epilogue does a3 (EPI_QKV): the row is an exact row of
+    // this layer step, and whether its key is written for the first time in the statistics epoch
+    // (the epilogue then keeps the overwritten key in Kfi) is decided here, once per row
+    if (lane == 0) {
+      if (mk.rowflag) mk.rowflag[r] = mk.tag;
+      if (mk.snap) {
+        mk.snap[i] = mk.dtag[r] != mk.epoch;
+        mk.dtag[r] = mk.epoch;
+      }
+    }
     const uint4 *s = reinterpret_cast<const uint4 *>(src + static_cast<int64_t>(r) * d);
     uint4 *o = reinterpret_cast<uint4 *>(dst + static_cast<int64_t>(i) * d);
     const uint4 *gv = reinterpret_cast<const uint4 *>(g);
@@ -976,8 +986,8 @@ void launch_embed_rows(const int *tokens, const int *rows, const int *M_ptr, int
   DY_CUDA_LAUNCH(launch_k(embed_rows_kernel, dim3(grid_for(M_cap, 8)), dim3(256), 0, st, 1, tokens, rows, M_ptr, M_cap, emb, H0, d));
 }
 void launch_gather_rmsnorm(const bf16 *src, const int *idx, const int *M_ptr, int M_cap, const bf16 *g, float eps,
-                           bf16 *dst, int d, cudaStream_t st) {
-  DY_CUDA_LAUNCH(launch_k(gather_rmsnorm_kernel, dim3(grid_for(M_cap, 4, 148 * 4)), dim3(128), 0, st, 1, src, idx, M_ptr, M_cap, g, eps, dst, d));
+                           bf16 *dst, int d, cudaStream_t st, RowMark mk) {
+  DY_CUDA_LAUNCH(launch_k(gather_rmsnorm_kernel, dim3(grid_for(M_cap, 4, 148 * 4)), dim3(128), 0, st, 1, src, idx, M_ptr, M_cap, g, eps, dst, d, mk));
 }
 void launch_gather_rows(const bf16 *src, const int *idx, const int *M_ptr, int M_cap, bf16 *dst, int width,
                         cudaStream_t st) {
@@ -989,7 +999,7 @@ void launch_scatter_rows(const bf16 *src, const int *idx, const int *M_ptr, int 
 }
 void launch_rmsnorm_rows(const bf16 *src, const int *M_ptr, int M_cap, const bf16 *g, float eps, bf16 *dst, int d,
                          cudaStream_t st) {
-  DY_CUDA_LAUNCH(launch_k(gather_rmsnorm_kernel, dim3(grid_for(M_cap, 4, 148 * 4)), dim3(128), 0, st, 1, src, nullptr, M_ptr, M_cap, g, eps, dst, d));
+  DY_CUDA_LAUNCH(launch_k(gather_rmsnorm_kernel, dim3(grid_for(M_cap, 4, 148 * 4)), dim3(128), 0, st, 1, src, nullptr, M_ptr, M_cap, g, eps, dst, d, RowMark{}));
 }
 void launch_qkv_post(const bf16 *qkv, const int *idx, const int *M_ptr, int M_cap, const bf16 *bias, int N, int H,
                      int KVH, int hd, const float2 *rope_cs, bf16 *Qc, bf16 *Kc, bf16 *Vc, bf16 *dV, bf16 *Qx,

@@ -9,8 +9,17 @@ typedef __nv_bfloat16 bf16;
 namespace dy {
 void launch_embed_rows(const int *tokens, const int *rows, const int *M_ptr, int M_cap, const bf16 *emb, bf16 *H0,
                        int d, cudaStream_t st);
+// optional row bookkeeping of a1 for the fused a2+a3 epilogue (EPI_QKV): rowflag[r] = tag, and, with
+// snap set, snap[i] = (dtag[r] != epoch) then dtag[r] = epoch (statistics epochs, D21)
+struct RowMark {
+  uint32_t *rowflag = nullptr;
+  uint32_t tag = 0;
+  uint32_t *dtag = nullptr;
+  uint32_t epoch = 0;
+  uint8_t *snap = nullptr;
+};
 void launch_gather_rmsnorm(const bf16 *src, const int *idx, const int *M_ptr, int M_cap, const bf16 *g, float eps,
-                           bf16 *dst, int d, cudaStream_t st);
+                           bf16 *dst, int d, cudaStream_t st, RowMark mk = RowMark{});
 void launch_gather_rows(const bf16 *src, const int *idx, const int *M_ptr, int M_cap, bf16 *dst, int width,
                         cudaStream_t st);
 void launch_scatter_rows(const bf16 *src, const int *idx, const int *M_ptr, int M_cap, bf16 *dst, int width,

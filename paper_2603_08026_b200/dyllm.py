@@ -111,6 +111,7 @@ def lib():
 
 OPT_SKINNY_GEMM, OPT_SKINNY_SPLIT, OPT_ATTN_FUSED, OPT_SKINNY_ONE_CHUNK, OPT_PDL, OPT_ATTN_INC, OPT_ATTN_T4 = 1, 2, 3, 4, 5, 6, 7
 OPT_ATTN_PINC, OPT_ATTN_COS, OPT_SKINNY_CHUNK, OPT_SKINNY_KROT, OPT_SKINNY_DEBUG, OPT_SKINNY_KB = 8, 9, 10, 11, 12, 13
+OPT_QKV_FUSED = 14
 
 
 def set_option(option: int, value: int) -> int:
