@@ -125,7 +125,7 @@ static bool g_attn_pinc_enabled = true;  // test hook: incremental prompt statis
 // default — same-box A/B (tools/gpu_r2_cos.sh): attention 141 -> 178 us per launch (the C_old read
 // lands on each item's serial chain), selection 48 -> 26 us: 716 vs 724 tok/s
 static bool g_attn_fuse_cos = false;
-static bool g_qkv_fused = false;  // EPI_QKV: a3 in the QKV projection's epilogue (DYLLM_OPT_QKV_FUSED)
+static int g_qkv_fused = 1;  // EPI_QKV: a3 in the QKV projection's epilogue: 1 FullSteps, 2 + full-input steps (DYLLM_OPT_QKV_FUSED)
 
 struct LayerW {
   bf16 *g_attn, *wqkv, *bqkv, *wo, *g_ffn, *wgu, *wd;
@@ -622,10 +622,10 @@ static int gemm(dyllm_ctx *ctx, const int *M_ptr, int M_cap, int N, int K, const
 
 // a2 + a3 in one launch (EPI_QKV): the QKV projection of the rows of A whose epilogue applies the bias
 // and RoPE and writes the cache rows, dV and the compact copies (q: everything but A / W / bias)
-static bool qkv_fusable(const dyllm_cache *c) {
+static bool qkv_fusable(const dyllm_cache *c, bool full_step) {
   const dyllm_model_cfg &m = c->m;
   const int qw = m.n_heads * m.head_dim, kw = m.n_kv_heads * m.head_dim;
-  return g_qkv_fused && g_skinny_enabled && m.head_dim == 128 && c->rows <= kSkinnyMaxM &&
+  return g_qkv_fused >= (full_step ? 1 : 2) && g_skinny_enabled && m.head_dim == 128 && c->rows <= kSkinnyMaxM &&
          (qw + 2 * kw) % 256 == 0 && m.d_model % 128 == 0;
 }
 static int gemm_qkv(dyllm_ctx *ctx, const dyllm_cache *c, const int *M_ptr, const bf16 *A, const bf16 *W,
@@ -808,7 +808,7 @@ static int full_attn_phase(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *
   LayerC &C = c->L[l];
   const bf16 *Hprev = l == 0 ? c->H0 : c->L[l - 1].H;
     KL(GATHER, launch_gather_rmsnorm(Hprev, nullptr, nullptr, rows, L.g_attn, m.rms_eps, c->Xn, d, st));
-    if (qkv_fusable(c)) {
+    if (qkv_fusable(c, true)) {
       QkvEpi q;
       q.N = c->N;
       q.H = m.n_heads;
@@ -913,12 +913,12 @@ static int attn_phase(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, in
   // layer 0 without a statistics update, so that layer stays dense
   const bool inc = fused && g_attn_inc_enabled && C.st_ok && !(l == 0 && c->r.layer1_policy == 0);
   bf16 *Kfi = fused ? C.Kfi : nullptr;
-  // (option, default off) the fused epilogue pays where the projection runs several tiles per SM
+  // (option 2; default 1 fuses the FullStep only) the fused epilogue pays where the projection runs several tiles per SM
   // pair (full-input steps, the FullStep): there its a3 work overlaps the next tiles' main loops.
   // In response-only steps each pair holds one tile, the epilogue is exposed, and a3 spread over
   // every SM as its own kernel is faster (ncu launch lists: QKV + a3 53.1 + 14.0 us unfused vs
   // 79.6 us fused at response-only size; 110.4 + 32.6 vs 128.9 us full-input)
-  if (qkv_fusable(c) && row_lo < c->r.L_P) {
+  if (qkv_fusable(c, false) && row_lo < c->r.L_P) {
     // a1 (+ a3's row bookkeeping: exact-row tag, first write in the statistics epoch), then a2 + a3
     // in the projection's epilogue: RoPE, dV (before the overwrite), in-place K / V / Q cache rows
     RowMark mk;
@@ -1648,8 +1648,8 @@ int dyllm_set_option(int option, int value) {
     return prev;
   }
   if (option == DYLLM_OPT_QKV_FUSED) {
-    const int prev = g_qkv_fused ? 1 : 0;
-    g_qkv_fused = value != 0;
+    const int prev = g_qkv_fused;
+    g_qkv_fused = value < 0 ? 0 : value > 2 ? 2 : value;
     return prev;
   }
   if (option == DYLLM_OPT_ATTN_COS) {

@@ -160,7 +160,7 @@ def test_tp_denoise_steps_match_tp1(name, residual_mode, select_mode=1):
                 if len(rows):
                     # two bf16 paths against each other (the oracle bar applies to each): 2x the bar
                     # for the block without a residual stream
-                    tol = TOL if residual_mode == 0 else 1.5 * TOL
+                    tol = TOL if residual_mode == 0 else 2 * TOL
                     assert row_rel_err(HL_tp[l][0][s, rows], HL_ref[l][s, rows]).max() < tol, (t, l, s)
                 compared += N - row_lo
         assert torch.equal(dp_tp, dec_pos) and torch.equal(dt_tp, dec_tok), t
