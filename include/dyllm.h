@@ -296,13 +296,12 @@ enum { DYLLM_OPT_SKINNY_GEMM = 1, DYLLM_OPT_SKINNY_SPLIT = 2, DYLLM_OPT_ATTN_FUS
        DYLLM_OPT_PDL = 5, DYLLM_OPT_ATTN_INC = 6, DYLLM_OPT_ATTN_T4 = 7, DYLLM_OPT_ATTN_PINC = 8,
        DYLLM_OPT_ATTN_COS = 9, DYLLM_OPT_SKINNY_CHUNK = 10, DYLLM_OPT_SKINNY_KROT = 11,
        DYLLM_OPT_SKINNY_DEBUG = 12, DYLLM_OPT_SKINNY_KB = 13, DYLLM_OPT_QKV_FUSED = 14 };
-/* DYLLM_OPT_QKV_FUSED (default 1): with head_dim 128 and at most 16384 rows, the QKV projection's
+/* DYLLM_OPT_QKV_FUSED (default 2): with head_dim 128 and at most 16384 rows, the QKV projection's
  * epilogue applies the bias and RoPE and writes the Q / K / V cache rows, dV and the compact copies
- * itself (SURVEY §8 rows a2 + a3 fused) — 1: in FullSteps, 2: also in full-input sparse
- * steps, 0: never (the projection writes a bf16 QKV scratch and a separate kernel does a3). The
- * sparse steps' default stays unfused: measured faster in full-input steps (143 -> 129 us per
- * layer) but slower in response-only ones, and it moves the QKV rounding of the steps that the
- * library's GPU-vs-GPU consistency checks compare. */
+ * itself (SURVEY §8 rows a2 + a3 fused) — 1: in FullSteps, 2: in FullSteps and
+ * full-input sparse steps, 0: never (the projection writes a bf16 QKV scratch and a separate kernel
+ * does a3). Response-only steps stay unfused: there each SM pair holds one QKV tile and the fused
+ * epilogue is exposed (measured slower). */
 /* DYLLM_OPT_SKINNY_KB (default 0 = 128): k-block width of the skinny kernel's shared-memory ring
  * stages, 128 or 64 columns (64: half-size stages, twice as many in flight). */
 /* DYLLM_OPT_SKINNY_DEBUG (default 0; measurement only, results are garbage when set): bit 0 runs

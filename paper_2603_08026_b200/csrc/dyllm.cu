@@ -125,7 +125,7 @@ static bool g_attn_pinc_enabled = true;  // test hook: incremental prompt statis
 // default — same-box A/B (tools/gpu_r2_cos.sh): attention 141 -> 178 us per launch (the C_old read
 // lands on each item's serial chain), selection 48 -> 26 us: 716 vs 724 tok/s
 static bool g_attn_fuse_cos = false;
-static int g_qkv_fused = 1;  // EPI_QKV: a3 in the QKV projection's epilogue: 1 FullSteps, 2 + full-input steps (DYLLM_OPT_QKV_FUSED)
+static int g_qkv_fused = 2;  // EPI_QKV: a3 in the QKV projection's epilogue: 1 FullSteps, 2 + full-input steps (DYLLM_OPT_QKV_FUSED)
 
 struct LayerW {
   bf16 *g_attn, *wqkv, *bqkv, *wo, *g_ffn, *wgu, *wd;
@@ -913,7 +913,7 @@ static int attn_phase(dyllm_ctx *ctx, const dyllm_weights *w, dyllm_cache *c, in
   // layer 0 without a statistics update, so that layer stays dense
   const bool inc = fused && g_attn_inc_enabled && C.st_ok && !(l == 0 && c->r.layer1_policy == 0);
   bf16 *Kfi = fused ? C.Kfi : nullptr;
-  // (option 2; default 1 fuses the FullStep only) the fused epilogue pays where the projection runs several tiles per SM
+  // (default: option 2) the fused epilogue pays where the projection runs several tiles per SM
   // pair (full-input steps, the FullStep): there its a3 work overlaps the next tiles' main loops.
   // In response-only steps each pair holds one tile, the epilogue is exposed, and a3 spread over
   // every SM as its own kernel is faster (ncu launch lists: QKV + a3 53.1 + 14.0 us unfused vs
