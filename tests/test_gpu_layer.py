@@ -311,12 +311,12 @@ def test_layer_step_paper_literal_block(mode):
 
 @pytest.mark.parametrize("name", ["small128", "small128_gqa"])
 @pytest.mark.parametrize("mode", ["fi", "ro"])
-def test_layer_step_qkv_fused(name, mode):
-    """a2 + a3 in one launch in a sparse step (DYLLM_OPT_QKV_FUSED = 2: the QKV projection's epilogue
-    applies bias / RoPE, keeps the overwritten keys, writes dV and the cache rows; full-input steps)
-    against the oracle's Alg. 3 layer (FullSteps use the fused path by default)."""
+def test_layer_step_qkv_unfused(name, mode):
+    """a3 as its own kernel in every step kind (DYLLM_OPT_QKV_FUSED = 0: the projection writes a bf16
+    QKV scratch, qkv_post applies bias / RoPE / dV / cache writes) against the oracle's Alg. 3 layer
+    (by default full-input steps and FullSteps run a2 + a3 in the projection's epilogue)."""
     from paper_2603_08026_b200 import dyllm as dy
-    prev = dy.set_option(dy.OPT_QKV_FUSED, 2)
+    prev = dy.set_option(dy.OPT_QKV_FUSED, 0)
     try:
         _teacher_forced_layer(name, 1, mode)
     finally:
